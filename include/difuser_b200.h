@@ -1,0 +1,136 @@
+/*
+ * difuser_b200.h — C-ABI of the B200-native sketch-IM hot path
+ * (DiFuseR, arxiv 2410.14047).  Drop-in boundary for the reference's
+ * `difuser::run` (proj/include/difuser/runtime.hpp:56) and its Python binding
+ * `_difuser.run_json` (proj/bindings/pymodule.cpp:75-90).
+ *
+ * Conventions:
+ *  - every entry point returns an int status (0 = ok) and never throws;
+ *    dfs_last_error() returns the thread-local message of the last failure;
+ *    status classes mirror the reference's exceptions: DFS_EINVAL =
+ *    std::invalid_argument (ValueError), DFS_ERUNTIME = std::runtime_error
+ *    (RuntimeError), DFS_ECUDA = CUDA failure, DFS_ENOMEM, DFS_EINDEX;
+ *  - plain pointers and sizes only; host pointers are caller-owned and only
+ *    read during the call; library-allocated outputs are released with
+ *    dfs_free();
+ *  - a context is bound to one CUDA device and is not re-entrant; distinct
+ *    contexts may run concurrently.  There is no CPU fallback: without a GPU
+ *    dfs_ctx_create fails with DFS_ECUDA.
+ */
+#ifndef DIFUSER_B200_H
+#define DIFUSER_B200_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DFS_OK 0
+#define DFS_EINVAL 1
+#define DFS_ERUNTIME 2
+#define DFS_ECUDA 3
+#define DFS_ENOMEM 4
+#define DFS_EINDEX 5
+
+typedef struct dfs_graph dfs_graph; /* host WeightedGraph (graph.hpp:44-58) */
+typedef struct dfs_ctx dfs_ctx;     /* device context (one GPU)            */
+
+/* RunConfig (proj/include/difuser/runtime.hpp:13-22) + pybind kwargs
+ * (proj/bindings/pymodule.cpp:86-89).  mode: "fasst" | "naive";
+ * weights: "const:p" | "wc" | "normal:m,s" | "uniform:lo,hi". */
+typedef struct dfs_config {
+  uint32_t k;
+  uint32_t r;
+  uint32_t devices; /* mu: sample-space partitions (FASST devices) */
+  const char *mode;
+  const char *weights;
+  double rebuild_eps;
+  uint64_t seed;
+  int32_t sim_cap; /* default 256 (runtime.hpp:21) */
+  int32_t jacobi;  /* 0: in-place async schedule; 1: the reference's Jacobi schedule */
+} dfs_config;
+
+/* Phase timings (runtime.hpp:24-27) plus instrumentation of the last run. */
+typedef struct dfs_stats {
+  double build, fill, simulate, select, cascade, total, upload;
+  uint64_t sketch_edge_updates; /* live (item, sim) pairs merged by simulate */
+  uint64_t items_processed;
+  uint64_t sweeps_total;
+  uint64_t items_fwd, items_rev;
+} dfs_stats;
+
+const char *dfs_last_error(void);
+int dfs_version(void);
+void dfs_free(void *p);
+
+/* ---- hash / sampling helpers (hash.hpp:91-93, sampling.hpp:23-39,
+ *      pymodule.cpp:123-133) ------------------------------------------------ */
+uint32_t dfs_edge_hash(uint64_t u, uint64_t v);
+uint32_t dfs_random_value_at(uint64_t seed, uint32_t r);
+int dfs_to_fixed_point(double w, uint32_t *out);
+int dfs_is_sampled(uint32_t x, uint32_t h, double w, int *out);
+
+/* ---- host graph (graph.cpp:41-348; pymodule.cpp:35-73) ------------------- */
+int dfs_graph_from_text(const char *text, size_t len, int directed, dfs_graph **out);
+int dfs_graph_load(const char *path, int directed, dfs_graph **out);
+int dfs_graph_save_cache(const dfs_graph *g, const char *path);
+int dfs_graph_from_csr(uint32_t n, uint64_t m, const uint64_t *offsets, const uint32_t *adj,
+                       const uint64_t *orig_ids /* nullable */, dfs_graph **out);
+/* Deterministic synthetic inputs: kind "rmat" (a = scale) or "er" (a = n). */
+int dfs_graph_generate(const char *kind, uint32_t a, uint64_t m, uint64_t seed, dfs_graph **out);
+void dfs_graph_free(dfs_graph *g);
+uint32_t dfs_graph_n(const dfs_graph *g);
+uint64_t dfs_graph_m(const dfs_graph *g);
+/* Borrowed views valid until dfs_graph_free. */
+int dfs_graph_arrays(const dfs_graph *g, const uint64_t **offsets, const uint32_t **adj,
+                     const uint64_t **orig_ids, const uint32_t **ehash,
+                     const uint32_t **in_degree);
+/* apply_weights (runtime.cpp:15-17) on the host: out has m entries. */
+int dfs_graph_weights(const dfs_graph *g, const char *spec, uint64_t seed, uint32_t *out);
+/* Weight-spec canonical string (WeightSetting::to_string, graph.cpp:228-245). */
+int dfs_weight_string(const char *spec, char **out);
+
+/* ---- device context ------------------------------------------------------ */
+int dfs_ctx_create(int device, dfs_ctx **out);
+void dfs_ctx_destroy(dfs_ctx *ctx);
+/* H2D of the CSR + on-device ehash/in-degree/transpose (resident graph). */
+int dfs_upload(dfs_ctx *ctx, const dfs_graph *g);
+
+/* ---- hot path ------------------------------------------------------------
+ * dfs_run_json: run_json (pymodule.cpp:75-90): uploads g, applies weights,
+ * runs the greedy loop, returns the report JSON (report.cpp:9-41).
+ * dfs_run_resident_json: same on the graph already uploaded by dfs_upload
+ * (g is still needed for randomized normal/uniform weights, else nullable). */
+int dfs_run_json(dfs_ctx *ctx, const dfs_graph *g, const dfs_config *cfg, int timings,
+                 char **json_out);
+int dfs_run_resident_json(dfs_ctx *ctx, const dfs_graph *g, const dfs_config *cfg, int timings,
+                          char **json_out);
+int dfs_last_stats(const dfs_ctx *ctx, dfs_stats *out);
+
+/* ---- stage entry points (parity harness; engine.hpp / fasst.hpp / sketch.hpp)
+ * dfs_prepare = make_plan + apply_weights + build_device_graph for all tau. */
+int dfs_prepare(dfs_ctx *ctx, const dfs_graph *g, const dfs_config *cfg);
+int dfs_plan(const dfs_ctx *ctx, uint32_t *x_sorted, uint32_t *order, int *degraded);
+int dfs_device_graph_size(dfs_ctx *ctx, uint32_t tau, uint64_t *m_tau, uint32_t *words);
+int dfs_device_graph(dfs_ctx *ctx, uint32_t tau, uint64_t *offsets, uint32_t *adj,
+                     uint64_t *mask);
+int dfs_fill(dfs_ctx *ctx, uint32_t tau);                                   /* sketch.cpp:55-66 */
+int dfs_simulate(dfs_ctx *ctx, uint32_t tau, int cap, int jacobi, int *sweeps); /* engine.cpp:88-96 */
+int dfs_scores(dfs_ctx *ctx, uint32_t tau, double *out_n);                  /* sketch.cpp:119-137 */
+int dfs_commit_cascade(dfs_ctx *ctx, uint32_t tau, uint32_t seed, uint64_t *visited); /* engine.cpp:106-144 */
+int dfs_visited_count(dfs_ctx *ctx, uint32_t tau, uint64_t *out);          /* sketch.cpp:139 */
+int dfs_get_registers(dfs_ctx *ctx, uint32_t tau, int8_t *out_nJ);
+int dfs_set_registers(dfs_ctx *ctx, uint32_t tau, const int8_t *in_nJ);
+
+/* ---- verification oracles (oracle.cpp; host, not the hot path) ----------- */
+int dfs_influence(const dfs_graph *g, const uint32_t *seeds, uint32_t nseeds, uint32_t trials,
+                  uint64_t seed, uint32_t runs, const char *weights, double *mean,
+                  double *std_error);
+int dfs_greedy_exact(const dfs_graph *g, uint32_t k, uint32_t trials, uint64_t seed,
+                     const char *weights, uint32_t *out_k);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DIFUSER_B200_H */

@@ -1,0 +1,294 @@
+"""B200-native sketch-based influence maximization (DiFuseR, arxiv 2410.14047).
+
+Drop-in mirror of the reference's Python surface (``difuser`` package,
+proj/python/difuser/__init__.py and proj/bindings/pymodule.cpp): the same
+names, keyword defaults and exception classes, backed by hand-written sm_100a
+kernels behind the C-ABI in ``include/difuser_b200.h``.  There is no CPU
+fallback: without the built library or a GPU the hot-path calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json as _json
+import threading
+
+import numpy as np
+
+from . import _capi
+from ._capi import Config, Stats, check, lib
+
+__all__ = [
+    "Graph", "edge_hash", "graph_from_text", "greedy_exact", "influence", "is_sampled",
+    "load_graph", "random_value_at", "run", "run_json", "save_cache", "generate", "Context",
+]
+
+
+class Graph:
+    """Immutable dense CSR graph (proj/include/difuser/graph.hpp:44-58)."""
+
+    def __init__(self, handle):
+        self._h = C.c_void_p(handle)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _capi._lib is not None:
+            _capi._lib.dfs_graph_free(h)
+            self._h = None
+
+    @property
+    def n(self) -> int:
+        return int(lib().dfs_graph_n(self._h))
+
+    @property
+    def m(self) -> int:
+        return int(lib().dfs_graph_m(self._h))
+
+    def _arrays(self):
+        ps = [C.c_void_p() for _ in range(5)]
+        check(lib().dfs_graph_arrays(self._h, *[C.byref(p) for p in ps]))
+        return ps
+
+    def _view(self, idx, dtype, count):
+        if count == 0:
+            return np.zeros(0, dtype)
+        p = self._arrays()[idx].value
+        buf = (C.c_char * (count * np.dtype(dtype).itemsize)).from_address(p)
+        return np.frombuffer(buf, dtype=dtype, count=count).copy()
+
+    @property
+    def offsets(self) -> np.ndarray:
+        return self._view(0, np.uint64, self.n + 1)
+
+    @property
+    def adj(self) -> np.ndarray:
+        return self._view(1, np.uint32, self.m)
+
+    @property
+    def ehash(self) -> np.ndarray:
+        return self._view(3, np.uint32, self.m)
+
+    @property
+    def in_degree(self) -> np.ndarray:
+        return self._view(4, np.uint32, self.n)
+
+    @property
+    def orig_ids(self):
+        return self._view(2, np.uint64, self.n).tolist()
+
+    def out_degree(self, u: int) -> int:
+        if not (0 <= u < self.n):
+            raise IndexError()
+        off = self._arrays()[0].value
+        a = C.c_uint64.from_address(off + 8 * u).value
+        b = C.c_uint64.from_address(off + 8 * (u + 1)).value
+        return b - a
+
+    def weights(self, spec: str = "const:0.1", seed: int = 0) -> np.ndarray:
+        """apply_weights on the host (runtime.cpp:15-17), fixed point."""
+        out = np.zeros(max(self.m, 1), np.uint32)
+        check(lib().dfs_graph_weights(self._h, spec.encode(), seed, out.ctypes.data))
+        return out[: self.m]
+
+    def __repr__(self):
+        return f"<difuser.Graph n={self.n} m={self.m}>"
+
+
+def _new_graph(fn, *args) -> Graph:
+    h = C.c_void_p()
+    check(fn(*args, C.byref(h)))
+    return Graph(h.value)
+
+
+def load_graph(path: str, directed: bool = True) -> Graph:
+    """Load an edge-list text file or a binary graph cache."""
+    return _new_graph(lib().dfs_graph_load, str(path).encode(), int(directed))
+
+
+def graph_from_text(text: str, directed: bool = True) -> Graph:
+    """Build a graph from edge-list text ("u v [p]" lines)."""
+    b = text.encode()
+    return _new_graph(lib().dfs_graph_from_text, b, len(b), int(directed))
+
+
+def graph_from_csr(offsets, adj, orig_ids=None) -> Graph:
+    offsets = np.ascontiguousarray(offsets, np.uint64)
+    adj = np.ascontiguousarray(adj, np.uint32)
+    oid = None if orig_ids is None else np.ascontiguousarray(orig_ids, np.uint64)
+    return _new_graph(lib().dfs_graph_from_csr, len(offsets) - 1, len(adj), offsets.ctypes.data,
+                      adj.ctypes.data if len(adj) else None,
+                      None if oid is None else oid.ctypes.data)
+
+
+def generate(kind: str, a: int, m: int, seed: int = 0) -> Graph:
+    """Deterministic synthetic graph: kind "rmat" (a = scale) or "er" (a = n)."""
+    return _new_graph(lib().dfs_graph_generate, kind.encode(), a, m, seed)
+
+
+def save_cache(graph: Graph, path: str) -> None:
+    check(lib().dfs_graph_save_cache(graph._h, str(path).encode()))
+
+
+def edge_hash(u: int, v: int) -> int:
+    """31-bit hash of the ordered endpoint pair."""
+    return int(lib().dfs_edge_hash(u, v))
+
+
+def random_value_at(seed: int, r: int) -> int:
+    """Per-simulation 31-bit value at index r."""
+    return int(lib().dfs_random_value_at(seed, r))
+
+
+def is_sampled(x: int, h: int, w: float) -> bool:
+    """Does the simulation owning value x sample an edge with hash h?"""
+    out = C.c_int()
+    check(lib().dfs_is_sampled(x, h, float(w), C.byref(out)))
+    return bool(out.value)
+
+
+def _config(k, r, devices, mode, weights, rebuild_eps, seed, sim_cap=256, jacobi=0):
+    return Config(k, r, devices, mode.encode(), weights.encode(), float(rebuild_eps), seed,
+                  sim_cap, jacobi)
+
+
+class Context:
+    """One CUDA device: resident graph, prepared partitions, stage entry points."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib().dfs_ctx_create(device, C.byref(h)))
+        self._h = h
+        self.device = device
+        self._graph = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _capi._lib is not None:
+            _capi._lib.dfs_ctx_destroy(h)
+            self._h = None
+
+    # ---- hot path
+    def upload(self, graph: Graph):
+        check(lib().dfs_upload(self._h, graph._h))
+        self._graph = graph
+
+    def _take_json(self, p):
+        s = C.cast(p, C.c_char_p).value.decode()
+        lib().dfs_free(p)
+        return s
+
+    def run_json(self, graph, k=10, r=256, devices=1, mode="fasst", weights="const:0.1",
+                 rebuild_eps=0.01, seed=0, timings=True, jacobi=0, resident=False):
+        cfg = _config(k, r, devices, mode, weights, rebuild_eps, seed, jacobi=jacobi)
+        out = C.c_void_p()
+        if resident:
+            check(lib().dfs_run_resident_json(self._h, graph._h if graph is not None else None,
+                                              C.byref(cfg), int(timings), C.byref(out)))
+        else:
+            check(lib().dfs_run_json(self._h, graph._h, C.byref(cfg), int(timings), C.byref(out)))
+        return self._take_json(out)
+
+    def stats(self) -> dict:
+        st = Stats()
+        check(lib().dfs_last_stats(self._h, C.byref(st)))
+        return {f: getattr(st, f) for f, _ in Stats._fields_}
+
+    # ---- stage API (parity harness)
+    def prepare(self, graph, k=1, r=256, devices=1, mode="fasst", weights="const:0.1",
+                rebuild_eps=0.01, seed=0, jacobi=0):
+        self._cfg = dict(k=k, r=r, devices=devices)
+        cfg = _config(k, r, devices, mode, weights, rebuild_eps, seed, jacobi=jacobi)
+        check(lib().dfs_prepare(self._h, graph._h, C.byref(cfg)))
+        self._graph = graph
+        self._J = r // devices
+
+    def plan(self):
+        r = self._cfg["r"]
+        x = np.zeros(r, np.uint32)
+        o = np.zeros(r, np.uint32)
+        d = C.c_int()
+        check(lib().dfs_plan(self._h, x.ctypes.data, o.ctypes.data, C.byref(d)))
+        return x, o, bool(d.value)
+
+    def device_graph(self, tau: int):
+        m = C.c_uint64()
+        w = C.c_uint32()
+        check(lib().dfs_device_graph_size(self._h, tau, C.byref(m), C.byref(w)))
+        n = self._graph.n
+        off = np.zeros(n + 1, np.uint64)
+        adj = np.zeros(max(m.value, 1), np.uint32)
+        mask = np.zeros(max(m.value * w.value, 1), np.uint64)
+        check(lib().dfs_device_graph(self._h, tau, off.ctypes.data, adj.ctypes.data,
+                                     mask.ctypes.data))
+        return off, adj[: m.value], mask[: m.value * w.value], w.value
+
+    def fill(self, tau: int):
+        check(lib().dfs_fill(self._h, tau))
+
+    def simulate(self, tau: int, cap: int = 256, jacobi: int = 0) -> int:
+        s = C.c_int()
+        check(lib().dfs_simulate(self._h, tau, cap, jacobi, C.byref(s)))
+        return s.value
+
+    def scores(self, tau: int) -> np.ndarray:
+        out = np.zeros(max(self._graph.n, 1), np.float64)
+        check(lib().dfs_scores(self._h, tau, out.ctypes.data))
+        return out[: self._graph.n]
+
+    def commit_cascade(self, tau: int, seed: int) -> int:
+        v = C.c_uint64()
+        check(lib().dfs_commit_cascade(self._h, tau, seed, C.byref(v)))
+        return v.value
+
+    def visited_count(self, tau: int) -> int:
+        v = C.c_uint64()
+        check(lib().dfs_visited_count(self._h, tau, C.byref(v)))
+        return v.value
+
+    def registers(self, tau: int) -> np.ndarray:
+        out = np.zeros(max(self._graph.n * self._J, 1), np.int8)
+        check(lib().dfs_get_registers(self._h, tau, out.ctypes.data))
+        return out[: self._graph.n * self._J]
+
+    def set_registers(self, tau: int, regs) -> None:
+        regs = np.ascontiguousarray(regs, np.int8)
+        check(lib().dfs_set_registers(self._h, tau, regs.ctypes.data))
+
+
+_ctx_lock = threading.Lock()
+_default = {}
+
+
+def default_context(device: int = 0) -> Context:
+    with _ctx_lock:
+        if device not in _default:
+            _default[device] = Context(device)
+        return _default[device]
+
+
+def run_json(graph, k=10, r=256, devices=1, mode="fasst", weights="const:0.1", rebuild_eps=0.01,
+             seed=0, timings=True):
+    """Select seeds; returns the report as a JSON string (pymodule.cpp:75-90)."""
+    return default_context().run_json(graph, k=k, r=r, devices=devices, mode=mode,
+                                      weights=weights, rebuild_eps=rebuild_eps, seed=seed,
+                                      timings=timings)
+
+
+def run(graph, **kwargs):
+    """Select seeds and return the report as a dict (see run_json)."""
+    return _json.loads(run_json(graph, **kwargs))
+
+
+def influence(graph, seeds, trials=10000, seed=0, runs=1, weights="const:0.1"):
+    """Monte Carlo influence of a dense-id seed set: (mean, std_error)."""
+    s = np.ascontiguousarray(list(seeds), np.uint32)
+    mean, se = C.c_double(), C.c_double()
+    check(lib().dfs_influence(graph._h, s.ctypes.data if len(s) else None, len(s), trials, seed,
+                              runs, weights.encode(), C.byref(mean), C.byref(se)))
+    return mean.value, se.value
+
+
+def greedy_exact(graph, k, trials=1000, seed=0, weights="const:0.1"):
+    """Reference greedy selection (dense ids)."""
+    out = np.zeros(max(k, 1), np.uint32)
+    check(lib().dfs_greedy_exact(graph._h, k, trials, seed, weights.encode(), out.ctypes.data))
+    return out[:k].tolist()

@@ -1,0 +1,175 @@
+// dfs.h — internal declarations shared by the host runtime (runtime.cpp) and
+// the sm_100a kernels (kernels.cu).  Not part of the public C-ABI
+// (include/difuser_b200.h).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace dfs {
+
+// Status codes of the C-ABI; mapped to the reference's exception classes by
+// the Python mirror (std::invalid_argument -> ValueError, runtime_error ->
+// RuntimeError, see proj/bindings/pymodule.cpp and SURVEY.md §8(b)).
+enum Status : int {
+  kOk = 0,
+  kInvalid = 1,   // std::invalid_argument
+  kRuntime = 2,   // std::runtime_error
+  kCuda = 3,      // CUDA failure (RuntimeError)
+  kNoMem = 4,     // allocation failure (MemoryError)
+  kIndex = 5,     // out-of-range (IndexError)
+};
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what);
+#define DFS_CUDA(x) ::dfs::cuda_check((x), #x)
+
+// Simulations are grouped in 32-sim batches (one u32 of live/visited bits).
+constexpr uint32_t kBatch = 32;
+// Items per work chunk: a warp owns one chunk (4 passes of 32 lanes).
+constexpr uint32_t kChunk = 128;
+
+// ---------------------------------------------------------------- device views
+// Full weighted graph, resident for the context (CSR by source u, plus its
+// transpose by target v).  ehash/in_degree are computed on the device.
+struct DevGraph {
+  uint32_t n = 0;
+  uint64_t m = 0;
+  uint64_t* off = nullptr;    // n+1
+  uint32_t* adj = nullptr;    // m   (target v of edge e)
+  uint32_t* src = nullptr;    // m   (source u of edge e)
+  uint32_t* ehash = nullptr;  // m
+  uint32_t* indeg = nullptr;  // n
+  uint64_t* toff = nullptr;   // n+1 (transpose offsets by v)
+  uint32_t* tedge = nullptr;  // m   (edge ids sorted by (v, e))
+};
+
+// One direction of the sampled ("device") graph as sparse 32-sim items:
+// item i of row r = (other endpoint, live mask over batch b).  Rows are split
+// into chunks of <= kChunk items; chunk c covers items [cbeg[c], cbeg[c+1]).
+struct Items {
+  uint64_t count = 0;
+  uint64_t chunks = 0;
+  uint64_t* row_off = nullptr;     // n+1 item offsets per row
+  uint32_t* other = nullptr;       // count
+  uint32_t* mask = nullptr;        // count
+  uint8_t* batch = nullptr;        // count
+  uint32_t* chunk_row = nullptr;   // chunks
+  uint64_t* chunk_beg = nullptr;   // chunks+1
+  uint32_t* row_chunk = nullptr;   // n+1 first chunk of each row
+};
+
+// Device-resident control block of one rank (sample-space partition tau).
+struct RankCtl {
+  unsigned long long visited;   // running VISITED register count
+  unsigned long long updates;   // live (item, sim) pairs merged (instrumentation)
+  unsigned long long items_processed;
+  unsigned int tick;            // strictly increasing stamp source
+  unsigned int sweeps;          // sweeps of the last simulate
+  unsigned int total_sweeps;
+  unsigned int levels;          // cascade levels (last)
+  int error;                    // 1 = simulate cap exceeded
+  unsigned int dirty_count;     // rows to rescore
+  unsigned int pad[6];
+};
+
+// Work queues used by the persistent simulate / cascade kernels.  Three
+// rotating generations (index = sweep % 3) so that a generation can be reset
+// while the next one is being filled without an extra grid barrier.
+struct Queues {
+  uint32_t* chunks[3];          // chunk ids to process
+  uint32_t* rows[3];            // rows (deduplicated) of that generation
+  unsigned int* counts;         // [3] chunk counts, [3..5] row counts, [6..8] work counters
+};
+
+struct RankDev {
+  uint32_t n = 0, J = 0, Jp = 0, W32 = 0, tau = 0;
+  uint32_t j_offset = 0;
+  uint64_t reg_key = 0;
+  uint32_t* x = nullptr;          // Jp sorted slice values (pads 0xFFFFFFFF)
+  uint64_t* jkey = nullptr;       // Jp register hash keys
+  int8_t* regs = nullptr;         // n*Jp
+  int8_t* snap = nullptr;         // n*Jp (Jacobi schedule only)
+  uint32_t* vis = nullptr;        // n*W32 visited bitset
+  uint32_t* fresh[2] = {nullptr, nullptr};  // n*W32 cascade frontier bits
+  uint32_t* lstamp = nullptr;     // n  queue-membership stamps
+  uint32_t* dstamp = nullptr;     // n  dirty-row stamps
+  uint32_t* dirty = nullptr;      // n  rows to rescore
+  double* scores = nullptr;       // n
+  RankCtl* ctl = nullptr;
+  Queues q{};
+  Items fwd, rev;                 // cascade uses fwd (by u), simulate uses rev (by v)
+};
+
+// Run-level control block (single device copy, written by the round kernels).
+struct RunCtl {
+  unsigned int step;
+  unsigned int choice;
+  unsigned int saturated;
+  unsigned int rebuild_now;
+  unsigned int n_rebuilds;
+  unsigned int argmax_done;       // last-block counter of the argmax
+  unsigned int pad[2];
+  double oldscore;
+};
+
+struct RunArrays {
+  RunCtl* ctl = nullptr;
+  uint8_t* committed = nullptr;   // n
+  uint32_t* seeds = nullptr;      // k
+  double* traj = nullptr;         // k
+  uint32_t* rebuild_rounds = nullptr;  // k
+  double* reduced = nullptr;      // n (tree-summed scores, mu > 1)
+  double* blk_score = nullptr;    // argmax partials
+  uint32_t* blk_arg = nullptr;
+  uint32_t* blk_min = nullptr;
+  uint32_t nblk = 0;
+};
+
+// ---------------------------------------------------------------- launchers
+// Graph preparation (once per upload): src, ehash, in-degree, transpose.
+size_t graph_prepare_tmp_bytes(uint64_t m, uint32_t n);
+void launch_graph_prepare(DevGraph& g, void* tmp, size_t tmp_bytes, cudaStream_t s);
+// Weights: kind 0 = const (W), 1 = wc (from in-degree).  Other kinds are
+// computed on the host (std::mt19937_64) and uploaded.
+void launch_weights(const DevGraph& g, int kind, uint32_t W, uint32_t* w, cudaStream_t s);
+// Exclusive scan u32 -> u64 (out has n+1 entries; out[n] = total).
+size_t scan_tmp_bytes(uint64_t n);
+void scan_u32_u64(const uint32_t* in, uint64_t* out, uint64_t n, void* tmp, size_t tmp_bytes,
+                  cudaStream_t s);
+// Sampled-item construction for one rank and direction (dir 0 = by source u
+// over the CSR, dir 1 = by target v over the transpose).  write = 0 counts
+// items per edge position into cnt; write = 1 emits them at pos_off.
+void launch_items_pass(const DevGraph& g, const uint32_t* w, const RankDev& r, int dir,
+                       int fasst, int write, uint32_t* cnt, const uint64_t* pos_off,
+                       Items& it, cudaStream_t s);
+// row_off[r] = pos_off[graph row start]; then per-row chunk counts.
+void launch_row_offsets(const DevGraph& g, int dir, const uint64_t* pos_off, Items& it,
+                        uint32_t* row_cnt, cudaStream_t s);
+void launch_chunk_write(uint32_t n, Items& it, const uint64_t* row_chunk64, cudaStream_t s);
+// Fill registers (VISITED kept, pads VISITED).  gate: run only if *gate == want.
+void launch_fill(const RankDev& r, const unsigned int* gate, unsigned int want, cudaStream_t s);
+// Persistent cooperative simulate to convergence.  jacobi != 0 reproduces the
+// reference's snapshot schedule exactly (same sweep count).
+void launch_simulate(const RankDev& r, int jacobi, int cap, const unsigned int* gate,
+                     unsigned int want, cudaStream_t s);
+// Row scores: full = all rows, else the dirty list of the last cascade.
+void launch_score(const RankDev& r, int full, const unsigned int* gate, unsigned int want,
+                  cudaStream_t s);
+void launch_treesum(const double* const* parts_dev, uint32_t mu, uint32_t n, double* out,
+                    cudaStream_t s);
+void launch_argmax(const double* scores, RunArrays& ra, uint32_t n, cudaStream_t s);
+// Commit of *choice (or of `seed` when choice == nullptr) + full cascade.
+void launch_cascade(const RankDev& r, const unsigned int* choice, uint32_t seed,
+                    cudaStream_t s);
+void launch_round_end(RunArrays& ra, RankCtl* const* ctls_dev, uint32_t mu, uint32_t k,
+                      uint32_t r, double eps, cudaStream_t s);
+int coop_grid(int which);  // 0 simulate, 1 cascade
+
+}  // namespace dfs

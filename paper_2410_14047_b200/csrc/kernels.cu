@@ -1,0 +1,841 @@
+// kernels.cu — sm_100a kernels of the sketch-IM hot path.
+//
+// Memory-bound integer work throughout (byte max-merge, xor/compare sampling,
+// bitset BFS): no tensor cores.  The design points:
+//  * sampling is never materialised as dense masks (the reference bakes
+//    m_tau x ceil(J/64) words, proj/src/fasst.cpp:72-82); instead each edge is
+//    expanded once per run into sparse 32-sim "items" (other endpoint, live
+//    mask, batch) — only batches where the edge is live in >= 1 simulation.
+//    With FASST-sorted x values the live simulations of an edge form one
+//    contiguous window, found by two binary searches;
+//  * simulate is a persistent cooperative kernel: push-style (source row v to
+//    all u with a live edge u->v), in place, lock-free byte-max via 64-bit
+//    CAS, frontier of changed rows between sweeps, one grid barrier per sweep;
+//  * the cascade (coverage removal) is a persistent level-synchronous bitset
+//    BFS over the forward items; the score is bit-exact via an integer sum.
+#include <cooperative_groups.h>
+#include <cub/cub.cuh>
+#include <cuda/std/functional>
+
+#include "dfs.h"
+#include "hash.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace dfs {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(e == cudaErrorMemoryAllocation ? kNoMem : kCuda,
+                std::string("CUDA error: ") + cudaGetErrorString(e) + " at " + what);
+}
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    DFS_CUDA(cudaGetDevice(&dev));
+    DFS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return sms;
+}
+
+int grid_for(uint64_t work, int per_block = kThreads) {
+  uint64_t b = (work + per_block - 1) / per_block;
+  uint64_t cap = uint64_t(num_sms()) * 16;
+  if (b > cap) b = cap;
+  return b ? int(b) : 1;
+}
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
+
+template <class T>
+__device__ __forceinline__ T ld_volatile(const T* p) {
+  return *reinterpret_cast<const volatile T*>(p);
+}
+
+// ---------------------------------------------------------------- graph prep
+__global__ void k_src(uint32_t n, const uint64_t* __restrict__ off, uint32_t* __restrict__ src) {
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t u = warp; u < n; u += nw)
+    for (uint64_t e = off[u] + lane_id(); e < off[u + 1]; e += 32) src[e] = uint32_t(u);
+}
+
+__global__ void k_ehash_indeg(uint64_t m, const uint32_t* __restrict__ src,
+                              const uint32_t* __restrict__ adj, uint32_t* __restrict__ ehash,
+                              uint32_t* __restrict__ indeg, uint32_t* __restrict__ iota) {
+  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < m;
+       e += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t v = adj[e];
+    ehash[e] = edge_hash(src[e], v);  // graph.cpp:180, on dense ids
+    atomicAdd(&indeg[v], 1u);
+    iota[e] = uint32_t(e);
+  }
+}
+
+__global__ void k_u32_to_u64(const uint32_t* __restrict__ in, uint64_t* __restrict__ out,
+                             uint64_t n) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    out[i] = in[i];
+}
+
+// ---------------------------------------------------------------- weights
+// graph.cpp:30-35 + :250-258: W = llround(w * 2^31), wc w = 1/indeg(v).
+__global__ void k_weights(uint64_t m, int kind, uint32_t W, const uint32_t* __restrict__ adj,
+                          const uint32_t* __restrict__ indeg, uint32_t* __restrict__ w) {
+  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < m;
+       e += uint64_t(gridDim.x) * blockDim.x) {
+    if (kind == 0) {
+      w[e] = W;
+    } else {
+      const double p = __ddiv_rn(1.0, double(indeg[adj[e]]));
+      w[e] = uint32_t(llround(__dmul_rn(p, 2147483648.0)));
+    }
+  }
+}
+
+// ---------------------------------------------------------------- items
+// Live window of an edge in the sorted slice: (x ^ h) < W implies x agrees
+// with h on all bits above floor(log2 W), i.e. x lies in one aligned block of
+// size 2^(floor(log2 W)+1) around h; sorted order turns
+// that block into the contiguous slot range [lo, hi).
+__device__ __forceinline__ void edge_window(const uint32_t* sx, uint32_t J, uint32_t h,
+                                            uint32_t W, int fasst, uint32_t& lo, uint32_t& hi) {
+  if (!fasst) {
+    lo = 0;
+    hi = J;
+    return;
+  }
+  const int b = 31 - __clz(W);  // W >= 1
+  const uint64_t span = uint64_t(1) << (b + 1);
+  const uint64_t lx = (uint64_t(h) / span) * span;
+  const uint64_t hx = lx + span;  // exclusive
+  uint32_t a = 0, z = J;          // lower_bound(lx)
+  while (a < z) {
+    uint32_t mid = (a + z) >> 1;
+    if (uint64_t(sx[mid]) < lx) a = mid + 1; else z = mid;
+  }
+  lo = a;
+  z = J;  // lower_bound(hx)
+  while (a < z) {
+    uint32_t mid = (a + z) >> 1;
+    if (uint64_t(sx[mid]) < hx) a = mid + 1; else z = mid;
+  }
+  hi = a;
+}
+
+// dir 0: positions = CSR edges (row = src u, other = adj v)
+// dir 1: positions = transpose (edge = tedge[p], row = adj v, other = src u)
+template <int WRITE>
+__global__ void k_items(uint64_t npos, int dir, const uint32_t* __restrict__ tedge,
+                        const uint32_t* __restrict__ adj, const uint32_t* __restrict__ src,
+                        const uint32_t* __restrict__ ehash, const uint32_t* __restrict__ w,
+                        const uint32_t* __restrict__ x, uint32_t J, uint32_t Jp, int fasst,
+                        uint32_t* __restrict__ cnt, const uint64_t* __restrict__ pos_off,
+                        uint32_t* __restrict__ it_other, uint32_t* __restrict__ it_mask,
+                        uint8_t* __restrict__ it_batch) {
+  extern __shared__ uint32_t sx[];
+  for (uint32_t i = threadIdx.x; i < Jp; i += blockDim.x) sx[i] = x[i];
+  __syncthreads();
+  for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < npos;
+       p += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t e = dir ? tedge[p] : uint32_t(p);
+    const uint32_t W = w[e];
+    uint32_t c = 0;
+    if (W != 0) {  // fasst.cpp:71 — W = 0 never samples
+      const uint32_t h = ehash[e];
+      uint32_t lo, hi;
+      edge_window(sx, J, h, W, fasst, lo, hi);
+      if (hi > lo) {
+        uint64_t o = WRITE ? pos_off[p] : 0;
+        const uint32_t other = WRITE ? (dir ? src[e] : adj[e]) : 0;
+        for (uint32_t b = lo >> 5; b <= (hi - 1) >> 5; ++b) {
+          uint32_t mk = 0;
+          const uint32_t* xb = sx + b * 32;
+#pragma unroll 8
+          for (int i = 0; i < 32; ++i) mk |= uint32_t((xb[i] ^ h) < W) << i;  // sampling.hpp:37-39
+          if (mk) {
+            if (WRITE) {
+              it_other[o] = other;
+              it_mask[o] = mk;
+              it_batch[o] = uint8_t(b);
+              ++o;
+            }
+            ++c;
+          }
+        }
+      }
+    }
+    if (!WRITE) cnt[p] = c;
+  }
+}
+
+__global__ void k_row_offsets(uint32_t n, const uint64_t* __restrict__ graph_off,
+                              const uint64_t* __restrict__ pos_off, uint64_t* __restrict__ row_off,
+                              uint32_t* __restrict__ row_cnt) {
+  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r <= n;
+       r += uint64_t(gridDim.x) * blockDim.x) {
+    row_off[r] = pos_off[graph_off[r]];
+    if (r < n) {
+      const uint64_t items = pos_off[graph_off[r + 1]] - pos_off[graph_off[r]];
+      row_cnt[r] = uint32_t((items + kChunk - 1) / kChunk);
+    }
+  }
+}
+
+__global__ void k_chunk_write(uint32_t n, const uint64_t* __restrict__ row_chunk64,
+                              const uint64_t* __restrict__ row_off, uint32_t* __restrict__ row_chunk,
+                              uint32_t* __restrict__ chunk_row, uint64_t* __restrict__ chunk_beg,
+                              uint64_t total_items) {
+  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r <= n;
+       r += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t c0 = row_chunk64[r];
+    row_chunk[r] = uint32_t(c0);
+    if (r == n) {
+      chunk_beg[c0] = total_items;
+      continue;
+    }
+    const uint64_t c1 = row_chunk64[r + 1];
+    for (uint64_t c = c0; c < c1; ++c) {
+      chunk_row[c] = uint32_t(r);
+      chunk_beg[c] = row_off[r] + (c - c0) * kChunk;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- fill
+// sketch.cpp:55-66: M[u][j] = clz64(fmix64(jkey[j] + u*golden)) unless VISITED.
+// One thread per 4 registers (one u32 store, coalesced across the warp).
+__global__ void k_fill(uint32_t n, uint32_t J, uint32_t Jp, const uint64_t* __restrict__ jkey,
+                       const uint32_t* __restrict__ vis, int8_t* __restrict__ regs,
+                       const unsigned int* gate, unsigned int want, RankCtl* ctl) {
+  if (gate && ld_volatile(gate) != want) return;
+  if (ctl && blockIdx.x == 0 && threadIdx.x == 0) ctl->dirty_count = 0;  // full rescore follows
+  const uint32_t q = Jp >> 2;
+  const uint32_t W32 = Jp >> 5;
+  const uint64_t total = uint64_t(n) * q;
+  for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t u = t / q;
+    const uint32_t j0 = uint32_t(t - u * q) * 4;
+    const uint32_t vb = vis[u * W32 + (j0 >> 5)] >> (j0 & 31);
+    const uint64_t ug = u * kGolden;
+    uint32_t word = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t j = j0 + k;
+      uint32_t byte = 0xFFu;
+      if (j < J && !((vb >> k) & 1u)) byte = uint32_t(__clzll(fmix64(__ldg(jkey + j) + ug)));
+      word |= byte << (8 * k);
+    }
+    reinterpret_cast<uint32_t*>(regs)[t] = word;
+  }
+}
+
+// ---------------------------------------------------------------- simulate
+// Byte-wise merge of 4 registers: dst takes max(dst, src) on live simulations;
+// VISITED (-1) in dst is absorbing, VISITED in src never wins
+// (engine.cpp:22-53).  bm = 0xFF per live byte.
+__device__ __forceinline__ uint32_t expand4(uint32_t m4) {
+  return ((m4 * 0x00204081u) & 0x01010101u) * 0xFFu;
+}
+__device__ __forceinline__ uint32_t merge4(uint32_t d, uint32_t s, uint32_t bm) {
+  const uint32_t sm = (s & bm) | (0x80808080u & ~bm);  // dead sims -> -128, never win
+  return __vmaxs4(d, sm) | __vcmpeq4(d, 0xFFFFFFFFu);   // keep VISITED
+}
+__device__ __forceinline__ unsigned long long merge8(unsigned long long d, unsigned long long s,
+                                                     uint32_t m8) {
+  const uint32_t lo = merge4(uint32_t(d), uint32_t(s), expand4(m8 & 15u));
+  const uint32_t hi = merge4(uint32_t(d >> 32), uint32_t(s >> 32), expand4(m8 >> 4));
+  return (static_cast<unsigned long long>(hi) << 32) | lo;
+}
+
+// Warp-cooperative push of row u into the next generation (deduplicated by
+// stamp): appends u to rows[gn] and all of u's chunks to chunks[gn].
+__device__ __forceinline__ void push_row(uint32_t u, uint32_t stamp, uint32_t* lstamp,
+                                         const uint32_t* row_chunk, uint32_t* rows,
+                                         uint32_t* chunks, unsigned int* chunk_cnt,
+                                         unsigned int* row_cnt) {
+  if (atomicExch(&lstamp[u], stamp) == stamp) return;
+  const unsigned ri = atomicAdd(row_cnt, 1u);
+  rows[ri] = u;
+  const uint32_t c0 = row_chunk[u], c1 = row_chunk[u + 1];
+  if (c1 > c0) {
+    const unsigned ci = atomicAdd(chunk_cnt, c1 - c0);
+    for (uint32_t c = c0; c < c1; ++c) chunks[ci + (c - c0)] = c;
+  }
+}
+
+struct SimArgs {
+  RankDev r;
+  int jacobi;
+  int cap;
+  const unsigned int* gate;
+  unsigned int want;
+};
+
+// Persistent simulate-to-convergence (engine.cpp:57-96 semantics).  Sweep s
+// processes the reverse chunks of rows that changed in sweep s-1 (all chunks
+// in sweep 1).  Async mode reads and writes the live matrix in place (the
+// fixpoint is schedule-independent: DESIGN.md §simulate); Jacobi mode reads
+// the snapshot and re-syncs changed rows after each sweep, which reproduces
+// the reference's sweep count exactly.
+__global__ void __launch_bounds__(kThreads) k_simulate(SimArgs a) {
+  if (a.gate && ld_volatile(a.gate) != a.want) return;  // grid-uniform
+  cg::grid_group grid = cg::this_grid();
+  const RankDev& r = a.r;
+  unsigned int* cnt = r.q.counts;
+  const uint32_t base = ld_volatile(&r.ctl->tick);
+  const unsigned lane = lane_id();
+  const uint64_t gwarp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (gwarp == 0 && lane < 9) cnt[lane] = 0;
+  if (a.jacobi) {  // SimulateBuffers::reset (engine.cpp:9-15): snapshot := registers
+    const uint64_t n16 = uint64_t(r.n) * r.Jp / 16;
+    const uint4* s4 = reinterpret_cast<const uint4*>(r.regs);
+    uint4* d4 = reinterpret_cast<uint4*>(r.snap);
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
+         i += uint64_t(gridDim.x) * blockDim.x)
+      d4[i] = s4[i];
+  }
+  grid.sync();
+
+  const int8_t* srcm = a.jacobi ? r.snap : r.regs;
+  unsigned long long upd = 0, nitems = 0;
+  uint32_t s = 1;
+  int err = 0;
+  for (;; ++s) {
+    const int g = s % 3, gn = (s + 1) % 3, gr = (s + 2) % 3;
+    if (s > 1 && ld_volatile(&cnt[3 + g]) == 0) break;  // no row changed in sweep s-1
+    if (s > uint32_t(a.cap)) {
+      err = 1;
+      break;
+    }
+    const uint32_t nc = (s == 1) ? uint32_t(r.rev.chunks) : ld_volatile(&cnt[g]);
+    if (gwarp == 0 && lane == 0) {
+      cnt[gr] = 0;
+      cnt[3 + gr] = 0;
+      cnt[6 + gr] = 0;
+    }
+    const uint32_t stamp = base + s;
+    for (;;) {
+      unsigned ci = 0;
+      if (lane == 0) ci = atomicAdd(&cnt[6 + g], 1u);
+      ci = __shfl_sync(0xffffffffu, ci, 0);
+      if (ci >= nc) break;
+      const uint32_t c = (s == 1) ? ci : r.q.chunks[g][ci];
+      const uint32_t v = r.rev.chunk_row[c];
+      const uint64_t beg = r.rev.chunk_beg[c], end = r.rev.chunk_beg[c + 1];
+      const int8_t* srow = srcm + uint64_t(v) * r.Jp;
+      for (uint64_t i0 = beg; i0 < end; i0 += 32) {
+        const uint64_t i = i0 + lane;
+        if (i < end) {
+          const uint32_t u = __ldg(r.rev.other + i);
+          const uint32_t mk = __ldg(r.rev.mask + i);
+          const uint32_t b = __ldg(r.rev.batch + i);
+          const unsigned long long* sp =
+              reinterpret_cast<const unsigned long long*>(srow + b * 32);
+          unsigned long long* dp =
+              reinterpret_cast<unsigned long long*>(r.regs + uint64_t(u) * r.Jp + b * 32);
+          bool changed = false;
+#pragma unroll
+          for (int wv = 0; wv < 4; ++wv) {
+            const uint32_t m8 = (mk >> (8 * wv)) & 0xFFu;
+            if (!m8) continue;
+            const unsigned long long sv = __ldcg(sp + wv);
+            unsigned long long dv = __ldcg(dp + wv);
+            unsigned long long nv = merge8(dv, sv, m8);
+            while (nv != dv) {
+              const unsigned long long old = atomicCAS(dp + wv, dv, nv);
+              if (old == dv) {
+                changed = true;
+                break;
+              }
+              dv = old;
+              nv = merge8(dv, sv, m8);
+            }
+          }
+          upd += __popc(mk);
+          ++nitems;
+          if (changed)
+            push_row(u, stamp, r.lstamp, r.rev.row_chunk, r.q.rows[gn], r.q.chunks[gn], &cnt[gn],
+                     &cnt[3 + gn]);
+        }
+      }
+    }
+    grid.sync();
+    if (a.jacobi) {  // engine.cpp:81-82: re-sync snapshot rows that moved
+      const unsigned nr = ld_volatile(&cnt[3 + gn]);
+      const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+      for (uint64_t k = gwarp; k < nr; k += nw) {
+        const uint64_t row = uint64_t(r.q.rows[gn][k]) * r.Jp;
+        const uint4* sp4 = reinterpret_cast<const uint4*>(r.regs + row);
+        uint4* dp4 = reinterpret_cast<uint4*>(r.snap + row);
+        for (uint32_t j = lane; j < r.Jp / 16; j += 32) dp4[j] = __ldcg(sp4 + j);
+      }
+      grid.sync();
+    }
+  }
+  // Instrumentation: one atomic per warp.
+  for (int o = 16; o; o >>= 1) {
+    upd += __shfl_xor_sync(0xffffffffu, upd, o);
+    nitems += __shfl_xor_sync(0xffffffffu, nitems, o);
+  }
+  if (lane == 0 && upd) {
+    atomicAdd(&r.ctl->updates, upd);
+    atomicAdd(&r.ctl->items_processed, nitems);
+  }
+  if (gwarp == 0 && lane == 0) {
+    r.ctl->sweeps = err ? s : s - 1;
+    r.ctl->total_sweeps += err ? s : s - 1;
+    r.ctl->tick = base + s + 2;
+    if (err) r.ctl->error = 1;
+  }
+}
+
+// ---------------------------------------------------------------- score
+// sketch.cpp:119-131: live = #non-VISITED, denom = sum 2^-M[j] (ascending j),
+// score = live*live / (denom*phi).  With every live register <= K and
+// J * 2^K <= 2^53, each sequential partial sum is an exact multiple of 2^-K
+// below 2^53 * 2^-K, so the reference's double sum is exact and equals the
+// integer sum sum 2^(K-M[j]) scaled by 2^-K.  Rows with a
+// larger register fall back to the sequential double sum.
+__global__ void k_score(const int8_t* __restrict__ regs, uint32_t n, uint32_t J, uint32_t Jp,
+                        int K, int full, const uint32_t* __restrict__ rows, RankCtl* ctl,
+                        double* __restrict__ scores, const unsigned int* gate, unsigned int want) {
+  if (gate && ld_volatile(gate) != want) return;
+  const uint32_t nrows = full ? n : ld_volatile(&ctl->dirty_count);
+  const unsigned lane = lane_id();
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t k = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; k < nrows; k += nw) {
+    const uint32_t u = full ? uint32_t(k) : rows[k];
+    const uint32_t* row = reinterpret_cast<const uint32_t*>(regs + uint64_t(u) * Jp);
+    uint32_t live = 0;
+    int mx = 0;
+    unsigned long long isum = 0;
+    for (uint32_t q = lane; q < Jp / 4; q += 32) {
+      const uint32_t wv = __ldcg(row + q);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int rv = int(int8_t(wv >> (8 * b)));
+        if (rv >= 0) {
+          ++live;
+          mx = max(mx, rv);
+          if (rv <= K) isum += 1ull << (K - rv);
+        }
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      live += __shfl_xor_sync(0xffffffffu, live, o);
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      isum += __shfl_xor_sync(0xffffffffu, isum, o);
+    }
+    if (lane == 0) {
+      double sc = 0.0;
+      if (live) {
+        double denom;
+        if (mx <= K) {
+          denom = ldexp(double(isum), -K);
+        } else {  // exact sequential replay (rare)
+          denom = 0.0;
+          const int8_t* rb = regs + uint64_t(u) * Jp;
+          for (uint32_t j = 0; j < J; ++j)
+            if (rb[j] >= 0) denom = __dadd_rn(denom, ldexp(1.0, -int(rb[j])));
+        }
+        const double lv = double(live);
+        sc = __ddiv_rn(__dmul_rn(lv, lv), __dmul_rn(denom, kPhi));
+      }
+      scores[u] = sc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- reduce/argmax
+// collectives.cpp:44-64: level k folds rank+2^k into rank (fixed order).
+__global__ void k_treesum(const double* const* __restrict__ parts, uint32_t mu, uint32_t n,
+                          double* __restrict__ out) {
+  for (uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n;
+       v += uint64_t(gridDim.x) * blockDim.x) {
+    double acc[64];
+    for (uint32_t t = 0; t < mu; ++t) acc[t] = parts[t][v];
+    for (uint32_t st = 1; st < mu; st <<= 1)
+      for (uint32_t t = 0; t + st < mu; t += 2 * st) acc[t] = __dadd_rn(acc[t], acc[t + st]);
+    out[v] = acc[0];
+  }
+}
+
+struct Best {
+  double s;
+  uint32_t v;
+  uint32_t minu;
+};
+__device__ __forceinline__ Best best_of(Best a, Best b) {
+  Best r;
+  // runtime.cpp:95-119: strict '>' from 0.0 in ascending v == max score, ties
+  // to the smallest id, only positive scores qualify.
+  if (b.s > a.s || (b.s == a.s && b.v < a.v)) {
+    r.s = b.s;
+    r.v = b.v;
+  } else {
+    r.s = a.s;
+    r.v = a.v;
+  }
+  r.minu = min(a.minu, b.minu);
+  return r;
+}
+
+__global__ void __launch_bounds__(kThreads) k_argmax(const double* __restrict__ scores,
+                                                     uint32_t n, RunArrays ra) {
+  Best b{0.0, 0xFFFFFFFFu, 0xFFFFFFFFu};
+  for (uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n;
+       v += uint64_t(gridDim.x) * blockDim.x) {
+    if (ra.committed[v]) continue;
+    const double s = scores[v];
+    if (b.minu == 0xFFFFFFFFu) b.minu = uint32_t(v);
+    if (s > b.s) {  // ascending v within a thread: strict > keeps the first
+      b.s = s;
+      b.v = uint32_t(v);
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    Best x{__shfl_xor_sync(0xffffffffu, b.s, o), __shfl_xor_sync(0xffffffffu, b.v, o),
+           __shfl_xor_sync(0xffffffffu, b.minu, o)};
+    b = best_of(b, x);
+  }
+  __shared__ Best sb[kWarps];
+  __shared__ bool last;
+  if (lane_id() == 0) sb[threadIdx.x >> 5] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Best t = sb[0];
+    for (int w = 1; w < kWarps; ++w) t = best_of(t, sb[w]);
+    ra.blk_score[blockIdx.x] = t.s;
+    ra.blk_arg[blockIdx.x] = t.v;
+    ra.blk_min[blockIdx.x] = t.minu;
+    __threadfence();
+    last = atomicAdd(&ra.ctl->argmax_done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    Best t{0.0, 0xFFFFFFFFu, 0xFFFFFFFFu};
+    for (uint32_t k = 0; k < gridDim.x; ++k)
+      t = best_of(t, Best{ld_volatile(ra.blk_score + k), ld_volatile(ra.blk_arg + k),
+                          ld_volatile(ra.blk_min + k)});
+    uint32_t choice = t.v;
+    if (choice == 0xFFFFFFFFu) {  // saturated: smallest uncommitted id
+      ra.ctl->saturated = 1;
+      choice = t.minu;
+    }
+    ra.ctl->choice = choice;
+    ra.committed[choice] = 1;
+    ra.ctl->argmax_done = 0;
+  }
+}
+
+// ---------------------------------------------------------------- cascade
+struct CasArgs {
+  RankDev r;
+  const unsigned int* choice;
+  uint32_t seed;
+};
+
+// commit_seed + cascade (engine.cpp:106-144): level-synchronous BFS of fresh
+// VISITED bits along forward items; cand = fresh_u & live & ~vis_v.  Post:
+// VISITED_j(v) <=> v reachable from a committed seed in sample j.
+__global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  const RankDev& r = a.r;
+  unsigned int* cnt = r.q.counts;
+  const uint32_t base = ld_volatile(&r.ctl->tick);
+  const unsigned lane = lane_id();
+  const uint64_t gwarp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t W32 = r.W32;
+  unsigned long long marked = 0;
+
+  if (gwarp == 0) {
+    if (lane < 9) cnt[lane] = 0;
+    __syncwarp();
+    const uint32_t s = a.choice ? ld_volatile(a.choice) : a.seed;
+    if (lane == 0) {
+      r.ctl->dirty_count = 1;
+      r.dirty[0] = s;
+      r.dstamp[s] = base;
+    }
+    // engine.cpp:106-118: every non-VISITED register of s becomes fresh.
+    bool any = false;
+    for (uint32_t w = lane; w < W32; w += 32) {
+      const uint32_t rem = r.J - w * 32;
+      const uint32_t tail = rem >= 32 ? 0xFFFFFFFFu : ((1u << rem) - 1u);
+      const uint32_t bits = tail & ~r.vis[uint64_t(s) * W32 + w];
+      if (bits) {
+        r.vis[uint64_t(s) * W32 + w] |= bits;
+        r.fresh[1][uint64_t(s) * W32 + w] = bits;
+        int8_t* rb = r.regs + uint64_t(s) * r.Jp + w * 32;
+        for (uint32_t t = bits; t; t &= t - 1) rb[__ffs(t) - 1] = -1;
+        marked += __popc(bits);
+        any = true;
+      }
+    }
+    any = __any_sync(0xffffffffu, any);
+    __syncwarp();
+    if (any && lane == 0)
+      push_row(s, base + 1, r.lstamp, r.fwd.row_chunk, r.q.rows[1], r.q.chunks[1], &cnt[1],
+               &cnt[4]);
+  }
+  grid.sync();
+
+  uint32_t L = 1;
+  for (;; ++L) {
+    const int g = L % 3, gn = (L + 1) % 3, gr = (L + 2) % 3;
+    const uint32_t nc = ld_volatile(&cnt[g]);
+    if (nc == 0) break;
+    if (gwarp == 0 && lane == 0) {
+      cnt[gr] = 0;
+      cnt[3 + gr] = 0;
+      cnt[6 + gr] = 0;
+    }
+    const uint32_t* fcur = r.fresh[L & 1];
+    uint32_t* fnxt = r.fresh[(L + 1) & 1];
+    const uint32_t stamp = base + L + 1;
+    for (;;) {
+      unsigned ci = 0;
+      if (lane == 0) ci = atomicAdd(&cnt[6 + g], 1u);
+      ci = __shfl_sync(0xffffffffu, ci, 0);
+      if (ci >= nc) break;
+      const uint32_t c = r.q.chunks[g][ci];
+      const uint32_t u = r.fwd.chunk_row[c];
+      const uint64_t beg = r.fwd.chunk_beg[c], end = r.fwd.chunk_beg[c + 1];
+      for (uint64_t i = beg + lane; i < end; i += 32) {
+        const uint32_t b = r.fwd.batch[i];
+        uint32_t cand = __ldcg(fcur + uint64_t(u) * W32 + b) & r.fwd.mask[i];
+        if (!cand) continue;
+        const uint32_t v = r.fwd.other[i];
+        uint32_t* vw = r.vis + uint64_t(v) * W32 + b;
+        cand &= ~__ldcg(vw);
+        if (!cand) continue;
+        const uint32_t nb = cand & ~atomicOr(vw, cand);
+        if (!nb) continue;
+        int8_t* rb = r.regs + uint64_t(v) * r.Jp + b * 32;
+        for (uint32_t t = nb; t; t &= t - 1) rb[__ffs(t) - 1] = -1;
+        atomicOr(fnxt + uint64_t(v) * W32 + b, nb);
+        marked += __popc(nb);
+        if (atomicExch(&r.dstamp[v], base) != base) r.dirty[atomicAdd(&r.ctl->dirty_count, 1u)] = v;
+        push_row(v, stamp, r.lstamp, r.fwd.row_chunk, r.q.rows[gn], r.q.chunks[gn], &cnt[gn],
+                 &cnt[3 + gn]);
+      }
+    }
+    grid.sync();
+    // engine.cpp:137-139: clear the consumed fresh rows.
+    const unsigned nr = ld_volatile(&cnt[3 + g]);
+    uint32_t* fc = r.fresh[L & 1];
+    for (uint64_t k = gwarp; k < nr; k += nw) {
+      const uint64_t row = uint64_t(r.q.rows[g][k]) * W32;
+      for (uint32_t w = lane; w < W32; w += 32) fc[row + w] = 0;
+    }
+    grid.sync();
+  }
+  for (int o = 16; o; o >>= 1) marked += __shfl_xor_sync(0xffffffffu, marked, o);
+  if (lane == 0 && marked) atomicAdd(&r.ctl->visited, marked);
+  if (gwarp == 0 && lane == 0) {
+    r.ctl->levels = L;
+    r.ctl->tick = base + L + 2;
+  }
+}
+
+// ---------------------------------------------------------------- round end
+__global__ void k_round_end(RunArrays ra, RankCtl* const* ctls, uint32_t mu, uint32_t k,
+                            uint32_t R, double eps) {
+  if (threadIdx.x || blockIdx.x) return;
+  unsigned long long covered = 0;  // collectives.cpp:96-113 (exact u64 sum)
+  for (uint32_t t = 0; t < mu; ++t) covered += ld_volatile(&ctls[t]->visited);
+  const double score = __ddiv_rn(double(covered), double(R));  // runtime.cpp:130
+  RunCtl* c = ra.ctl;
+  const uint32_t step = c->step;
+  ra.seeds[step] = c->choice;
+  ra.traj[step] = score;
+  // runtime.cpp:139-140
+  const bool rebuild =
+      step + 1 < k && __dadd_rn(score, -c->oldscore) > __dmul_rn(eps, score);
+  c->rebuild_now = rebuild ? 1u : 0u;
+  if (rebuild) {
+    ra.rebuild_rounds[c->n_rebuilds++] = step;
+    c->oldscore = score;
+  }
+  c->step = step + 1;
+}
+
+}  // namespace
+
+// ================================================================= launchers
+size_t graph_prepare_tmp_bytes(uint64_t m, uint32_t n) {
+  size_t sort_bytes = 0, scan_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, (const uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, m ? m : 1);
+  scan_bytes = scan_tmp_bytes(n + 1);
+  // layout: iota(m) | keys_out(m) | counts64 (n+1) | cub temp
+  return 2 * (m + 16) * sizeof(uint32_t) + (n + 16) * sizeof(uint64_t) +
+         std::max(sort_bytes, scan_bytes) + 1024;
+}
+
+size_t scan_tmp_bytes(uint64_t n) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveScan(nullptr, bytes, (const uint32_t*)nullptr, (uint64_t*)nullptr,
+                                 cuda::std::plus<uint64_t>{}, uint64_t(0), n ? n : 1);
+  return bytes + 256;
+}
+
+void scan_u32_u64(const uint32_t* in, uint64_t* out, uint64_t n, void* tmp, size_t tmp_bytes,
+                  cudaStream_t s) {
+  // exclusive scan of n values into out[0..n); out[n] = total via a scan of n+1
+  // values whose last input is read as 0 (caller guarantees in[n] == 0).
+  size_t bytes = tmp_bytes;
+  DFS_CUDA(cub::DeviceScan::ExclusiveScan(tmp, bytes, in, out, cuda::std::plus<uint64_t>{},
+                                          uint64_t(0), n + 1, s));
+}
+
+void launch_graph_prepare(DevGraph& g, void* tmp, size_t tmp_bytes, cudaStream_t s) {
+  const uint64_t m = g.m;
+  char* p = static_cast<char*>(tmp);
+  uint32_t* iota = reinterpret_cast<uint32_t*>(p);
+  p += (m + 16) * sizeof(uint32_t);
+  uint32_t* keys_out = reinterpret_cast<uint32_t*>(p);
+  p += (m + 16) * sizeof(uint32_t);
+  uint64_t* off64 = reinterpret_cast<uint64_t*>(p);
+  (void)off64;
+  p += (g.n + 16) * sizeof(uint64_t);
+  void* cubtmp = p;
+  size_t cub_bytes = tmp_bytes - size_t(p - static_cast<char*>(tmp));
+
+  DFS_CUDA(cudaMemsetAsync(g.indeg, 0, (size_t(g.n) + 1) * sizeof(uint32_t), s));
+  if (m) {
+    k_src<<<grid_for(uint64_t(g.n) * 32), kThreads, 0, s>>>(g.n, g.off, g.src);
+    k_ehash_indeg<<<grid_for(m), kThreads, 0, s>>>(m, g.src, g.adj, g.ehash, g.indeg, iota);
+    int end_bit = 1;
+    while (end_bit < 32 && (uint64_t(1) << end_bit) < g.n) ++end_bit;
+    size_t bytes = cub_bytes;
+    DFS_CUDA(cub::DeviceRadixSort::SortPairs(cubtmp, bytes, g.adj, keys_out, iota, g.tedge, m, 0,
+                                             end_bit, s));
+  }
+  // toff = exclusive scan of in-degrees (indeg[n] == 0 by the memset above)
+  size_t bytes = cub_bytes;
+  DFS_CUDA(cub::DeviceScan::ExclusiveScan(cubtmp, bytes, g.indeg, g.toff,
+                                          cuda::std::plus<uint64_t>{}, uint64_t(0), g.n + 1, s));
+  DFS_CUDA(cudaGetLastError());
+}
+
+void launch_weights(const DevGraph& g, int kind, uint32_t W, uint32_t* w, cudaStream_t s) {
+  if (!g.m) return;
+  k_weights<<<grid_for(g.m), kThreads, 0, s>>>(g.m, kind, W, g.adj, g.indeg, w);
+  DFS_CUDA(cudaGetLastError());
+}
+
+void launch_items_pass(const DevGraph& g, const uint32_t* w, const RankDev& r, int dir, int fasst,
+                       int write, uint32_t* cnt, const uint64_t* pos_off, Items& it,
+                       cudaStream_t s) {
+  if (!g.m) return;
+  const size_t smem = size_t(r.Jp) * sizeof(uint32_t);
+  static bool attr = false;
+  if (!attr) {
+    DFS_CUDA(cudaFuncSetAttribute(k_items<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
+    DFS_CUDA(cudaFuncSetAttribute(k_items<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
+    attr = true;
+  }
+  const int grid = grid_for(g.m);
+  if (write)
+    k_items<1><<<grid, kThreads, smem, s>>>(g.m, dir, g.tedge, g.adj, g.src, g.ehash, w, r.x, r.J,
+                                            r.Jp, fasst, cnt, pos_off, it.other, it.mask,
+                                            it.batch);
+  else
+    k_items<0><<<grid, kThreads, smem, s>>>(g.m, dir, g.tedge, g.adj, g.src, g.ehash, w, r.x, r.J,
+                                            r.Jp, fasst, cnt, pos_off, nullptr, nullptr, nullptr);
+  DFS_CUDA(cudaGetLastError());
+}
+
+void launch_row_offsets(const DevGraph& g, int dir, const uint64_t* pos_off, Items& it,
+                        uint32_t* row_cnt, cudaStream_t s) {
+  k_row_offsets<<<grid_for(uint64_t(g.n) + 1), kThreads, 0, s>>>(g.n, dir ? g.toff : g.off,
+                                                                   pos_off, it.row_off, row_cnt);
+  DFS_CUDA(cudaGetLastError());
+}
+
+void launch_chunk_write(uint32_t n, Items& it, const uint64_t* row_chunk64, cudaStream_t s) {
+  k_chunk_write<<<grid_for(uint64_t(n) + 1), kThreads, 0, s>>>(
+      n, row_chunk64, it.row_off, it.row_chunk, it.chunk_row, it.chunk_beg, it.count);
+  DFS_CUDA(cudaGetLastError());
+}
+
+void launch_fill(const RankDev& r, const unsigned int* gate, unsigned int want, cudaStream_t s) {
+  const uint64_t total = uint64_t(r.n) * (r.Jp / 4);
+  if (!total) return;
+  k_fill<<<grid_for(total), kThreads, 0, s>>>(r.n, r.J, r.Jp, r.jkey, r.vis, r.regs, gate, want,
+                                              r.ctl);
+  DFS_CUDA(cudaGetLastError());
+}
+
+int coop_grid(int which) {
+  static int g[2] = {0, 0};
+  if (!g[which]) {
+    int per = 0;
+    if (which == 0)
+      DFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_simulate, kThreads, 0));
+    else
+      DFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cascade, kThreads, 0));
+    if (per < 1) per = 1;
+    g[which] = per * num_sms();
+  }
+  return g[which];
+}
+
+void launch_simulate(const RankDev& r, int jacobi, int cap, const unsigned int* gate,
+                     unsigned int want, cudaStream_t s) {
+  SimArgs a{r, jacobi, cap, gate, want};
+  void* args[] = {&a};
+  DFS_CUDA(cudaLaunchCooperativeKernel((void*)k_simulate, dim3(coop_grid(0)), dim3(kThreads), args,
+                                       0, s));
+}
+
+void launch_score(const RankDev& r, int full, const unsigned int* gate, unsigned int want,
+                  cudaStream_t s) {
+  int lj = 0;
+  while ((1u << lj) < r.J) ++lj;
+  const int K = 53 - lj;
+  const uint64_t rows = full ? r.n : r.n;  // grid sized for the worst case
+  k_score<<<grid_for(rows * 32), kThreads, 0, s>>>(r.regs, r.n, r.J, r.Jp, K, full, r.dirty, r.ctl,
+                                                   r.scores, gate, want);
+  DFS_CUDA(cudaGetLastError());
+}
+
+void launch_treesum(const double* const* parts_dev, uint32_t mu, uint32_t n, double* out,
+                    cudaStream_t s) {
+  k_treesum<<<grid_for(n), kThreads, 0, s>>>(parts_dev, mu, n, out);
+  DFS_CUDA(cudaGetLastError());
+}
+
+void launch_argmax(const double* scores, RunArrays& ra, uint32_t n, cudaStream_t s) {
+  k_argmax<<<ra.nblk, kThreads, 0, s>>>(scores, n, ra);
+  DFS_CUDA(cudaGetLastError());
+}
+
+void launch_cascade(const RankDev& r, const unsigned int* choice, uint32_t seed, cudaStream_t s) {
+  CasArgs a{r, choice, seed};
+  void* args[] = {&a};
+  DFS_CUDA(cudaLaunchCooperativeKernel((void*)k_cascade, dim3(coop_grid(1)), dim3(kThreads), args,
+                                       0, s));
+}
+
+void launch_round_end(RunArrays& ra, RankCtl* const* ctls_dev, uint32_t mu, uint32_t k, uint32_t r,
+                      double eps, cudaStream_t s) {
+  k_round_end<<<1, 32, 0, s>>>(ra, ctls_dev, mu, k, r, eps);
+  DFS_CUDA(cudaGetLastError());
+}
+
+}  // namespace dfs

@@ -1,0 +1,532 @@
+// runtime.cpp — host runtime of the sketch-IM hot path.
+//
+// The greedy loop of proj/src/runtime.cpp:37-179 runs as a fixed sequence of
+// asynchronous launches on one stream: every decision the reference's root
+// thread takes (argmax with the committed mask, saturation fallback, the
+// eps-gated rebuild) is taken on the device and read by later kernels through
+// device-resident control blocks, so the host never waits between rounds.
+// Sample-space partitions (FASST "devices", fasst.cpp:21-88) that share one
+// GPU are executed back to back on the same stream; their scores are combined
+// in the reference's binomial order (collectives.cpp:44-64).
+#include "runtime.h"
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <numeric>
+
+#include "hash.cuh"
+
+namespace dfs {
+
+namespace {
+using Clock = std::chrono::steady_clock;
+double since(Clock::time_point t0) {
+  return std::chrono::duration<double>(Clock::now() - t0).count();
+}
+uint32_t ceil_log2(uint32_t mu) {
+  uint32_t l = 0;
+  for (uint32_t s = 1; s < mu; s <<= 1) ++l;
+  return l;
+}
+template <class T>
+T* as(void* p) {
+  return static_cast<T*>(p);
+}
+}  // namespace
+
+// ---------------------------------------------------------------- arena
+Arena::~Arena() { release(); }
+
+void Arena::release() {
+  for (auto& kv : bufs_)
+    if (kv.second.p) cudaFree(kv.second.p);
+  bufs_.clear();
+  total_ = 0;
+}
+
+void* Arena::get(const std::string& name, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  bytes = (bytes + 255) & ~size_t(255);
+  Buf& b = bufs_[name];
+  if (b.bytes < bytes) {
+    if (b.p) {
+      DFS_CUDA(cudaFree(b.p));
+      total_ -= b.bytes;
+    }
+    b.p = nullptr;
+    b.bytes = 0;
+    cudaError_t e = cudaMalloc(&b.p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw Error(kNoMem, "device allocation of " + std::to_string(bytes) + " bytes for " + name +
+                              " failed: " + cudaGetErrorString(e));
+    }
+    b.bytes = bytes;
+    total_ += bytes;
+  }
+  return b.p;
+}
+
+// ---------------------------------------------------------------- context
+Context::Context(int device) : device_(device) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    throw Error(kCuda, "no CUDA device available (the sm_100a path has no CPU fallback)");
+  }
+  if (device < 0 || device >= count) throw Error(kInvalid, "bad device ordinal");
+  DFS_CUDA(cudaSetDevice(device));
+  DFS_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+}
+
+Context::~Context() {
+  cudaSetDevice(device_);
+  if (stream_) cudaStreamSynchronize(stream_);
+  arena_.release();
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Context::sync() { DFS_CUDA(cudaStreamSynchronize(stream_)); }
+
+void Context::upload(const HostGraph& hg) {
+  DFS_CUDA(cudaSetDevice(device_));
+  auto t0 = Clock::now();
+  g_ = DevGraph{};
+  g_.n = hg.n;
+  g_.m = hg.m;
+  const size_t n1 = size_t(hg.n) + 1, m = std::max<uint64_t>(hg.m, 1);
+  g_.off = as<uint64_t>(arena_.get("g.off", n1 * 8));
+  g_.adj = as<uint32_t>(arena_.get("g.adj", m * 4));
+  g_.src = as<uint32_t>(arena_.get("g.src", m * 4));
+  g_.ehash = as<uint32_t>(arena_.get("g.ehash", m * 4));
+  g_.indeg = as<uint32_t>(arena_.get("g.indeg", n1 * 4));
+  g_.toff = as<uint64_t>(arena_.get("g.toff", n1 * 8));
+  g_.tedge = as<uint32_t>(arena_.get("g.tedge", m * 4));
+  DFS_CUDA(cudaMemcpyAsync(g_.off, hg.offsets.data(), n1 * 8, cudaMemcpyHostToDevice, stream_));
+  if (hg.m)
+    DFS_CUDA(cudaMemcpyAsync(g_.adj, hg.adj.data(), hg.m * 4, cudaMemcpyHostToDevice, stream_));
+  const size_t tb = graph_prepare_tmp_bytes(hg.m, hg.n);
+  launch_graph_prepare(g_, arena_.get("tmp.prep", tb), tb, stream_);
+  orig_id_ = hg.orig_id;
+  sync();
+  last_.upload = since(t0);
+}
+
+void Context::alloc_rank(RankDev& r, uint32_t tau) {
+  const std::string p = "r" + std::to_string(tau) + ".";
+  const uint32_t n = g_.n;
+  const size_t nn = std::max<size_t>(n, 1);
+  r.n = n;
+  r.tau = tau;
+  r.J = cfg_.r / cfg_.mu;
+  r.Jp = (r.J + kBatch - 1) / kBatch * kBatch;
+  r.W32 = r.Jp / kBatch;
+  r.j_offset = tau * r.J;
+  r.reg_key = derive_seed(cfg_.seed, kSeedTagRegisters);
+  r.x = as<uint32_t>(arena_.get(p + "x", r.Jp * 4));
+  r.jkey = as<uint64_t>(arena_.get(p + "jkey", r.Jp * 8));
+  r.regs = as<int8_t>(arena_.get(p + "regs", nn * r.Jp));
+  r.snap = cfg_.jacobi ? as<int8_t>(arena_.get(p + "snap", nn * r.Jp)) : nullptr;
+  r.vis = as<uint32_t>(arena_.get(p + "vis", nn * r.W32 * 4));
+  r.fresh[0] = as<uint32_t>(arena_.get(p + "fresh0", nn * r.W32 * 4));
+  r.fresh[1] = as<uint32_t>(arena_.get(p + "fresh1", nn * r.W32 * 4));
+  r.lstamp = as<uint32_t>(arena_.get(p + "lstamp", nn * 4));
+  r.dstamp = as<uint32_t>(arena_.get(p + "dstamp", nn * 4));
+  r.dirty = as<uint32_t>(arena_.get(p + "dirty", nn * 4));
+  r.scores = as<double>(arena_.get(p + "scores", nn * 8));
+  r.ctl = as<RankCtl>(arena_.get(p + "ctl", sizeof(RankCtl)));
+  r.q.counts = as<unsigned int>(arena_.get(p + "qcnt", 16 * 4));
+  // Host-side slice: slot values (sorted for FASST) and register keys of the
+  // global register index tau*J + j (runtime.cpp:72, sketch.cpp:55-58).
+  std::vector<uint32_t> xs(r.Jp, 0xFFFFFFFFu);
+  std::vector<uint64_t> jk(r.Jp, 0);
+  for (uint32_t j = 0; j < r.J; ++j) {
+    xs[j] = x_[size_t(tau) * r.J + j];
+    jk[j] = splitmix64_at(r.reg_key, uint64_t(r.j_offset) + j);
+  }
+  DFS_CUDA(cudaMemcpyAsync(r.x, xs.data(), r.Jp * 4, cudaMemcpyHostToDevice, stream_));
+  DFS_CUDA(cudaMemcpyAsync(r.jkey, jk.data(), r.Jp * 8, cudaMemcpyHostToDevice, stream_));
+  sync();  // host staging vectors go out of scope
+}
+
+void Context::build_items(RankDev& r, int dir) {
+  const std::string p = "r" + std::to_string(r.tau) + (dir ? ".rev." : ".fwd.");
+  Items& it = dir ? r.rev : r.fwd;
+  const uint64_t m = g_.m;
+  const uint32_t n = g_.n;
+  uint32_t* cnt = as<uint32_t>(arena_.get("tmp.cnt", (std::max<uint64_t>(m, n) + 2) * 4));
+  uint64_t* pos = as<uint64_t>(arena_.get("tmp.pos", (m + 2) * 8));
+  const size_t sb = scan_tmp_bytes(std::max<uint64_t>(m, n) + 2);
+  void* stmp = arena_.get("tmp.scan", sb);
+  DFS_CUDA(cudaMemsetAsync(cnt, 0, (m + 1) * 4, stream_));
+  launch_items_pass(g_, w_, r, dir, cfg_.fasst ? 1 : 0, 0, cnt, nullptr, it, stream_);
+  scan_u32_u64(cnt, pos, m, stmp, sb, stream_);
+  DFS_CUDA(cudaMemcpyAsync(&it.count, pos + m, 8, cudaMemcpyDeviceToHost, stream_));
+  sync();
+  const size_t ic = std::max<uint64_t>(it.count, 1);
+  it.other = as<uint32_t>(arena_.get(p + "other", ic * 4));
+  it.mask = as<uint32_t>(arena_.get(p + "mask", ic * 4));
+  it.batch = as<uint8_t>(arena_.get(p + "batch", ic));
+  it.row_off = as<uint64_t>(arena_.get(p + "row_off", (size_t(n) + 1) * 8));
+  launch_items_pass(g_, w_, r, dir, cfg_.fasst ? 1 : 0, 1, cnt, pos, it, stream_);
+  // per-row chunk counts (reuse cnt as row_cnt, n+1 entries with [n] = 0)
+  uint32_t* row_cnt = cnt;
+  DFS_CUDA(cudaMemsetAsync(row_cnt, 0, (size_t(n) + 1) * 4, stream_));
+  launch_row_offsets(g_, dir, pos, it, row_cnt, stream_);
+  uint64_t* row_chunk64 = as<uint64_t>(arena_.get("tmp.rowchunk", (size_t(n) + 2) * 8));
+  scan_u32_u64(row_cnt, row_chunk64, n, stmp, sb, stream_);
+  DFS_CUDA(cudaMemcpyAsync(&it.chunks, row_chunk64 + n, 8, cudaMemcpyDeviceToHost, stream_));
+  sync();
+  if (it.chunks >= (uint64_t(1) << 32)) throw Error(kRuntime, "too many work chunks");
+  it.chunk_row = as<uint32_t>(arena_.get(p + "chunk_row", std::max<uint64_t>(it.chunks, 1) * 4));
+  it.chunk_beg = as<uint64_t>(arena_.get(p + "chunk_beg", (it.chunks + 1) * 8));
+  it.row_chunk = as<uint32_t>(arena_.get(p + "row_chunk", (size_t(n) + 1) * 4));
+  launch_chunk_write(n, it, row_chunk64, stream_);
+}
+
+void Context::reset_rank_state(RankDev& r) {
+  const size_t nn = std::max<uint32_t>(r.n, 1);
+  DFS_CUDA(cudaMemsetAsync(r.vis, 0, nn * r.W32 * 4, stream_));
+  DFS_CUDA(cudaMemsetAsync(r.fresh[0], 0, nn * r.W32 * 4, stream_));
+  DFS_CUDA(cudaMemsetAsync(r.fresh[1], 0, nn * r.W32 * 4, stream_));
+  DFS_CUDA(cudaMemsetAsync(r.lstamp, 0, nn * 4, stream_));
+  DFS_CUDA(cudaMemsetAsync(r.dstamp, 0, nn * 4, stream_));
+  DFS_CUDA(cudaMemsetAsync(r.regs, 0, nn * r.Jp, stream_));
+  DFS_CUDA(cudaMemsetAsync(r.scores, 0, nn * 8, stream_));
+  DFS_CUDA(cudaMemsetAsync(r.q.counts, 0, 16 * 4, stream_));
+  RankCtl c{};
+  c.tick = 1;
+  DFS_CUDA(cudaMemcpyAsync(r.ctl, &c, sizeof c, cudaMemcpyHostToDevice, stream_));
+  sync();
+}
+
+void Context::prepare(const RunConfig& cfg, const HostGraph* host_w_src) {
+  if (!has_graph()) throw Error(kRuntime, "no graph uploaded");
+  DFS_CUDA(cudaSetDevice(device_));
+  // runtime.cpp:38-42, then gen_random_vector (sampling.cpp:8), make_plan
+  // (fasst.cpp:21-27) — same checks, same order, same exception classes.
+  if (cfg.k == 0 || cfg.k > g_.n) throw Error(kInvalid, "run: k must be in [1, n]");
+  if (cfg.mu == 0) throw Error(kInvalid, "run: mu must be >= 1");
+  if (!(cfg.rebuild_eps >= 0.0)) throw Error(kInvalid, "run: rebuild_eps must be >= 0");
+  if (cfg.r == 0) throw Error(kInvalid, "gen_random_vector: R must be >= 1");
+  if (cfg.r % cfg.mu != 0)
+    throw Error(kInvalid, "make_plan: mu must divide R (" + std::to_string(cfg.mu) + " vs " +
+                              std::to_string(cfg.r) + ")");
+  if (cfg.mu > 64) throw Error(kInvalid, "run: at most 64 sample-space partitions per context");
+  if (cfg.r / cfg.mu > 8192) throw Error(kInvalid, "run: at most 8192 simulations per partition");
+  auto t0 = Clock::now();
+  cfg_ = cfg;
+  // ---- plan (fasst.cpp:21-48): X_r, stable sort for FASST
+  const uint64_t xs = derive_seed(cfg.seed, kSeedTagSamples);
+  std::vector<uint32_t> x(cfg.r);
+  for (uint32_t i = 0; i < cfg.r; ++i) x[i] = random_value_at(xs, i);
+  order_.resize(cfg.r);
+  std::iota(order_.begin(), order_.end(), 0u);
+  degraded_ = false;
+  if (cfg.fasst) {
+    std::stable_sort(order_.begin(), order_.end(),
+                     [&](uint32_t a, uint32_t b) { return x[a] < x[b]; });
+    degraded_ = (cfg.r / cfg.mu) < 32;
+  }
+  x_.resize(cfg.r);
+  for (uint32_t i = 0; i < cfg.r; ++i) x_[i] = x[order_[i]];
+  // ---- weights (apply_weights, runtime.cpp:15-17)
+  w_ = as<uint32_t>(arena_.get("g.w", std::max<uint64_t>(g_.m, 1) * 4));
+  switch (cfg.weights.kind) {
+    case WeightKind::Constant:
+      launch_weights(g_, 0, to_fixed_point(cfg.weights.a), w_, stream_);
+      break;
+    case WeightKind::WeightedCascade: launch_weights(g_, 1, 0, w_, stream_); break;
+    default: {
+      if (!host_w_src) throw Error(kRuntime, "randomized weights need the host graph");
+      std::vector<uint32_t> hw;
+      assign_weights(*host_w_src, cfg.weights, derive_seed(cfg.seed, kSeedTagWeights), hw);
+      DFS_CUDA(cudaMemcpyAsync(w_, hw.data(), g_.m * 4, cudaMemcpyHostToDevice, stream_));
+      sync();
+    }
+  }
+  // ---- per-rank state and sampled items (fasst.cpp:50-88, build phase)
+  ranks_.assign(cfg.mu, RankDev{});
+  for (uint32_t t = 0; t < cfg.mu; ++t) {
+    RankDev& r = ranks_[t];
+    alloc_rank(r, t);
+    build_items(r, 0);
+    build_items(r, 1);
+    const std::string p = "r" + std::to_string(t) + ".q.";
+    const uint64_t cap = std::max<uint64_t>(std::max(r.fwd.chunks, r.rev.chunks), 1);
+    for (int gi = 0; gi < 3; ++gi) {
+      r.q.chunks[gi] = as<uint32_t>(arena_.get(p + "c" + std::to_string(gi), cap * 4));
+      r.q.rows[gi] = as<uint32_t>(arena_.get(p + "r" + std::to_string(gi),
+                                             std::max<uint32_t>(g_.n, 1) * 4));
+    }
+    reset_rank_state(r);
+  }
+  prep_seconds_ = since(t0);
+}
+
+Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
+  auto t_total = Clock::now();
+  prepare(cfg, host_w_src);
+  const uint32_t n = g_.n, mu = cfg.mu, k = cfg.k;
+  cudaStream_t s = stream_;
+
+  // ---- run-level device state
+  RunArrays ra;
+  ra.ctl = as<RunCtl>(arena_.get("run.ctl", sizeof(RunCtl)));
+  ra.committed = as<uint8_t>(arena_.get("run.committed", std::max<uint32_t>(n, 1)));
+  ra.seeds = as<uint32_t>(arena_.get("run.seeds", k * 4));
+  ra.traj = as<double>(arena_.get("run.traj", k * 8));
+  ra.rebuild_rounds = as<uint32_t>(arena_.get("run.rb", k * 4));
+  ra.nblk = 4 * 148;
+  ra.blk_score = as<double>(arena_.get("run.bs", ra.nblk * 8));
+  ra.blk_arg = as<uint32_t>(arena_.get("run.ba", ra.nblk * 4));
+  ra.blk_min = as<uint32_t>(arena_.get("run.bm", ra.nblk * 4));
+  DFS_CUDA(cudaMemsetAsync(ra.ctl, 0, sizeof(RunCtl), s));
+  DFS_CUDA(cudaMemsetAsync(ra.committed, 0, std::max<uint32_t>(n, 1), s));
+  const double* argmax_src = ranks_[0].scores;
+  std::vector<RankCtl*> hctl(mu);
+  std::vector<const double*> hparts(mu);
+  for (uint32_t t = 0; t < mu; ++t) {
+    hctl[t] = ranks_[t].ctl;
+    hparts[t] = ranks_[t].scores;
+  }
+  RankCtl** dctl = as<RankCtl*>(arena_.get("run.ctls", mu * sizeof(void*)));
+  const double** dparts = as<const double*>(arena_.get("run.parts", mu * sizeof(void*)));
+  DFS_CUDA(cudaMemcpyAsync(dctl, hctl.data(), mu * sizeof(void*), cudaMemcpyHostToDevice, s));
+  DFS_CUDA(cudaMemcpyAsync(dparts, hparts.data(), mu * sizeof(void*), cudaMemcpyHostToDevice, s));
+  if (mu > 1) {
+    ra.reduced = as<double>(arena_.get("run.reduced", std::max<uint32_t>(n, 1) * 8));
+    argmax_src = ra.reduced;
+  }
+  const unsigned int* rebuild = &ra.ctl->rebuild_now;
+
+  // phase events: [0] start, per round 4 boundaries, plus the initial ones
+  std::vector<cudaEvent_t> ev;
+  auto mark = [&]() {
+    cudaEvent_t e;
+    DFS_CUDA(cudaEventCreate(&e));
+    DFS_CUDA(cudaEventRecord(e, s));
+    ev.push_back(e);
+    return ev.size() - 1;
+  };
+  PhaseTimings pt;
+  pt.build = prep_seconds_;
+  struct Span {
+    size_t a, b;
+    double* acc;
+  };
+  std::vector<Span> spans;
+
+  size_t e0 = mark();
+  for (uint32_t t = 0; t < mu; ++t) launch_fill(ranks_[t], nullptr, 0, s);
+  size_t e1 = mark();
+  for (uint32_t t = 0; t < mu; ++t) launch_simulate(ranks_[t], cfg.jacobi, cfg.sim_cap, nullptr, 0, s);
+  size_t e2 = mark();
+  for (uint32_t t = 0; t < mu; ++t) launch_score(ranks_[t], 1, nullptr, 0, s);
+  spans.push_back({e0, e1, &pt.fill});
+  spans.push_back({e1, e2, &pt.simulate});
+  size_t prev = e2;
+  for (uint32_t step = 0; step < k; ++step) {
+    // select: rescore dirty rows, binomial-order sum, argmax (runtime.cpp:88-122)
+    for (uint32_t t = 0; t < mu; ++t) launch_score(ranks_[t], 0, rebuild, 0, s);
+    if (mu > 1) launch_treesum(dparts, mu, n, ra.reduced, s);
+    launch_argmax(argmax_src, ra, n, s);
+    size_t a = mark();
+    spans.push_back({prev, a, &pt.select});
+    // commit + cascade (runtime.cpp:124-127) and the covered-count allreduce
+    for (uint32_t t = 0; t < mu; ++t) launch_cascade(ranks_[t], &ra.ctl->choice, 0, s);
+    launch_round_end(ra, dctl, mu, k, cfg.r, cfg.rebuild_eps, s);
+    size_t b = mark();
+    spans.push_back({a, b, &pt.cascade});
+    prev = b;
+    if (step + 1 < k) {  // eps-gated rebuild (runtime.cpp:139-153), predicated on device
+      for (uint32_t t = 0; t < mu; ++t) launch_fill(ranks_[t], rebuild, 1, s);
+      size_t c = mark();
+      for (uint32_t t = 0; t < mu; ++t)
+        launch_simulate(ranks_[t], cfg.jacobi, cfg.sim_cap, rebuild, 1, s);
+      size_t d = mark();
+      for (uint32_t t = 0; t < mu; ++t) launch_score(ranks_[t], 1, rebuild, 1, s);
+      spans.push_back({b, c, &pt.fill});
+      spans.push_back({c, d, &pt.simulate});
+      prev = d;
+    }
+  }
+  size_t eend = mark();
+  sync();
+
+  // ---- results
+  Report rep;
+  rep.config = cfg;
+  rep.n = n;
+  rep.m = g_.m;
+  rep.degraded_plan = degraded_;
+  RunCtl rc{};
+  DFS_CUDA(cudaMemcpy(&rc, ra.ctl, sizeof rc, cudaMemcpyDeviceToHost));
+  rep.seeds_dense.resize(k);
+  rep.score_trajectory.resize(k);
+  DFS_CUDA(cudaMemcpy(rep.seeds_dense.data(), ra.seeds, k * 4, cudaMemcpyDeviceToHost));
+  DFS_CUDA(cudaMemcpy(rep.score_trajectory.data(), ra.traj, k * 8, cudaMemcpyDeviceToHost));
+  rep.rebuilds = rc.n_rebuilds;
+  rep.rebuild_rounds.resize(rc.n_rebuilds);
+  if (rc.n_rebuilds)
+    DFS_CUDA(cudaMemcpy(rep.rebuild_rounds.data(), ra.rebuild_rounds, rc.n_rebuilds * 4,
+                        cudaMemcpyDeviceToHost));
+  rep.saturated = rc.saturated != 0;
+  for (uint32_t t = 0; t < mu; ++t) {
+    RankCtl c{};
+    DFS_CUDA(cudaMemcpy(&c, ranks_[t].ctl, sizeof c, cudaMemcpyDeviceToHost));
+    if (c.error) {
+      for (cudaEvent_t e : ev) cudaEventDestroy(e);
+      throw Error(kRuntime, "simulate did not converge within " + std::to_string(cfg.sim_cap) +
+                                " iterations; register monotonicity must be broken");
+    }
+    rep.sketch_edge_updates += c.updates;
+    rep.items_processed += c.items_processed;
+    rep.sweeps_total += c.total_sweeps;
+    rep.items_fwd += ranks_[t].fwd.count;
+    rep.items_rev += ranks_[t].rev.count;
+  }
+  for (uint32_t sd : rep.seeds_dense) rep.seeds.push_back(orig_id_[sd]);
+  // comms counters of the reference's collective schedule (collectives.cpp:
+  // 19,62,76,107; pinned by tests/test_runtime.cpp:169-180).
+  rep.reduced_elements = uint64_t(k) * (uint64_t(n) + 1) * (mu - 1);
+  rep.broadcast_elements = uint64_t(k) * 2 * (mu - 1);
+  rep.barriers = uint64_t(k) * (8 + ceil_log2(mu));
+  for (const Span& sp : spans) {
+    float ms = 0;
+    DFS_CUDA(cudaEventElapsedTime(&ms, ev[sp.a], ev[sp.b]));
+    *sp.acc += ms * 1e-3;
+  }
+  (void)eend;
+  for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  pt.upload = last_.upload;
+  pt.total = since(t_total);
+  rep.timings = pt;
+  last_ = pt;
+  return rep;
+}
+
+// ---------------------------------------------------------------- stage API
+static void check_tau(uint32_t tau, size_t n) {
+  if (tau >= n) throw Error(kIndex, "rank index out of range (prepare first)");
+}
+
+void Context::stage_fill(uint32_t tau) {
+  check_tau(tau, ranks_.size());
+  launch_fill(ranks_[tau], nullptr, 0, stream_);
+  sync();
+}
+
+int Context::stage_simulate(uint32_t tau, int cap, int jacobi) {
+  check_tau(tau, ranks_.size());
+  RankDev& r = ranks_[tau];
+  if (jacobi && !r.snap) {
+    r.snap = as<int8_t>(arena_.get("r" + std::to_string(tau) + ".snap",
+                                   std::max<size_t>(r.n, 1) * r.Jp));
+  }
+  launch_simulate(r, jacobi, cap, nullptr, 0, stream_);
+  RankCtl c{};
+  DFS_CUDA(cudaMemcpyAsync(&c, r.ctl, sizeof c, cudaMemcpyDeviceToHost, stream_));
+  sync();
+  if (c.error) {
+    int zero = 0;
+    DFS_CUDA(cudaMemcpy(&r.ctl->error, &zero, sizeof zero, cudaMemcpyHostToDevice));
+    return -1;
+  }
+  return int(c.sweeps);
+}
+
+void Context::stage_scores(uint32_t tau, double* out) {
+  check_tau(tau, ranks_.size());
+  launch_score(ranks_[tau], 1, nullptr, 0, stream_);
+  DFS_CUDA(cudaMemcpyAsync(out, ranks_[tau].scores, size_t(g_.n) * 8, cudaMemcpyDeviceToHost,
+                           stream_));
+  sync();
+}
+
+uint64_t Context::stage_commit_cascade(uint32_t tau, uint32_t seed) {
+  check_tau(tau, ranks_.size());
+  if (seed >= g_.n) throw Error(kIndex, "seed id out of range");
+  launch_cascade(ranks_[tau], nullptr, seed, stream_);
+  sync();
+  return stage_visited(tau);
+}
+
+uint64_t Context::stage_visited(uint32_t tau) {
+  check_tau(tau, ranks_.size());
+  RankCtl c{};
+  DFS_CUDA(cudaMemcpy(&c, ranks_[tau].ctl, sizeof c, cudaMemcpyDeviceToHost));
+  return c.visited;
+}
+
+void Context::stage_get_registers(uint32_t tau, int8_t* out) {
+  check_tau(tau, ranks_.size());
+  const RankDev& r = ranks_[tau];
+  if (!r.n) return;
+  DFS_CUDA(cudaMemcpy2DAsync(out, r.J, r.regs, r.Jp, r.J, r.n, cudaMemcpyDeviceToHost, stream_));
+  sync();
+}
+
+void Context::stage_set_registers(uint32_t tau, const int8_t* in) {
+  check_tau(tau, ranks_.size());
+  RankDev& r = ranks_[tau];
+  if (!r.n) return;
+  // registers + the VISITED bitset mirror + running count (sketch.hpp:35-87)
+  std::vector<int8_t> full(size_t(r.n) * r.Jp, int8_t(-1));
+  std::vector<uint32_t> vis(size_t(r.n) * r.W32, 0);
+  uint64_t visited = 0;
+  for (uint32_t u = 0; u < r.n; ++u)
+    for (uint32_t j = 0; j < r.J; ++j) {
+      const int8_t v = in[size_t(u) * r.J + j];
+      full[size_t(u) * r.Jp + j] = v;
+      if (v == -1) {
+        vis[size_t(u) * r.W32 + j / 32] |= 1u << (j % 32);
+        ++visited;
+      }
+    }
+  DFS_CUDA(cudaMemcpy(r.regs, full.data(), full.size(), cudaMemcpyHostToDevice));
+  DFS_CUDA(cudaMemcpy(r.vis, vis.data(), vis.size() * 4, cudaMemcpyHostToDevice));
+  DFS_CUDA(cudaMemcpy(&r.ctl->visited, &visited, 8, cudaMemcpyHostToDevice));
+}
+
+// Reference layout of the device graph (engine.hpp:14-29): CSR of the edges
+// live in >= 1 local simulation plus u64 liveness masks, rebuilt on the host
+// from the forward items (edges appear as consecutive items of their row).
+void Context::stage_device_graph(uint32_t tau, std::vector<uint64_t>& off,
+                                 std::vector<uint32_t>& adj, std::vector<uint64_t>& mask,
+                                 uint32_t* words_out) {
+  check_tau(tau, ranks_.size());
+  const RankDev& r = ranks_[tau];
+  const Items& it = r.fwd;
+  const uint32_t words = (r.J + 63) / 64;
+  std::vector<uint64_t> roff(size_t(r.n) + 1);
+  std::vector<uint32_t> other(it.count), mk(it.count);
+  std::vector<uint8_t> b(it.count);
+  DFS_CUDA(cudaMemcpy(roff.data(), it.row_off, roff.size() * 8, cudaMemcpyDeviceToHost));
+  if (it.count) {
+    DFS_CUDA(cudaMemcpy(other.data(), it.other, it.count * 4, cudaMemcpyDeviceToHost));
+    DFS_CUDA(cudaMemcpy(mk.data(), it.mask, it.count * 4, cudaMemcpyDeviceToHost));
+    DFS_CUDA(cudaMemcpy(b.data(), it.batch, it.count, cudaMemcpyDeviceToHost));
+  }
+  off.assign(size_t(r.n) + 1, 0);
+  adj.clear();
+  mask.clear();
+  for (uint32_t u = 0; u < r.n; ++u) {
+    off[u] = adj.size();
+    for (uint64_t i = roff[u]; i < roff[u + 1]; ++i) {
+      if (i == roff[u] || other[i] != other[i - 1]) {
+        adj.push_back(other[i]);
+        mask.resize(mask.size() + words, 0);
+      }
+      const uint32_t j0 = uint32_t(b[i]) * 32;
+      uint64_t* mw = mask.data() + mask.size() - words;
+      mw[j0 / 64] |= uint64_t(mk[i]) << (j0 % 64);
+    }
+  }
+  off[r.n] = adj.size();
+  *words_out = words;
+}
+
+}  // namespace dfs

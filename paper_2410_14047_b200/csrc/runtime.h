@@ -1,0 +1,123 @@
+// runtime.h — host runtime: device context, resident graph, sample-space
+// partitions ("ranks", FASST, proj/src/fasst.cpp:21-88) and the greedy loop
+// of proj/src/runtime.cpp:37-179 driven entirely from the device (no host
+// round-trips between rounds).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "dfs.h"
+#include "graph.h"
+
+namespace dfs {
+
+// Grow-only named device buffers: repeated runs at the same sizes reuse them.
+class Arena {
+ public:
+  ~Arena();
+  void* get(const std::string& name, size_t bytes);
+  size_t bytes() const { return total_; }
+  void release();
+
+ private:
+  struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+  };
+  std::unordered_map<std::string, Buf> bufs_;
+  size_t total_ = 0;
+};
+
+struct RunConfig {  // proj/include/difuser/runtime.hpp:13-22
+  uint32_t k = 1, r = 256, mu = 1;
+  bool fasst = true;
+  WeightSetting weights{};
+  double rebuild_eps = 0.01;
+  uint64_t seed = 0;
+  int sim_cap = 256;
+  int jacobi = 0;  // 1: exact reference sweep schedule (parity/debug)
+};
+
+struct PhaseTimings {  // runtime.hpp:24-27 (seconds; device-event based)
+  double build = 0, fill = 0, simulate = 0, select = 0, cascade = 0, total = 0;
+  double upload = 0;  // H2D + graph preparation (outside run() scope)
+};
+
+struct Report {  // runtime.hpp:29-41
+  RunConfig config;
+  uint64_t n = 0, m = 0;
+  std::vector<uint64_t> seeds;
+  std::vector<uint32_t> seeds_dense;
+  std::vector<double> score_trajectory;
+  std::vector<uint32_t> rebuild_rounds;
+  uint32_t rebuilds = 0;
+  bool saturated = false, degraded_plan = false;
+  uint64_t reduced_elements = 0, broadcast_elements = 0, barriers = 0;
+  PhaseTimings timings;
+  // instrumentation (not part of the JSON contract)
+  uint64_t sketch_edge_updates = 0, items_processed = 0, sweeps_total = 0;
+  uint64_t items_fwd = 0, items_rev = 0, device_edges = 0;
+};
+
+std::string report_to_json(const Report& rep, bool include_timings);
+
+class Context {
+ public:
+  explicit Context(int device);
+  ~Context();
+  int device() const { return device_; }
+  cudaStream_t stream() const { return stream_; }
+
+  // H2D of the CSR (offsets, adj) + on-device ehash, in-degree, transpose.
+  void upload(const HostGraph& g);
+  bool has_graph() const { return g_.n > 0; }
+
+  // Plan + weights + per-rank sampled items (the reference's "build" phase).
+  void prepare(const RunConfig& cfg, const HostGraph* host_w_src = nullptr);
+  // Full greedy run on the resident graph.
+  Report run(const RunConfig& cfg, const HostGraph* host_w_src = nullptr);
+
+  // ---- stage API (parity harness), rank tau of the prepared session
+  uint32_t ranks() const { return uint32_t(ranks_.size()); }
+  void stage_fill(uint32_t tau);
+  int stage_simulate(uint32_t tau, int cap, int jacobi);
+  void stage_scores(uint32_t tau, double* out);
+  uint64_t stage_commit_cascade(uint32_t tau, uint32_t seed);
+  uint64_t stage_visited(uint32_t tau);
+  void stage_get_registers(uint32_t tau, int8_t* out);
+  void stage_set_registers(uint32_t tau, const int8_t* in);
+  void stage_device_graph(uint32_t tau, std::vector<uint64_t>& off, std::vector<uint32_t>& adj,
+                          std::vector<uint64_t>& mask, uint32_t* words);
+  void stage_plan(std::vector<uint32_t>& x, std::vector<uint32_t>& order, bool* degraded) const {
+    x = x_;
+    order = order_;
+    *degraded = degraded_;
+  }
+  const PhaseTimings& last_timings() const { return last_; }
+  void sync();
+
+ private:
+  void build_items(RankDev& r, int dir);
+  void alloc_rank(RankDev& r, uint32_t tau);
+  void reset_rank_state(RankDev& r);
+
+  int device_ = 0;
+  cudaStream_t stream_ = nullptr;
+  Arena arena_;
+  DevGraph g_{};
+  std::vector<uint64_t> orig_id_;
+  uint32_t* w_ = nullptr;  // weights of the prepared config
+  RunConfig cfg_{};
+  std::vector<uint32_t> x_, order_;
+  bool degraded_ = false;
+  std::vector<RankDev> ranks_;
+  PhaseTimings last_{};
+  double prep_seconds_ = 0;
+};
+
+}  // namespace dfs

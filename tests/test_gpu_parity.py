@@ -1,0 +1,216 @@
+"""GPU parity: the sm_100a path through the C-ABI vs the reference's golden
+fixtures (tests/golden, produced by the compiled reference) and vs the oracle
+restatement (oracle/, checked against the same fixtures in
+test_oracle_golden.py).  Integer/byte state is compared bit-exactly; scores
+are compared as IEEE bit patterns; reports byte-identically (minus timings).
+"""
+import json
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _graph(D, gd):
+    return D.graph_from_csr(np.array(gd["offsets"], np.uint64), np.array(gd["adj"], np.uint32),
+                            np.array(gd["orig_ids"], np.uint64))
+
+
+@pytest.fixture(scope="module")
+def D():
+    import paper_2410_14047_b200 as D
+    return D
+
+
+def test_run_json_byte_identical(D, ctx, golden):
+    runs = golden["runs"]
+    for case in runs["cases"]:
+        g = _graph(D, runs["graphs"][case["graph"]])
+        got = ctx.run_json(g, timings=False, **case["config"])
+        assert got == case["json"], (case["graph"], case["config"])
+
+
+def test_run_json_jacobi_schedule_same_report(D, ctx, golden):
+    runs = golden["runs"]
+    for case in runs["cases"][:12]:
+        g = _graph(D, runs["graphs"][case["graph"]])
+        got = ctx.run_json(g, timings=False, jacobi=1, **case["config"])
+        assert got == case["json"], (case["graph"], case["config"])
+
+
+def test_stage_traces(D, ctx, golden):
+    graphs = golden["runs"]["graphs"]
+    for tr in golden["traces"]:
+        g = _graph(D, graphs[tr["graph"]])
+        ctx.prepare(g, r=tr["r"], devices=tr["mu"], mode=tr["mode"], weights=tr["weights"],
+                    seed=tr["seed"])
+        tau, J = tr["tau"], tr["r"] // tr["mu"]
+        # sampled-edge set: device graph + baked masks (fasst.cpp:50-88)
+        off, adj, mask, words = ctx.device_graph(tau)
+        assert words == tr["mask_words"]
+        assert off.tolist() == tr["dg_offsets"]
+        assert adj.tolist() == tr["dg_adj"]
+        assert mask.tolist() == tr["dg_mask"]
+        # fill (sketch.cpp:55-66)
+        ctx.fill(tau)
+        assert ctx.registers(tau).tobytes().hex() == tr["regs_fill"]
+        # simulate: async schedule -> same registers; Jacobi -> same sweep count too
+        sweeps = ctx.simulate(tau)
+        assert 1 <= sweeps <= tr["sweeps"]
+        assert ctx.registers(tau).tobytes().hex() == tr["regs_sim"]
+        ctx.fill(tau)
+        assert ctx.simulate(tau, jacobi=1) == tr["sweeps"]
+        assert ctx.registers(tau).tobytes().hex() == tr["regs_sim"]
+        # row scores, bit-exact doubles (sketch.cpp:119-131)
+        assert [float(s).hex() for s in ctx.scores(tau)] == tr["scores"]
+        # commit + cascade (engine.cpp:106-144)
+        for s, regs, vis in zip(tr["seeds"], tr["regs_cascade"], tr["visited"]):
+            assert ctx.commit_cascade(tau, s) == vis
+            assert ctx.registers(tau).tobytes().hex() == regs
+        assert J == len(tr["regs_fill"]) // 2 // g.n
+
+
+def _oracle_csr(g):
+    return O.CSR(g.offsets, g.adj, np.array(g.orig_ids, np.uint64))
+
+
+@pytest.mark.parametrize("devices", [1, 8])
+def test_c1_config_matches_oracle(D, ctx, devices):
+    """BASELINE configs[0]: ER n=10k avg-deg 8, IC p=0.1, R=64, K=10."""
+    g = D.generate("er", 10000, 80000, 7)
+    got = json.loads(ctx.run_json(g, k=10, r=64, devices=devices, weights="const:0.1", seed=7,
+                                  timings=False))
+    ref = O.run(_oracle_csr(g), k=10, r=64, devices=devices, weights="const:0.1", seed=7)
+    for key, val in ref.items():
+        assert got[key] == val, key
+
+
+@pytest.mark.parametrize("spec", [
+    dict(n=3000, m=24000, k=12, r=256, devices=1, weights="const:0.05"),
+    dict(n=3000, m=24000, k=12, r=256, devices=2, weights="wc"),
+    dict(n=2000, m=30000, k=8, r=96, devices=3, weights="const:0.2", mode="naive"),
+    dict(n=5000, m=20000, k=15, r=1024, devices=4, weights="const:0.01"),
+    dict(n=1500, m=9000, k=10, r=100, devices=1, weights="const:0.3", rebuild_eps=0.0),
+])
+def test_random_configs_match_oracle(D, ctx, spec):
+    spec = dict(spec)
+    n, m = spec.pop("n"), spec.pop("m")
+    g = D.generate("er", n, m, 11)
+    got = json.loads(ctx.run_json(g, seed=5, timings=False, **spec))
+    ref = O.run(_oracle_csr(g), seed=5, **spec)
+    for key, val in ref.items():
+        assert got[key] == val, key
+
+
+def test_rmat_registers_match_oracle(D, ctx):
+    g = D.generate("rmat", 12, 40000, 3)
+    cg = _oracle_csr(g)
+    for r, mu, w in [(256, 1, "const:0.01"), (512, 2, "wc"), (64, 1, "const:0.2")]:
+        ctx.prepare(g, r=r, devices=mu, weights=w, seed=9)
+        wf = cg.weights(w)
+        x, _, _ = O.make_plan(r, mu, "fasst", 9)
+        J = r // mu
+        for tau in range(mu):
+            off, adj, mask = O.device_graph(cg, wf, x[tau * J:(tau + 1) * J])
+            goff, gadj, gmask, _ = ctx.device_graph(tau)
+            assert np.array_equal(off, goff) and np.array_equal(adj, gadj)
+            assert np.array_equal(mask, gmask)
+            regs = O.fill(g.n, J, tau * J, O.splitmix64_at(9, 2))
+            ctx.fill(tau)
+            assert np.array_equal(ctx.registers(tau), regs)
+            sweeps = O.simulate(g.n, off, adj, mask, J, regs)
+            assert ctx.simulate(tau) <= sweeps
+            assert np.array_equal(ctx.registers(tau), regs)
+            ctx.fill(tau)
+            assert ctx.simulate(tau, jacobi=1) == sweeps
+            sc = ctx.scores(tau)
+            want = [O.row_score(regs[u * J:(u + 1) * J]) for u in range(g.n)]
+            assert sc.tolist() == want
+
+
+def test_pre_visited_registers_respected(D, ctx):
+    """engine test 'simulate respects pre-VISITED registers'."""
+    g = D.generate("er", 20, 60, 3)
+    ctx.prepare(g, r=64, weights="const:0.8", seed=9)
+    rng = np.random.default_rng(4)
+    regs = np.zeros(g.n * 64, np.int8)
+    for _ in range(200):
+        regs[rng.integers(g.n) * 64 + rng.integers(64)] = -1
+    before = int((regs == -1).sum())
+    ctx.set_registers(0, regs)
+    ctx.fill(0)
+    cg = _oracle_csr(g)
+    x, _, _ = O.make_plan(64, 1, "fasst", 9)
+    off, adj, mask = O.device_graph(cg, cg.weights("const:0.8"), x)
+    ref = regs.copy()
+    O.fill(g.n, 64, 0, O.splitmix64_at(9, 2), ref)
+    O.simulate(g.n, off, adj, mask, 64, ref)
+    ctx.simulate(0)
+    got = ctx.registers(0)
+    assert np.array_equal(got, ref)
+    assert int((got == -1).sum()) == before == ctx.visited_count(0)
+
+
+def test_simulate_cap_and_depth():
+    """Chain of 12, max planted at the tail: Jacobi needs depth+1 = 12 sweeps,
+    cap 3 raises (tests/test_engine.cpp:114-134)."""
+    import paper_2410_14047_b200 as D
+    ctx = D.Context(0)
+    g = D.graph_from_csr(np.array(list(range(12)) + [11], np.uint64),
+                         np.arange(1, 12, dtype=np.uint32), list(range(12)))
+    ctx.prepare(g, r=64, weights="const:1", seed=5)
+    regs = np.zeros(12 * 64, np.int8)
+    regs[11 * 64] = 50
+    ctx.set_registers(0, regs)
+    with pytest.raises(RuntimeError):
+        ctx.simulate(0, cap=3, jacobi=1)
+    ctx.set_registers(0, regs)
+    assert ctx.simulate(0, cap=64, jacobi=1) == 12
+    assert all(ctx.registers(0)[u * 64] == 50 for u in range(12))
+
+
+def test_recommit_covered_seed_is_noop(D, ctx):
+    g = D.graph_from_csr(np.array([0, 1, 2, 3, 4, 5, 5], np.uint64),
+                         np.arange(1, 6, dtype=np.uint32), list(range(6)))
+    ctx.prepare(g, r=32, weights="const:1", seed=2)
+    ctx.fill(0)
+    assert ctx.commit_cascade(0, 0) == 6 * 32
+    assert ctx.commit_cascade(0, 3) == 6 * 32
+
+
+def test_validation_errors(D, ctx):
+    g = D.graph_from_text("0 1\n1 2\n2 3\n")
+    with pytest.raises(ValueError):
+        ctx.run_json(g, k=0, r=64)
+    with pytest.raises(ValueError):
+        ctx.run_json(g, k=5, r=64)
+    with pytest.raises(ValueError):
+        ctx.run_json(g, k=1, r=64, devices=0)
+    with pytest.raises(ValueError):
+        ctx.run_json(g, k=1, r=63, devices=2)
+    with pytest.raises(ValueError):
+        ctx.run_json(g, k=1, r=64, rebuild_eps=-0.5)
+    with pytest.raises(ValueError):
+        ctx.run_json(g, k=1, r=0)
+    with pytest.raises(RuntimeError):
+        ctx.run_json(g, k=1, r=64, mode="bogus")
+    with pytest.raises(RuntimeError):
+        ctx.run_json(g, k=1, r=64, weights="const:2")
+
+
+def test_python_smoke_mirror(D):
+    """tests/py/test_smoke.py:40-51 through the package-level API."""
+    chain = D.graph_from_text("0 1\n1 2\n2 3\n", directed=True)
+    rep = D.run(chain, k=2, r=64, weights="const:1", seed=3)
+    assert rep["seeds"][0] == 0
+    assert rep["config"]["k"] == 2
+    assert len(rep["score_trajectory"]) == 2
+    assert rep["score_trajectory"][0] == pytest.approx(4.0)
+    assert rep["saturated"]
+    quiet = json.loads(D.run_json(chain, k=2, r=64, weights="const:1", seed=3, timings=False))
+    assert "timings" not in quiet
+    assert quiet["seeds"] == rep["seeds"]
+    assert set(rep["timings"]) == {"build", "fill", "simulate", "select", "cascade", "total"}
