@@ -1,0 +1,373 @@
+#!/usr/bin/env python3
+"""bench.py — end-to-end sketch-IM on B200 (BASELINE.json metric).
+
+One step = one full greedy influence-maximisation run, the reference's
+``run()`` scope (proj/src/runtime.cpp:37-179: device-graph build, fill,
+simulate to convergence, K rounds of score/argmax/commit/cascade and eps-gated
+rebuilds) on the configuration BASELINE.json quotes for one GPU (configs[1]):
+R-MAT scale-20, 16M edges, IC p=0.01, R=256 simulations, K=50 seeds.
+
+  value  -- seconds per IM run with the graph resident in HBM (lower is better)
+  e2e    -- the same through the drop-in API run_json(host graph): pinned host
+            CSR -> H2D -> run -> report readback, every step
+  --impl reference -- the reference's own CPU implementation (oracle/_ref,
+            compiled from /root/reference) on the host cores, same workload.
+
+Multi-GPU (torchrun, N ranks): FASST sample-space partitioning, devices = N,
+one partition per GPU (paper_2410_14047_b200.dist).  Timing is the max over
+ranks of CUDA-event time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "end-to-end IM seconds for K=50 and sketch-edge updates/sec at 1/2/4/8 B200"
+CONFIGS = {
+    # name: (generator, a, m, weights, r, k, description)
+    "c2": ("rmat", 20, 16_000_000, "const:0.01", 256, 50,
+           "C2: R-MAT scale-20 (16M edges), IC p=0.01, R=256, K=50"),
+    "c1": ("er", 10_000, 80_000, "const:0.1", 64, 10,
+           "C1: Erdos-Renyi n=10k avg-deg 8, IC p=0.1, R=64, K=10"),
+    "c3": ("rmat", 23, 100_000_000, "wc", 1024, 50,
+           "C3: R-MAT scale-23 (100M edges), weighted cascade, R=1024, K=50"),
+    "c3ic": ("rmat", 23, 100_000_000, "const:0.01", 1024, 50,
+             "north star: R-MAT scale-23 (100M edges), IC p=0.01, R=1024, K=50"),
+}
+SEED = 7
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), \
+        int(os.environ.get("LOCAL_RANK", 0))
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def make_graph(D, cfgname):
+    gen, a, m, *_ = CONFIGS[cfgname]
+    t0 = time.time()
+    g = D.generate(gen, a, m, SEED)
+    log(f"[bench] generated {cfgname}: n={g.n} m={g.m} in {time.time() - t0:.1f}s")
+    return g
+
+
+# ----------------------------------------------------------------- reference arm
+def reference_devices(r):
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    d = 1
+    while d * 2 <= min(cores, 64, r):
+        d *= 2
+    return d
+
+
+def run_reference(D, cfgname, steps, warmup, graph=None):
+    """The reference's own run_json (compiled from /root/reference into
+    oracle/_ref) on host threads; falls back to the plain-C oracle port."""
+    import oracle as O
+    gen, a, m, wspec, r, k, desc = CONFIGS[cfgname]
+    g = graph if graph is not None else make_graph(D, cfgname)
+    ref, _ = O.load_reference()
+    devices = reference_devices(r)
+    times = []
+    if ref is not None:
+        path = f"/tmp/difuser_bench_{cfgname}_{os.getpid()}.bin"
+        D.save_cache(g, path)
+        rg = ref.load_graph(path)
+        os.unlink(path)
+        kind = "reference"
+        for i in range(warmup + steps):
+            t0 = time.perf_counter()
+            rep = json.loads(ref.run_json(rg, k=k, r=r, devices=devices, mode="fasst",
+                                          weights=wspec, rebuild_eps=0.01, seed=SEED,
+                                          timings=True))
+            dt = time.perf_counter() - t0
+            if i >= warmup:
+                times.append(dt)
+        inner = rep["timings"]
+    else:
+        import numpy as np
+        kind = "port"
+        devices = 1
+        cg = O.CSR(g.offsets, g.adj, np.array(g.orig_ids, np.uint64))
+        for i in range(warmup + steps):
+            t0 = time.perf_counter()
+            O.run(cg, k=k, r=r, devices=1, weights=wspec, seed=SEED)
+            dt = time.perf_counter() - t0
+            if i >= warmup:
+                times.append(dt)
+        inner = None
+    value = statistics.mean(times)
+    return {"value": value, "unit": "s", "cores": devices, "kind": kind,
+            "sample": f"full {desc} run_json(devices={devices}) x{steps}"
+                      f" (reference timings.total of last step: "
+                      f"{inner['total'] if inner else 'n/a'})"}
+
+
+# ----------------------------------------------------------------- our arm
+def algorithmic_bytes(D, ctx, g, cfgname, devices):
+    """Reference-schedule work units of SURVEY.md §8(d), counted by an
+    instrumented Jacobi replay (same schedule as proj/src/engine.cpp:57-96)."""
+    gen, a, m, wspec, r, k, desc = CONFIGS[cfgname]
+    ctx.run_json(None, k=k, r=r, devices=devices, weights=wspec, seed=SEED, timings=False,
+                 jacobi=1, count=1, resident=True)
+    st = ctx.stats()
+    E, B, T, S = st["cnt_edges"], st["cnt_batches"], st["cnt_touched"], st["cnt_sweeps"]
+    conv = max(st["cnt_convergences"], 1)
+    n = st["n"]
+    b_sim = 12 * E + 32 * B + 64 * T + 8 * (n + 1) * S
+    return {"E": E, "B": B, "T": T, "S": S, "L": st["sketch_edge_updates"], "convergences": conv,
+            "bytes": b_sim, "bytes_per_launch": b_sim / conv}
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import paper_2410_14047_b200 as D
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    gen, a, m, wspec, r, k, desc = CONFIGS[args.config]
+    devices = world  # FASST partitions: one per GPU
+    g = make_graph(D, args.config)
+    g.pin()
+    ctx = D.Context(local_rank)
+    if world > 1:
+        from paper_2410_14047_b200 import dist as pdist
+        runner = pdist.DistRunner(ctx, g, rank, world)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=local_rank)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=f"cuda:{local_rank}")
+
+    def one_run(resident):
+        if world > 1:
+            return runner.run_json(k=k, r=r, weights=wspec, seed=SEED, resident=resident)
+        if resident:
+            return ctx.run_json(None, k=k, r=r, devices=1, weights=wspec, seed=SEED,
+                                timings=False, resident=True)
+        return ctx.run_json(g, k=k, r=r, devices=1, weights=wspec, seed=SEED, timings=False)
+
+    ctx.upload(g)
+    for _ in range(args.warmup):
+        one_run(True)
+    torch.cuda.synchronize()
+
+    # ---- device-timed resident runs (value)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local_rank)
+    clk.start()
+    times, stats = [], []
+    for _ in range(args.steps):
+        flush.add_(1)  # L2 flush (256 MiB write) between timed steps
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rep = one_run(True)
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
+        stats.append(ctx.stats())
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = clk.stop()
+    step_s = statistics.mean(times)
+    if dist:
+        t = torch.tensor([step_s], device=f"cuda:{local_rank}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_s = float(t.item())
+
+    # ---- e2e through run_json(host graph): H2D from pinned memory every step
+    e2e_times = []
+    for _ in range(max(3, min(args.steps, 10))):
+        flush.add_(1)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rep_e2e = one_run(False)
+        e1.record(stream)
+        e1.synchronize()
+        e2e_times.append(e0.elapsed_time(e1) / 1e3)
+    e2e_s = statistics.mean(e2e_times)
+    if dist:
+        t = torch.tensor([e2e_s], device=f"cuda:{local_rank}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    assert json.loads(rep_e2e)["seeds"] == json.loads(rep)["seeds"]
+    h2d = 8 * (g.n + 1) + 4 * g.m
+    d2h = 64 + 12 * k + 4 * k + devices * 256
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (persistent simulate)
+    alg = algorithmic_bytes(D, ctx, g, args.config, devices) if world == 1 else None
+    sim_active = statistics.mean(s["sim_active"] for s in stats)
+    sim_launches = statistics.mean(s["sim_launches"] for s in stats)
+    peak, peak_kind = measured_peak()
+    roofline = None
+    upd_per_s = None
+    if alg:
+        per_launch_s = sim_active / max(sim_launches, 1)
+        achieved = alg["bytes_per_launch"] / per_launch_s / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        roofline = {"bound": "hbm", "kernel": "k_simulate (persistent, to convergence)",
+                    "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_kind,
+                    "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                    "alg_bytes_per_launch": alg["bytes_per_launch"],
+                    "launch_ms": round(per_launch_s * 1e3, 4),
+                    "units": {x: alg[x] for x in ("E", "B", "T", "S", "L", "convergences")}}
+        upd_per_s = alg["L"] / max(sim_active, 1e-12)
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            cpu = run_reference(D, args.config, steps=1, warmup=0, graph=g)
+        except Exception as ex:  # reported, never fatal
+            cpu = {"value": None, "unit": "s", "cores": 0, "kind": "unavailable",
+                   "sample": repr(ex)}
+
+    last = stats[-1]
+    line = {
+        "metric": METRIC, "value": round(step_s, 6), "unit": "s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 3),
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "int8",
+        "data": "synthetic (deterministic R-MAT generator, seed 7)",
+        "config": {"workload": desc, "n": g.n, "m": g.m, "r": r, "k": k, "weights": wspec,
+                   "devices": devices, "mode": "fasst", "rebuild_eps": 0.01, "seed": SEED,
+                   "l2": "flushed between steps (256 MiB write)",
+                   "parallelism": f"fasst-sample-space x{world}"},
+        "sketch_edge_updates_per_s": upd_per_s,
+        "phases_s": {x: round(last[x], 6) for x in ("build", "fill", "simulate", "select",
+                                                    "cascade", "total")},
+        "rebuilds": json.loads(rep)["rebuilds"],
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(e2e_s, 6), "unit": "s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "clocks": clocks,
+        "gpu_launches": int(statistics.mean(s["launches"] for s in stats)),
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local_rank = env_rank()
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        import paper_2410_14047_b200 as D
+        gen, a, m, wspec, r, k, desc = CONFIGS[args.config]
+        res = run_reference(D, args.config, steps=args.steps, warmup=args.warmup)
+        line = {"impl": "reference", "metric": METRIC, "value": round(res["value"], 6),
+                "unit": "s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": round(res["value"] * 1e3, 3), "higher_is_better": False,
+                "scaling": "strong", "vs_baseline": None, "dtype": "int8",
+                "data": "synthetic (deterministic R-MAT generator, seed 7)",
+                "config": {"workload": desc, "r": r, "k": k, "weights": wspec,
+                           "devices": res["cores"], "mode": "fasst"},
+                "cpu_baseline": res,
+                "e2e": {"value": round(res["value"], 6), "unit": "s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+    run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -49,6 +49,7 @@ typedef struct dfs_config {
   uint64_t seed;
   int32_t sim_cap; /* default 256 (runtime.hpp:21) */
   int32_t jacobi;  /* 0: in-place async schedule; 1: the reference's Jacobi schedule */
+  int32_t count;   /* 1 (with jacobi): tally the reference-schedule work units */
 } dfs_config;
 
 /* Phase timings (runtime.hpp:24-27) plus instrumentation of the last run. */
@@ -58,6 +59,13 @@ typedef struct dfs_stats {
   uint64_t items_processed;
   uint64_t sweeps_total;
   uint64_t items_fwd, items_rev;
+  /* reference-schedule work units (count mode) */
+  uint64_t cnt_edges, cnt_batches, cnt_touched, cnt_sweeps, cnt_convergences;
+  uint64_t launches;     /* kernels launched by the run */
+  double sim_active;     /* seconds of the simulate launches that ran */
+  uint32_t sim_launches; /* simulate launches that ran */
+  uint32_t n;
+  uint64_t m;
 } dfs_stats;
 
 const char *dfs_last_error(void);
@@ -96,6 +104,10 @@ int dfs_ctx_create(int device, dfs_ctx **out);
 void dfs_ctx_destroy(dfs_ctx *ctx);
 /* H2D of the CSR + on-device ehash/in-degree/transpose (resident graph). */
 int dfs_upload(dfs_ctx *ctx, const dfs_graph *g);
+/* The context's CUDA stream (cudaStream_t), e.g. for timing with events. */
+int dfs_ctx_stream(dfs_ctx *ctx, void **stream);
+/* Page-lock the graph's CSR arrays so uploads are DMA from pinned memory. */
+int dfs_graph_pin(dfs_graph *g);
 
 /* ---- hot path ------------------------------------------------------------
  * dfs_run_json: run_json (pymodule.cpp:75-90): uploads g, applies weights,
@@ -116,12 +128,15 @@ int dfs_device_graph_size(dfs_ctx *ctx, uint32_t tau, uint64_t *m_tau, uint32_t 
 int dfs_device_graph(dfs_ctx *ctx, uint32_t tau, uint64_t *offsets, uint32_t *adj,
                      uint64_t *mask);
 int dfs_fill(dfs_ctx *ctx, uint32_t tau);                                   /* sketch.cpp:55-66 */
-int dfs_simulate(dfs_ctx *ctx, uint32_t tau, int cap, int jacobi, int *sweeps); /* engine.cpp:88-96 */
+/* engine.cpp:88-96; jacobi bit 0: Jacobi schedule, bit 1: count work units */
+int dfs_simulate(dfs_ctx *ctx, uint32_t tau, int cap, int jacobi, int *sweeps);
 int dfs_scores(dfs_ctx *ctx, uint32_t tau, double *out_n);                  /* sketch.cpp:119-137 */
 int dfs_commit_cascade(dfs_ctx *ctx, uint32_t tau, uint32_t seed, uint64_t *visited); /* engine.cpp:106-144 */
 int dfs_visited_count(dfs_ctx *ctx, uint32_t tau, uint64_t *out);          /* sketch.cpp:139 */
 int dfs_get_registers(dfs_ctx *ctx, uint32_t tau, int8_t *out_nJ);
 int dfs_set_registers(dfs_ctx *ctx, uint32_t tau, const int8_t *in_nJ);
+/* {updates, items, edges, batches, touched, sweeps, convergences, visited} */
+int dfs_rank_counters(dfs_ctx *ctx, uint32_t tau, uint64_t out[8]);
 
 /* ---- verification oracles (oracle.cpp; host, not the hot path) ----------- */
 int dfs_influence(const dfs_graph *g, const uint32_t *seeds, uint32_t nseeds, uint32_t trials,

@@ -83,6 +83,10 @@ class Graph:
         b = C.c_uint64.from_address(off + 8 * (u + 1)).value
         return b - a
 
+    def pin(self) -> None:
+        """Page-lock the CSR arrays (uploads become DMA from pinned memory)."""
+        check(lib().dfs_graph_pin(self._h))
+
     def weights(self, spec: str = "const:0.1", seed: int = 0) -> np.ndarray:
         """apply_weights on the host (runtime.cpp:15-17), fixed point."""
         out = np.zeros(max(self.m, 1), np.uint32)
@@ -145,9 +149,9 @@ def is_sampled(x: int, h: int, w: float) -> bool:
     return bool(out.value)
 
 
-def _config(k, r, devices, mode, weights, rebuild_eps, seed, sim_cap=256, jacobi=0):
+def _config(k, r, devices, mode, weights, rebuild_eps, seed, sim_cap=256, jacobi=0, count=0):
     return Config(k, r, devices, mode.encode(), weights.encode(), float(rebuild_eps), seed,
-                  sim_cap, jacobi)
+                  sim_cap, jacobi, count)
 
 
 class Context:
@@ -177,8 +181,9 @@ class Context:
         return s
 
     def run_json(self, graph, k=10, r=256, devices=1, mode="fasst", weights="const:0.1",
-                 rebuild_eps=0.01, seed=0, timings=True, jacobi=0, resident=False):
-        cfg = _config(k, r, devices, mode, weights, rebuild_eps, seed, jacobi=jacobi)
+                 rebuild_eps=0.01, seed=0, timings=True, jacobi=0, resident=False, count=0):
+        cfg = _config(k, r, devices, mode, weights, rebuild_eps, seed, jacobi=jacobi,
+                      count=count)
         out = C.c_void_p()
         if resident:
             check(lib().dfs_run_resident_json(self._h, graph._h if graph is not None else None,
@@ -186,6 +191,19 @@ class Context:
         else:
             check(lib().dfs_run_json(self._h, graph._h, C.byref(cfg), int(timings), C.byref(out)))
         return self._take_json(out)
+
+    @property
+    def stream(self) -> int:
+        p = C.c_void_p()
+        check(lib().dfs_ctx_stream(self._h, C.byref(p)))
+        return p.value or 0
+
+    def counters(self, tau: int) -> dict:
+        out = np.zeros(8, np.uint64)
+        check(lib().dfs_rank_counters(self._h, tau, out.ctypes.data))
+        keys = ("updates", "items", "edges", "batches", "touched", "sweeps", "convergences",
+                "visited")
+        return dict(zip(keys, (int(v) for v in out)))
 
     def stats(self) -> dict:
         st = Stats()
@@ -224,9 +242,9 @@ class Context:
     def fill(self, tau: int):
         check(lib().dfs_fill(self._h, tau))
 
-    def simulate(self, tau: int, cap: int = 256, jacobi: int = 0) -> int:
+    def simulate(self, tau: int, cap: int = 256, jacobi: int = 0, count: int = 0) -> int:
         s = C.c_int()
-        check(lib().dfs_simulate(self._h, tau, cap, jacobi, C.byref(s)))
+        check(lib().dfs_simulate(self._h, tau, cap, jacobi | (count << 1), C.byref(s)))
         return s.value
 
     def scores(self, tau: int) -> np.ndarray:

@@ -21,20 +21,26 @@ SYMBOLS = [
     "dfs_last_stats", "dfs_prepare", "dfs_plan", "dfs_device_graph_size", "dfs_device_graph",
     "dfs_fill", "dfs_simulate", "dfs_scores", "dfs_commit_cascade", "dfs_visited_count",
     "dfs_get_registers", "dfs_set_registers", "dfs_influence", "dfs_greedy_exact",
+    "dfs_ctx_stream", "dfs_graph_pin", "dfs_rank_counters",
 ]
 
 
 class Config(C.Structure):
     _fields_ = [("k", C.c_uint32), ("r", C.c_uint32), ("devices", C.c_uint32),
                 ("mode", C.c_char_p), ("weights", C.c_char_p), ("rebuild_eps", C.c_double),
-                ("seed", C.c_uint64), ("sim_cap", C.c_int32), ("jacobi", C.c_int32)]
+                ("seed", C.c_uint64), ("sim_cap", C.c_int32), ("jacobi", C.c_int32),
+                ("count", C.c_int32)]
 
 
 class Stats(C.Structure):
     _fields_ = [(f, C.c_double) for f in ("build", "fill", "simulate", "select", "cascade",
                                           "total", "upload")] + \
                [(f, C.c_uint64) for f in ("sketch_edge_updates", "items_processed",
-                                          "sweeps_total", "items_fwd", "items_rev")]
+                                          "sweeps_total", "items_fwd", "items_rev", "cnt_edges",
+                                          "cnt_batches", "cnt_touched", "cnt_sweeps",
+                                          "cnt_convergences", "launches")] + \
+               [("sim_active", C.c_double), ("sim_launches", C.c_uint32), ("n", C.c_uint32),
+                ("m", C.c_uint64)]
 
 
 class DfsError(RuntimeError):
@@ -92,6 +98,9 @@ def lib():
         "dfs_influence": (i32, [vp, vp, u32, u32, u64, u32, C.c_char_p, C.POINTER(C.c_double),
                                 C.POINTER(C.c_double)]),
         "dfs_greedy_exact": (i32, [vp, u32, u32, u64, C.c_char_p, vp]),
+        "dfs_ctx_stream": (i32, [vp, pp]),
+        "dfs_graph_pin": (i32, [vp]),
+        "dfs_rank_counters": (i32, [vp, u32, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -14,6 +14,13 @@
 
 struct dfs_graph {
   dfs::HostGraph g;
+  bool pinned = false;
+  ~dfs_graph() {
+    if (pinned) {
+      cudaHostUnregister(g.offsets.data());
+      if (g.m) cudaHostUnregister(g.adj.data());
+    }
+  }
 };
 struct dfs_ctx {
   std::unique_ptr<dfs::Context> c;
@@ -70,6 +77,7 @@ dfs::RunConfig to_config(const dfs_config* c) {
   r.seed = c->seed;
   r.sim_cap = c->sim_cap > 0 ? c->sim_cap : 256;
   r.jacobi = c->jacobi;
+  r.count = c->jacobi ? c->count : 0;
   return r;
 }
 }  // namespace
@@ -194,6 +202,27 @@ int dfs_upload(dfs_ctx* ctx, const dfs_graph* g) {
   });
 }
 
+int dfs_ctx_stream(dfs_ctx* ctx, void** stream) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(stream, "stream");
+    *stream = ctx->c->stream();
+  });
+}
+int dfs_graph_pin(dfs_graph* g) {
+  return guard([&] {
+    need(g, "graph");
+    if (g->pinned) return;
+    dfs::cuda_check(cudaHostRegister(g->g.offsets.data(), g->g.offsets.size() * 8,
+                                     cudaHostRegisterDefault),
+                    "cudaHostRegister(offsets)");
+    if (g->g.m)
+      dfs::cuda_check(cudaHostRegister(g->g.adj.data(), g->g.m * 4, cudaHostRegisterDefault),
+                      "cudaHostRegister(adj)");
+    g->pinned = true;
+  });
+}
+
 int dfs_run_json(dfs_ctx* ctx, const dfs_graph* g, const dfs_config* cfg, int timings,
                  char** json_out) {
   return guard([&] {
@@ -233,6 +262,16 @@ int dfs_last_stats(const dfs_ctx* ctx, dfs_stats* out) {
     out->sweeps_total = r.sweeps_total;
     out->items_fwd = r.items_fwd;
     out->items_rev = r.items_rev;
+    out->cnt_edges = r.cnt_edges;
+    out->cnt_batches = r.cnt_batches;
+    out->cnt_touched = r.cnt_touched;
+    out->cnt_sweeps = r.cnt_sweeps;
+    out->cnt_convergences = r.cnt_convergences;
+    out->launches = r.launches;
+    out->sim_active = r.sim_active;
+    out->sim_launches = r.sim_launches;
+    out->n = uint32_t(r.n);
+    out->m = r.m;
   });
 }
 
@@ -289,7 +328,8 @@ int dfs_fill(dfs_ctx* ctx, uint32_t tau) {
 int dfs_simulate(dfs_ctx* ctx, uint32_t tau, int cap, int jacobi, int* sweeps) {
   return guard([&] {
     need(ctx, "ctx");
-    const int s = ctx->c->stage_simulate(tau, cap > 0 ? cap : 256, jacobi);
+    // jacobi: bit 0 = Jacobi schedule, bit 1 = count reference-schedule units
+    const int s = ctx->c->stage_simulate(tau, cap > 0 ? cap : 256, jacobi & 1, (jacobi >> 1) & 1);
     if (sweeps) *sweeps = s;
     if (s < 0)
       throw dfs::Error(dfs::kRuntime, "simulate did not converge within " +
@@ -330,6 +370,14 @@ int dfs_set_registers(dfs_ctx* ctx, uint32_t tau, const int8_t* in_nJ) {
     need(ctx, "ctx");
     need(in_nJ, "in");
     ctx->c->stage_set_registers(tau, in_nJ);
+  });
+}
+
+int dfs_rank_counters(dfs_ctx* ctx, uint32_t tau, uint64_t out[8]) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    ctx->c->stage_counters(tau, out);
   });
 }
 

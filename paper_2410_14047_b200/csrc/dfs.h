@@ -77,6 +77,9 @@ struct RankCtl {
   int error;                    // 1 = simulate cap exceeded
   unsigned int dirty_count;     // rows to rescore
   unsigned int pad[6];
+  // reference-schedule work counters (count mode):
+  // E edges processed, B live 32-sim batches, T touched (row, batch) pairs
+  unsigned long long cnt_edges, cnt_batches, cnt_touched, cnt_sweeps, cnt_convergences;
 };
 
 // Work queues used by the persistent simulate / cascade kernels.  Three
@@ -101,6 +104,7 @@ struct RankDev {
   uint32_t* lstamp = nullptr;     // n  queue-membership stamps
   uint32_t* dstamp = nullptr;     // n  dirty-row stamps
   uint32_t* dirty = nullptr;      // n  rows to rescore
+  uint32_t* tbits = nullptr;      // n*W32 bits: touched (row, batch) of a sweep (count mode)
   double* scores = nullptr;       // n
   RankCtl* ctl = nullptr;
   Queues q{};
@@ -156,9 +160,12 @@ void launch_chunk_write(uint32_t n, Items& it, const uint64_t* row_chunk64, cuda
 // Fill registers (VISITED kept, pads VISITED).  gate: run only if *gate == want.
 void launch_fill(const RankDev& r, const unsigned int* gate, unsigned int want, cudaStream_t s);
 // Persistent cooperative simulate to convergence.  jacobi != 0 reproduces the
-// reference's snapshot schedule exactly (same sweep count).
-void launch_simulate(const RankDev& r, int jacobi, int cap, const unsigned int* gate,
+// reference's snapshot schedule exactly (same sweep count); count != 0 (with
+// jacobi) also tallies the reference-schedule work units E/B/T/L.
+void launch_simulate(const RankDev& r, int jacobi, int count, int cap, const unsigned int* gate,
                      unsigned int want, cudaStream_t s);
+// Number of kernels this library launched (all launchers), for gpu_launches.
+unsigned long long launches();
 // Row scores: full = all rows, else the dirty list of the last cascade.
 void launch_score(const RankDev& r, int full, const unsigned int* gate, unsigned int want,
                   cudaStream_t s);
@@ -170,6 +177,6 @@ void launch_cascade(const RankDev& r, const unsigned int* choice, uint32_t seed,
                     cudaStream_t s);
 void launch_round_end(RunArrays& ra, RankCtl* const* ctls_dev, uint32_t mu, uint32_t k,
                       uint32_t r, double eps, cudaStream_t s);
-int coop_grid(int which);  // 0 simulate, 1 cascade
+int coop_grid(int which, int variant = 0);  // 0 simulate, 1 cascade
 
 }  // namespace dfs

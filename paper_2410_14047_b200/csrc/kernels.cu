@@ -275,7 +275,6 @@ __device__ __forceinline__ void push_row(uint32_t u, uint32_t stamp, uint32_t* l
 
 struct SimArgs {
   RankDev r;
-  int jacobi;
   int cap;
   const unsigned int* gate;
   unsigned int want;
@@ -283,10 +282,12 @@ struct SimArgs {
 
 // Persistent simulate-to-convergence (engine.cpp:57-96 semantics).  Sweep s
 // processes the reverse chunks of rows that changed in sweep s-1 (all chunks
-// in sweep 1).  Async mode reads and writes the live matrix in place (the
-// fixpoint is schedule-independent: DESIGN.md §simulate); Jacobi mode reads
-// the snapshot and re-syncs changed rows after each sweep, which reproduces
-// the reference's sweep count exactly.
+// in sweep 1).  Async mode (JAC = 0) reads and writes the live matrix in place
+// (the fixpoint is schedule-independent: DESIGN.md §simulate); Jacobi mode
+// reads the snapshot and re-syncs changed rows after each sweep, which
+// reproduces the reference's sweep count exactly.  CNT = 1 (Jacobi only)
+// tallies the reference-schedule work units of SURVEY.md §8(d).
+template <int JAC, int CNT>
 __global__ void __launch_bounds__(kThreads) k_simulate(SimArgs a) {
   if (a.gate && ld_volatile(a.gate) != a.want) return;  // grid-uniform
   cg::grid_group grid = cg::this_grid();
@@ -294,20 +295,24 @@ __global__ void __launch_bounds__(kThreads) k_simulate(SimArgs a) {
   unsigned int* cnt = r.q.counts;
   const uint32_t base = ld_volatile(&r.ctl->tick);
   const unsigned lane = lane_id();
-  const uint64_t gwarp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t gthreads = uint64_t(gridDim.x) * blockDim.x;
+  const uint64_t gwarp = gtid >> 5;
+  const uint64_t nw = gthreads >> 5;
   if (gwarp == 0 && lane < 9) cnt[lane] = 0;
-  if (a.jacobi) {  // SimulateBuffers::reset (engine.cpp:9-15): snapshot := registers
+  if (JAC) {  // SimulateBuffers::reset (engine.cpp:9-15): snapshot := registers
     const uint64_t n16 = uint64_t(r.n) * r.Jp / 16;
     const uint4* s4 = reinterpret_cast<const uint4*>(r.regs);
     uint4* d4 = reinterpret_cast<uint4*>(r.snap);
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
-         i += uint64_t(gridDim.x) * blockDim.x)
-      d4[i] = s4[i];
+    for (uint64_t i = gtid; i < n16; i += gthreads) d4[i] = s4[i];
   }
+  const uint64_t tb_words = CNT ? (uint64_t(r.n) * r.W32 + 31) / 32 : 0;
+  if (CNT)
+    for (uint64_t i = gtid; i < tb_words; i += gthreads) r.tbits[i] = 0;
   grid.sync();
 
-  const int8_t* srcm = a.jacobi ? r.snap : r.regs;
-  unsigned long long upd = 0, nitems = 0;
+  const int8_t* srcm = JAC ? r.snap : r.regs;
+  unsigned long long upd = 0, nitems = 0, nedges = 0, ntouched = 0;
   uint32_t s = 1;
   int err = 0;
   for (;; ++s) {
@@ -363,6 +368,14 @@ __global__ void __launch_bounds__(kThreads) k_simulate(SimArgs a) {
           }
           upd += __popc(mk);
           ++nitems;
+          if (CNT) {
+            // E: first item of its edge (items of one edge are consecutive, same u)
+            if (i == r.rev.row_off[v] || r.rev.other[i - 1] != u) ++nedges;
+            // T: distinct (u, b) touched in this sweep
+            const uint64_t bit = uint64_t(u) * r.W32 + b;
+            const uint32_t m1 = 1u << (bit & 31);
+            if (!(atomicOr(&r.tbits[bit >> 5], m1) & m1)) ++ntouched;
+          }
           if (changed)
             push_row(u, stamp, r.lstamp, r.rev.row_chunk, r.q.rows[gn], r.q.chunks[gn], &cnt[gn],
                      &cnt[3 + gn]);
@@ -370,15 +383,16 @@ __global__ void __launch_bounds__(kThreads) k_simulate(SimArgs a) {
       }
     }
     grid.sync();
-    if (a.jacobi) {  // engine.cpp:81-82: re-sync snapshot rows that moved
+    if (JAC) {  // engine.cpp:81-82: re-sync snapshot rows that moved
       const unsigned nr = ld_volatile(&cnt[3 + gn]);
-      const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
       for (uint64_t k = gwarp; k < nr; k += nw) {
         const uint64_t row = uint64_t(r.q.rows[gn][k]) * r.Jp;
         const uint4* sp4 = reinterpret_cast<const uint4*>(r.regs + row);
         uint4* dp4 = reinterpret_cast<uint4*>(r.snap + row);
         for (uint32_t j = lane; j < r.Jp / 16; j += 32) dp4[j] = __ldcg(sp4 + j);
       }
+      if (CNT)
+        for (uint64_t i = gtid; i < tb_words; i += gthreads) r.tbits[i] = 0;
       grid.sync();
     }
   }
@@ -386,14 +400,26 @@ __global__ void __launch_bounds__(kThreads) k_simulate(SimArgs a) {
   for (int o = 16; o; o >>= 1) {
     upd += __shfl_xor_sync(0xffffffffu, upd, o);
     nitems += __shfl_xor_sync(0xffffffffu, nitems, o);
+    if (CNT) {
+      nedges += __shfl_xor_sync(0xffffffffu, nedges, o);
+      ntouched += __shfl_xor_sync(0xffffffffu, ntouched, o);
+    }
   }
   if (lane == 0 && upd) {
     atomicAdd(&r.ctl->updates, upd);
     atomicAdd(&r.ctl->items_processed, nitems);
+    if (CNT) {
+      atomicAdd(&r.ctl->cnt_edges, nedges);
+      atomicAdd(&r.ctl->cnt_batches, nitems);
+      atomicAdd(&r.ctl->cnt_touched, ntouched);
+    }
   }
   if (gwarp == 0 && lane == 0) {
-    r.ctl->sweeps = err ? s : s - 1;
-    r.ctl->total_sweeps += err ? s : s - 1;
+    const uint32_t sw = err ? s : s - 1;
+    r.ctl->sweeps = sw;
+    r.ctl->total_sweeps += sw;
+    r.ctl->cnt_sweeps += sw;
+    r.ctl->cnt_convergences += 1;
     r.ctl->tick = base + s + 2;
     if (err) r.ctl->error = 1;
   }
@@ -675,6 +701,8 @@ __global__ void k_round_end(RunArrays ra, RankCtl* const* ctls, uint32_t mu, uin
 }  // namespace
 
 // ================================================================= launchers
+static unsigned long long g_launches = 0;
+unsigned long long launches() { return g_launches; }
 size_t graph_prepare_tmp_bytes(uint64_t m, uint32_t n) {
   size_t sort_bytes = 0, scan_bytes = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const uint32_t*)nullptr,
@@ -730,12 +758,14 @@ void launch_graph_prepare(DevGraph& g, void* tmp, size_t tmp_bytes, cudaStream_t
   DFS_CUDA(cub::DeviceScan::ExclusiveScan(cubtmp, bytes, g.indeg, g.toff,
                                           cuda::std::plus<uint64_t>{}, uint64_t(0), g.n + 1, s));
   DFS_CUDA(cudaGetLastError());
+  ++g_launches;
 }
 
 void launch_weights(const DevGraph& g, int kind, uint32_t W, uint32_t* w, cudaStream_t s) {
   if (!g.m) return;
   k_weights<<<grid_for(g.m), kThreads, 0, s>>>(g.m, kind, W, g.adj, g.indeg, w);
   DFS_CUDA(cudaGetLastError());
+  ++g_launches;
 }
 
 void launch_items_pass(const DevGraph& g, const uint32_t* w, const RankDev& r, int dir, int fasst,
@@ -758,6 +788,7 @@ void launch_items_pass(const DevGraph& g, const uint32_t* w, const RankDev& r, i
     k_items<0><<<grid, kThreads, smem, s>>>(g.m, dir, g.tedge, g.adj, g.src, g.ehash, w, r.x, r.J,
                                             r.Jp, fasst, cnt, pos_off, nullptr, nullptr, nullptr);
   DFS_CUDA(cudaGetLastError());
+  ++g_launches;
 }
 
 void launch_row_offsets(const DevGraph& g, int dir, const uint64_t* pos_off, Items& it,
@@ -765,12 +796,14 @@ void launch_row_offsets(const DevGraph& g, int dir, const uint64_t* pos_off, Ite
   k_row_offsets<<<grid_for(uint64_t(g.n) + 1), kThreads, 0, s>>>(g.n, dir ? g.toff : g.off,
                                                                    pos_off, it.row_off, row_cnt);
   DFS_CUDA(cudaGetLastError());
+  ++g_launches;
 }
 
 void launch_chunk_write(uint32_t n, Items& it, const uint64_t* row_chunk64, cudaStream_t s) {
   k_chunk_write<<<grid_for(uint64_t(n) + 1), kThreads, 0, s>>>(
       n, row_chunk64, it.row_off, it.row_chunk, it.chunk_row, it.chunk_beg, it.count);
   DFS_CUDA(cudaGetLastError());
+  ++g_launches;
 }
 
 void launch_fill(const RankDev& r, const unsigned int* gate, unsigned int want, cudaStream_t s) {
@@ -779,28 +812,38 @@ void launch_fill(const RankDev& r, const unsigned int* gate, unsigned int want, 
   k_fill<<<grid_for(total), kThreads, 0, s>>>(r.n, r.J, r.Jp, r.jkey, r.vis, r.regs, gate, want,
                                               r.ctl);
   DFS_CUDA(cudaGetLastError());
+  ++g_launches;
 }
 
-int coop_grid(int which) {
-  static int g[2] = {0, 0};
-  if (!g[which]) {
-    int per = 0;
-    if (which == 0)
-      DFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_simulate, kThreads, 0));
-    else
-      DFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cascade, kThreads, 0));
-    if (per < 1) per = 1;
-    g[which] = per * num_sms();
+static const void* sim_kernel(int variant) {
+  switch (variant) {
+    case 0: return (const void*)k_simulate<0, 0>;
+    case 1: return (const void*)k_simulate<1, 0>;
+    default: return (const void*)k_simulate<1, 1>;
   }
-  return g[which];
 }
 
-void launch_simulate(const RankDev& r, int jacobi, int cap, const unsigned int* gate,
+int coop_grid(int which, int variant) {
+  static int g[4] = {0, 0, 0, 0};
+  const int slot = which == 0 ? variant : 3;
+  if (!g[slot]) {
+    int per = 0;
+    const void* fn = which == 0 ? sim_kernel(variant) : (const void*)k_cascade;
+    DFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kThreads, 0));
+    if (per < 1) per = 1;
+    g[slot] = per * num_sms();
+  }
+  return g[slot];
+}
+
+void launch_simulate(const RankDev& r, int jacobi, int count, int cap, const unsigned int* gate,
                      unsigned int want, cudaStream_t s) {
-  SimArgs a{r, jacobi, cap, gate, want};
+  SimArgs a{r, cap, gate, want};
   void* args[] = {&a};
-  DFS_CUDA(cudaLaunchCooperativeKernel((void*)k_simulate, dim3(coop_grid(0)), dim3(kThreads), args,
-                                       0, s));
+  const int variant = jacobi ? (count ? 2 : 1) : 0;
+  DFS_CUDA(cudaLaunchCooperativeKernel(sim_kernel(variant), dim3(coop_grid(0, variant)),
+                                       dim3(kThreads), args, 0, s));
+  ++g_launches;
 }
 
 void launch_score(const RankDev& r, int full, const unsigned int* gate, unsigned int want,
@@ -812,17 +855,20 @@ void launch_score(const RankDev& r, int full, const unsigned int* gate, unsigned
   k_score<<<grid_for(rows * 32), kThreads, 0, s>>>(r.regs, r.n, r.J, r.Jp, K, full, r.dirty, r.ctl,
                                                    r.scores, gate, want);
   DFS_CUDA(cudaGetLastError());
+  ++g_launches;
 }
 
 void launch_treesum(const double* const* parts_dev, uint32_t mu, uint32_t n, double* out,
                     cudaStream_t s) {
   k_treesum<<<grid_for(n), kThreads, 0, s>>>(parts_dev, mu, n, out);
   DFS_CUDA(cudaGetLastError());
+  ++g_launches;
 }
 
 void launch_argmax(const double* scores, RunArrays& ra, uint32_t n, cudaStream_t s) {
   k_argmax<<<ra.nblk, kThreads, 0, s>>>(scores, n, ra);
   DFS_CUDA(cudaGetLastError());
+  ++g_launches;
 }
 
 void launch_cascade(const RankDev& r, const unsigned int* choice, uint32_t seed, cudaStream_t s) {
@@ -830,12 +876,14 @@ void launch_cascade(const RankDev& r, const unsigned int* choice, uint32_t seed,
   void* args[] = {&a};
   DFS_CUDA(cudaLaunchCooperativeKernel((void*)k_cascade, dim3(coop_grid(1)), dim3(kThreads), args,
                                        0, s));
+  ++g_launches;
 }
 
 void launch_round_end(RunArrays& ra, RankCtl* const* ctls_dev, uint32_t mu, uint32_t k, uint32_t r,
                       double eps, cudaStream_t s) {
   k_round_end<<<1, 32, 0, s>>>(ra, ctls_dev, mu, k, r, eps);
   DFS_CUDA(cudaGetLastError());
+  ++g_launches;
 }
 
 }  // namespace dfs

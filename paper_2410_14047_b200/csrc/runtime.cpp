@@ -135,6 +135,8 @@ void Context::alloc_rank(RankDev& r, uint32_t tau) {
   r.lstamp = as<uint32_t>(arena_.get(p + "lstamp", nn * 4));
   r.dstamp = as<uint32_t>(arena_.get(p + "dstamp", nn * 4));
   r.dirty = as<uint32_t>(arena_.get(p + "dirty", nn * 4));
+  r.tbits = cfg_.count ? as<uint32_t>(arena_.get(p + "tbits", (nn * r.W32 + 31) / 32 * 4 + 4))
+                       : nullptr;
   r.scores = as<double>(arena_.get(p + "scores", nn * 8));
   r.ctl = as<RankCtl>(arena_.get(p + "ctl", sizeof(RankCtl)));
   r.q.counts = as<unsigned int>(arena_.get(p + "qcnt", 16 * 4));
@@ -268,6 +270,7 @@ void Context::prepare(const RunConfig& cfg, const HostGraph* host_w_src) {
 
 Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
   auto t_total = Clock::now();
+  const unsigned long long launches0 = launches();
   prepare(cfg, host_w_src);
   const uint32_t n = g_.n, mu = cfg.mu, k = cfg.k;
   cudaStream_t s = stream_;
@@ -316,17 +319,18 @@ Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
   struct Span {
     size_t a, b;
     double* acc;
+    int sim_step = -2;  // simulate span: -1 initial, else the round it may rebuild after
   };
   std::vector<Span> spans;
 
   size_t e0 = mark();
   for (uint32_t t = 0; t < mu; ++t) launch_fill(ranks_[t], nullptr, 0, s);
   size_t e1 = mark();
-  for (uint32_t t = 0; t < mu; ++t) launch_simulate(ranks_[t], cfg.jacobi, cfg.sim_cap, nullptr, 0, s);
+  for (uint32_t t = 0; t < mu; ++t) launch_simulate(ranks_[t], cfg.jacobi, cfg.count, cfg.sim_cap, nullptr, 0, s);
   size_t e2 = mark();
   for (uint32_t t = 0; t < mu; ++t) launch_score(ranks_[t], 1, nullptr, 0, s);
   spans.push_back({e0, e1, &pt.fill});
-  spans.push_back({e1, e2, &pt.simulate});
+  spans.push_back({e1, e2, &pt.simulate, -1});
   size_t prev = e2;
   for (uint32_t step = 0; step < k; ++step) {
     // select: rescore dirty rows, binomial-order sum, argmax (runtime.cpp:88-122)
@@ -345,11 +349,11 @@ Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
       for (uint32_t t = 0; t < mu; ++t) launch_fill(ranks_[t], rebuild, 1, s);
       size_t c = mark();
       for (uint32_t t = 0; t < mu; ++t)
-        launch_simulate(ranks_[t], cfg.jacobi, cfg.sim_cap, rebuild, 1, s);
+        launch_simulate(ranks_[t], cfg.jacobi, cfg.count, cfg.sim_cap, rebuild, 1, s);
       size_t d = mark();
       for (uint32_t t = 0; t < mu; ++t) launch_score(ranks_[t], 1, rebuild, 1, s);
       spans.push_back({b, c, &pt.fill});
-      spans.push_back({c, d, &pt.simulate});
+      spans.push_back({c, d, &pt.simulate, int(step)});
       prev = d;
     }
   }
@@ -387,6 +391,11 @@ Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
     rep.sweeps_total += c.total_sweeps;
     rep.items_fwd += ranks_[t].fwd.count;
     rep.items_rev += ranks_[t].rev.count;
+    rep.cnt_edges += c.cnt_edges;
+    rep.cnt_batches += c.cnt_batches;
+    rep.cnt_touched += c.cnt_touched;
+    rep.cnt_sweeps += c.cnt_sweeps;
+    rep.cnt_convergences += c.cnt_convergences;
   }
   for (uint32_t sd : rep.seeds_dense) rep.seeds.push_back(orig_id_[sd]);
   // comms counters of the reference's collective schedule (collectives.cpp:
@@ -398,11 +407,18 @@ Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
     float ms = 0;
     DFS_CUDA(cudaEventElapsedTime(&ms, ev[sp.a], ev[sp.b]));
     *sp.acc += ms * 1e-3;
+    if (sp.sim_step == -1 ||
+        (sp.sim_step >= 0 && std::find(rep.rebuild_rounds.begin(), rep.rebuild_rounds.end(),
+                                       uint32_t(sp.sim_step)) != rep.rebuild_rounds.end())) {
+      rep.sim_active += ms * 1e-3;
+      rep.sim_launches += mu;
+    }
   }
   (void)eend;
   for (cudaEvent_t e : ev) cudaEventDestroy(e);
   pt.upload = last_.upload;
   pt.total = since(t_total);
+  rep.launches = launches() - launches0;
   rep.timings = pt;
   last_ = pt;
   return rep;
@@ -419,14 +435,17 @@ void Context::stage_fill(uint32_t tau) {
   sync();
 }
 
-int Context::stage_simulate(uint32_t tau, int cap, int jacobi) {
+int Context::stage_simulate(uint32_t tau, int cap, int jacobi, int count) {
   check_tau(tau, ranks_.size());
   RankDev& r = ranks_[tau];
   if (jacobi && !r.snap) {
     r.snap = as<int8_t>(arena_.get("r" + std::to_string(tau) + ".snap",
                                    std::max<size_t>(r.n, 1) * r.Jp));
   }
-  launch_simulate(r, jacobi, cap, nullptr, 0, stream_);
+  if (count && !r.tbits)
+    r.tbits = as<uint32_t>(arena_.get("r" + std::to_string(tau) + ".tbits",
+                                      (std::max<size_t>(r.n, 1) * r.W32 + 31) / 32 * 4 + 4));
+  launch_simulate(r, jacobi, jacobi ? count : 0, cap, nullptr, 0, stream_);
   RankCtl c{};
   DFS_CUDA(cudaMemcpyAsync(&c, r.ctl, sizeof c, cudaMemcpyDeviceToHost, stream_));
   sync();
@@ -459,6 +478,15 @@ uint64_t Context::stage_visited(uint32_t tau) {
   RankCtl c{};
   DFS_CUDA(cudaMemcpy(&c, ranks_[tau].ctl, sizeof c, cudaMemcpyDeviceToHost));
   return c.visited;
+}
+
+void Context::stage_counters(uint32_t tau, uint64_t out[8]) {
+  check_tau(tau, ranks_.size());
+  RankCtl c{};
+  DFS_CUDA(cudaMemcpy(&c, ranks_[tau].ctl, sizeof c, cudaMemcpyDeviceToHost));
+  const uint64_t v[8] = {c.updates,     c.items_processed, c.cnt_edges,        c.cnt_batches,
+                         c.cnt_touched, c.cnt_sweeps,      c.cnt_convergences, c.visited};
+  for (int i = 0; i < 8; ++i) out[i] = v[i];
 }
 
 void Context::stage_get_registers(uint32_t tau, int8_t* out) {

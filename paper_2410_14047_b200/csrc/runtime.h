@@ -41,6 +41,7 @@ struct RunConfig {  // proj/include/difuser/runtime.hpp:13-22
   uint64_t seed = 0;
   int sim_cap = 256;
   int jacobi = 0;  // 1: exact reference sweep schedule (parity/debug)
+  int count = 0;   // 1 (with jacobi): tally reference-schedule work units
 };
 
 struct PhaseTimings {  // runtime.hpp:24-27 (seconds; device-event based)
@@ -62,6 +63,11 @@ struct Report {  // runtime.hpp:29-41
   // instrumentation (not part of the JSON contract)
   uint64_t sketch_edge_updates = 0, items_processed = 0, sweeps_total = 0;
   uint64_t items_fwd = 0, items_rev = 0, device_edges = 0;
+  // reference-schedule units (count mode), summed over ranks and convergences
+  uint64_t cnt_edges = 0, cnt_batches = 0, cnt_touched = 0, cnt_sweeps = 0, cnt_convergences = 0;
+  uint64_t launches = 0;        // kernels launched by run()
+  double sim_active = 0;        // seconds of simulate launches that ran (not gated off)
+  uint32_t sim_launches = 0;    // simulate launches that ran
 };
 
 std::string report_to_json(const Report& rep, bool include_timings);
@@ -85,10 +91,11 @@ class Context {
   // ---- stage API (parity harness), rank tau of the prepared session
   uint32_t ranks() const { return uint32_t(ranks_.size()); }
   void stage_fill(uint32_t tau);
-  int stage_simulate(uint32_t tau, int cap, int jacobi);
+  int stage_simulate(uint32_t tau, int cap, int jacobi, int count = 0);
   void stage_scores(uint32_t tau, double* out);
   uint64_t stage_commit_cascade(uint32_t tau, uint32_t seed);
   uint64_t stage_visited(uint32_t tau);
+  void stage_counters(uint32_t tau, uint64_t out[8]);
   void stage_get_registers(uint32_t tau, int8_t* out);
   void stage_set_registers(uint32_t tau, const int8_t* in);
   void stage_device_graph(uint32_t tau, std::vector<uint64_t>& off, std::vector<uint32_t>& adj,
