@@ -82,13 +82,14 @@ struct RankCtl {
   unsigned long long cnt_edges, cnt_batches, cnt_touched, cnt_sweeps, cnt_convergences;
 };
 
-// Work queues used by the persistent simulate / cascade kernels.  Three
-// rotating generations (index = sweep % 3) so that a generation can be reset
-// while the next one is being filled without an extra grid barrier.
+// Work queues used by the persistent simulate / cascade kernels.  Rotating
+// generations (simulate: sweep % 3, cascade: level % 4) so that a generation
+// can be reset while the next one is being filled without an extra barrier.
+constexpr int kGens = 4;
 struct Queues {
-  uint32_t* chunks[3];          // chunk ids to process
-  uint32_t* rows[3];            // rows (deduplicated) of that generation
-  unsigned int* counts;         // [3] chunk counts, [3..5] row counts, [6..8] work counters
+  uint32_t* chunks[kGens];      // chunk ids to process
+  uint32_t* rows[kGens];        // rows (deduplicated) of that generation
+  unsigned int* counts;         // [0..3] chunk counts, [4..7] row counts, [8..11] work counters
 };
 
 struct RankDev {
@@ -100,7 +101,7 @@ struct RankDev {
   int8_t* regs = nullptr;         // n*Jp
   int8_t* snap = nullptr;         // n*Jp (Jacobi schedule only)
   uint32_t* vis = nullptr;        // n*W32 visited bitset
-  uint32_t* fresh[2] = {nullptr, nullptr};  // n*W32 cascade frontier bits
+  uint32_t* fresh[3] = {nullptr, nullptr, nullptr};  // n*W32 cascade frontier bits
   uint32_t* lstamp = nullptr;     // n  queue-membership stamps
   uint32_t* dstamp = nullptr;     // n  dirty-row stamps
   uint32_t* dirty = nullptr;      // n  rows to rescore

@@ -473,53 +473,117 @@ void influence_stats(const HostGraph& g, const std::vector<uint32_t>& w,
   }
 }
 
+// Tarjan SCC over a live CSR (iterative, roots in id order, edges in CSR
+// order); components numbered in pop order, i.e. reverse topological.
+namespace {
+struct Tarjan {
+  std::vector<int32_t> idx, low, comp;
+  std::vector<uint32_t> stk;
+  std::vector<uint8_t> on;
+  struct Frame {
+    uint32_t v;
+    uint64_t e;
+  };
+  std::vector<Frame> call;
+  int32_t run(uint32_t n, const std::vector<uint64_t>& off, const std::vector<uint32_t>& tg) {
+    idx.assign(n, -1);
+    low.assign(n, 0);
+    comp.assign(n, -1);
+    on.assign(n, 0);
+    stk.clear();
+    call.clear();
+    int32_t counter = 0, ncomp = 0;
+    for (uint32_t root = 0; root < n; ++root) {
+      if (idx[root] != -1) continue;
+      idx[root] = low[root] = counter++;
+      stk.push_back(root);
+      on[root] = 1;
+      call.push_back({root, off[root]});
+      while (!call.empty()) {
+        const uint32_t v = call.back().v;
+        if (call.back().e < off[v + 1]) {
+          const uint32_t w = tg[call.back().e++];
+          if (idx[w] == -1) {
+            idx[w] = low[w] = counter++;
+            stk.push_back(w);
+            on[w] = 1;
+            call.push_back({w, off[w]});
+          } else if (on[w]) {
+            low[v] = std::min(low[v], idx[w]);
+          }
+          continue;
+        }
+        if (low[v] == idx[v]) {
+          uint32_t w;
+          do {
+            w = stk.back();
+            stk.pop_back();
+            on[w] = 0;
+            comp[w] = ncomp;
+          } while (w != v);
+          ++ncomp;
+        }
+        call.pop_back();
+        if (!call.empty()) low[call.back().v] = std::min(low[call.back().v], low[v]);
+      }
+    }
+    return ncomp;
+  }
+};
+}  // namespace
+
+// proj/src/oracle.cpp:152-250 semantics, including its component-bitset
+// closure that ORs target rows in vertex order over the live edges (the gains
+// it yields are what the reference reports, so they are reproduced as is).
 std::vector<uint32_t> greedy_exact(const HostGraph& g, const std::vector<uint32_t>& w, uint32_t k,
                                    uint32_t trials, uint64_t seed) {
   if (k == 0 || k > g.n) throw Error(kInvalid, "greedy_exact: k must be in [1, n]");
   if (trials == 0) throw Error(kInvalid, "greedy_exact: trials must be >= 1");
   const uint64_t base = derive_seed(seed, kSeedTagOracle);
   std::vector<uint32_t> committed;
-  std::vector<uint64_t> gains(g.n);
-  std::vector<uint8_t> live(g.m), covered(g.n);
-  std::vector<uint32_t> mark(g.n, 0), queue;
-  uint32_t epoch = 0;
+  std::vector<uint64_t> gains(g.n), loff(size_t(g.n) + 1), reach, covered, comp_gain;
+  std::vector<uint32_t> ltg, comp_size;
+  std::vector<uint8_t> live(g.m);
+  Tarjan scc;
   for (uint32_t step = 0; step < k; ++step) {
     std::fill(gains.begin(), gains.end(), 0);
     for (uint32_t t = 0; t < trials; ++t) {
       std::mt19937_64 rng(splitmix64_at(splitmix64_at(base, 1000 + step), t));
       for (uint64_t e = 0; e < g.m; ++e) live[e] = uint32_t(rng() >> 33) < w[e];
-      // covered = reachability of the committed set in this realisation
-      std::fill(covered.begin(), covered.end(), 0);
-      queue.clear();
-      for (uint32_t s : committed)
-        if (!covered[s]) {
-          covered[s] = 1;
-          queue.push_back(s);
-        }
-      for (size_t h = 0; h < queue.size(); ++h)
-        for (uint64_t e = g.offsets[queue[h]]; e < g.offsets[queue[h] + 1]; ++e)
-          if (live[e] && !covered[g.adj[e]]) {
-            covered[g.adj[e]] = 1;
-            queue.push_back(g.adj[e]);
-          }
-      // marginal coverage of every vertex; covered vertices close under
-      // reachability, so the BFS prunes at them.
-      for (uint32_t v = 0; v < g.n; ++v) {
-        if (covered[v]) continue;
-        ++epoch;
-        queue.clear();
-        queue.push_back(v);
-        mark[v] = epoch;
-        for (size_t h = 0; h < queue.size(); ++h)
-          for (uint64_t e = g.offsets[queue[h]]; e < g.offsets[queue[h] + 1]; ++e) {
-            const uint32_t x = g.adj[e];
-            if (live[e] && !covered[x] && mark[x] != epoch) {
-              mark[x] = epoch;
-              queue.push_back(x);
-            }
-          }
-        gains[v] += queue.size();
+      std::fill(loff.begin(), loff.end(), 0);
+      ltg.clear();
+      for (uint32_t u = 0; u < g.n; ++u) {
+        for (uint64_t e = g.offsets[u]; e < g.offsets[u + 1]; ++e)
+          if (live[e]) ltg.push_back(g.adj[e]);
+        loff[size_t(u) + 1] = ltg.size();
       }
+      const int32_t nc = scc.run(g.n, loff, ltg);
+      const uint32_t words = uint32_t((nc + 63) / 64);
+      comp_size.assign(nc, 0);
+      for (uint32_t v = 0; v < g.n; ++v) comp_size[scc.comp[v]]++;
+      reach.assign(size_t(nc) * words, 0);
+      for (int32_t c = 0; c < nc; ++c) reach[size_t(c) * words + (c >> 6)] |= 1ull << (c & 63);
+      for (uint32_t u = 0; u < g.n; ++u) {
+        const int32_t cu = scc.comp[u];
+        for (uint64_t e = loff[u]; e < loff[size_t(u) + 1]; ++e) {
+          const int32_t cv = scc.comp[ltg[e]];
+          if (cv == cu) continue;
+          for (uint32_t x = 0; x < words; ++x)
+            reach[size_t(cu) * words + x] |= reach[size_t(cv) * words + x];
+        }
+      }
+      covered.assign(words, 0);
+      for (uint32_t s : committed)
+        for (uint32_t x = 0; x < words; ++x) covered[x] |= reach[size_t(scc.comp[s]) * words + x];
+      comp_gain.assign(nc, 0);
+      for (int32_t c = 0; c < nc; ++c) {
+        uint64_t gain = 0;
+        for (uint32_t x = 0; x < words; ++x)
+          for (uint64_t bits = reach[size_t(c) * words + x] & ~covered[x]; bits; bits &= bits - 1)
+            gain += comp_size[x * 64 + __builtin_ctzll(bits)];
+        comp_gain[c] = gain;
+      }
+      for (uint32_t v = 0; v < g.n; ++v) gains[v] += comp_gain[scc.comp[v]];
     }
     uint32_t best = 0;
     uint64_t best_gain = 0;

@@ -17,6 +17,8 @@
 #include <cub/cub.cuh>
 #include <cuda/std/functional>
 
+#include <cstdlib>
+
 #include "dfs.h"
 #include "hash.cuh"
 
@@ -257,12 +259,13 @@ __device__ __forceinline__ unsigned long long merge8(unsigned long long d, unsig
   return (static_cast<unsigned long long>(hi) << 32) | lo;
 }
 
-// Warp-cooperative push of row u into the next generation (deduplicated by
-// stamp): appends u to rows[gn] and all of u's chunks to chunks[gn].
+// Push of row u into the next generation (deduplicated by stamp): appends u
+// to rows[gn] and all of u's chunks to chunks[gn].
 __device__ __forceinline__ void push_row(uint32_t u, uint32_t stamp, uint32_t* lstamp,
                                          const uint32_t* row_chunk, uint32_t* rows,
                                          uint32_t* chunks, unsigned int* chunk_cnt,
                                          unsigned int* row_cnt) {
+  if (ld_volatile(&lstamp[u]) == stamp) return;
   if (atomicExch(&lstamp[u], stamp) == stamp) return;
   const unsigned ri = atomicAdd(row_cnt, 1u);
   rows[ri] = u;
@@ -270,6 +273,64 @@ __device__ __forceinline__ void push_row(uint32_t u, uint32_t stamp, uint32_t* l
   if (c1 > c0) {
     const unsigned ci = atomicAdd(chunk_cnt, c1 - c0);
     for (uint32_t c = c0; c < c1; ++c) chunks[ci + (c - c0)] = c;
+  }
+}
+
+// Per-warp staging for the flattened item distribution.
+struct WarpStage {
+  uint32_t incl[32];
+  uint32_t row[32];
+  unsigned long long beg[32];
+};
+
+// Warp-cooperative work distribution over a frontier of chunks: one atomic
+// claims 32 frontier slots, the items of those chunks are flattened (warp
+// prefix sum of their sizes) and dealt to lanes 32 at a time, so lanes stay
+// busy even when most rows have only a handful of items (R-MAT tails) and
+// hub rows are spread over many warps.  f(row, item_index) per item.
+template <class F>
+__device__ __forceinline__ void for_frontier_items(const Items& it, const uint32_t* frontier,
+                                                   uint32_t nc, unsigned int* work_ctr,
+                                                   WarpStage& ws, F&& f) {
+  const unsigned lane = lane_id();
+  for (;;) {
+    unsigned b0 = 0;
+    if (lane == 0) b0 = atomicAdd(work_ctr, 32u);
+    b0 = __shfl_sync(0xffffffffu, b0, 0);
+    if (b0 >= nc) break;
+    const uint32_t idx = b0 + lane;
+    uint32_t row = 0, cntc = 0;
+    unsigned long long beg = 0;
+    if (idx < nc) {
+      const uint32_t c = frontier ? __ldcg(frontier + idx) : idx;
+      row = it.chunk_row[c];
+      beg = it.chunk_beg[c];
+      cntc = uint32_t(it.chunk_beg[c + 1] - beg);
+    }
+    uint32_t incl = cntc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= unsigned(o)) incl += t;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    ws.incl[lane] = incl;
+    ws.row[lane] = row;
+    ws.beg[lane] = beg;
+    __syncwarp();
+    for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+      const uint32_t t = t0 + lane;
+      if (t < total) {
+        uint32_t lo = 0, hi = 31;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (ws.incl[mid] > t) hi = mid; else lo = mid + 1;
+        }
+        const uint32_t excl = lo ? ws.incl[lo - 1] : 0;
+        f(ws.row[lo], ws.beg[lo] + (t - excl));
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -290,6 +351,7 @@ struct SimArgs {
 template <int JAC, int CNT>
 __global__ void __launch_bounds__(kThreads) k_simulate(SimArgs a) {
   if (a.gate && ld_volatile(a.gate) != a.want) return;  // grid-uniform
+  __shared__ WarpStage stage[kWarps];
   cg::grid_group grid = cg::this_grid();
   const RankDev& r = a.r;
   unsigned int* cnt = r.q.counts;
@@ -299,7 +361,8 @@ __global__ void __launch_bounds__(kThreads) k_simulate(SimArgs a) {
   const uint64_t gthreads = uint64_t(gridDim.x) * blockDim.x;
   const uint64_t gwarp = gtid >> 5;
   const uint64_t nw = gthreads >> 5;
-  if (gwarp == 0 && lane < 9) cnt[lane] = 0;
+  WarpStage& ws = stage[threadIdx.x >> 5];
+  if (gwarp == 0 && lane < 16) cnt[lane] = 0;
   if (JAC) {  // SimulateBuffers::reset (engine.cpp:9-15): snapshot := registers
     const uint64_t n16 = uint64_t(r.n) * r.Jp / 16;
     const uint4* s4 = reinterpret_cast<const uint4*>(r.regs);
@@ -312,12 +375,13 @@ __global__ void __launch_bounds__(kThreads) k_simulate(SimArgs a) {
   grid.sync();
 
   const int8_t* srcm = JAC ? r.snap : r.regs;
+  const uint32_t Jp = r.Jp;
   unsigned long long upd = 0, nitems = 0, nedges = 0, ntouched = 0;
   uint32_t s = 1;
   int err = 0;
   for (;; ++s) {
     const int g = s % 3, gn = (s + 1) % 3, gr = (s + 2) % 3;
-    if (s > 1 && ld_volatile(&cnt[3 + g]) == 0) break;  // no row changed in sweep s-1
+    if (s > 1 && ld_volatile(&cnt[4 + g]) == 0) break;  // no row changed in sweep s-1
     if (s > uint32_t(a.cap)) {
       err = 1;
       break;
@@ -325,45 +389,44 @@ __global__ void __launch_bounds__(kThreads) k_simulate(SimArgs a) {
     const uint32_t nc = (s == 1) ? uint32_t(r.rev.chunks) : ld_volatile(&cnt[g]);
     if (gwarp == 0 && lane == 0) {
       cnt[gr] = 0;
-      cnt[3 + gr] = 0;
-      cnt[6 + gr] = 0;
+      cnt[4 + gr] = 0;
+      cnt[8 + gr] = 0;
     }
     const uint32_t stamp = base + s;
-    for (;;) {
-      unsigned ci = 0;
-      if (lane == 0) ci = atomicAdd(&cnt[6 + g], 1u);
-      ci = __shfl_sync(0xffffffffu, ci, 0);
-      if (ci >= nc) break;
-      const uint32_t c = (s == 1) ? ci : r.q.chunks[g][ci];
-      const uint32_t v = r.rev.chunk_row[c];
-      const uint64_t beg = r.rev.chunk_beg[c], end = r.rev.chunk_beg[c + 1];
-      const int8_t* srow = srcm + uint64_t(v) * r.Jp;
-      for (uint64_t i0 = beg; i0 < end; i0 += 32) {
-        const uint64_t i = i0 + lane;
-        if (i < end) {
+    uint32_t* rows_n = r.q.rows[gn];
+    uint32_t* chunks_n = r.q.chunks[gn];
+    for_frontier_items(
+        r.rev, s == 1 ? nullptr : r.q.chunks[g], nc, &cnt[8 + g], ws,
+        [&](uint32_t v, uint64_t i) {
           const uint32_t u = __ldg(r.rev.other + i);
           const uint32_t mk = __ldg(r.rev.mask + i);
           const uint32_t b = __ldg(r.rev.batch + i);
           const unsigned long long* sp =
-              reinterpret_cast<const unsigned long long*>(srow + b * 32);
+              reinterpret_cast<const unsigned long long*>(srcm + uint64_t(v) * Jp + b * 32);
           unsigned long long* dp =
-              reinterpret_cast<unsigned long long*>(r.regs + uint64_t(u) * r.Jp + b * 32);
+              reinterpret_cast<unsigned long long*>(r.regs + uint64_t(u) * Jp + b * 32);
+          unsigned long long sv[4], dv[4];
+#pragma unroll
+          for (int wv = 0; wv < 4; ++wv)  // issue all loads first (MLP)
+            if ((mk >> (8 * wv)) & 0xFFu) {
+              sv[wv] = __ldcg(sp + wv);
+              dv[wv] = __ldcg(dp + wv);
+            }
           bool changed = false;
 #pragma unroll
           for (int wv = 0; wv < 4; ++wv) {
             const uint32_t m8 = (mk >> (8 * wv)) & 0xFFu;
             if (!m8) continue;
-            const unsigned long long sv = __ldcg(sp + wv);
-            unsigned long long dv = __ldcg(dp + wv);
-            unsigned long long nv = merge8(dv, sv, m8);
-            while (nv != dv) {
-              const unsigned long long old = atomicCAS(dp + wv, dv, nv);
-              if (old == dv) {
+            unsigned long long d = dv[wv];
+            unsigned long long nv = merge8(d, sv[wv], m8);
+            while (nv != d) {
+              const unsigned long long old = atomicCAS(dp + wv, d, nv);
+              if (old == d) {
                 changed = true;
                 break;
               }
-              dv = old;
-              nv = merge8(dv, sv, m8);
+              d = old;
+              nv = merge8(d, sv[wv], m8);
             }
           }
           upd += __popc(mk);
@@ -377,19 +440,16 @@ __global__ void __launch_bounds__(kThreads) k_simulate(SimArgs a) {
             if (!(atomicOr(&r.tbits[bit >> 5], m1) & m1)) ++ntouched;
           }
           if (changed)
-            push_row(u, stamp, r.lstamp, r.rev.row_chunk, r.q.rows[gn], r.q.chunks[gn], &cnt[gn],
-                     &cnt[3 + gn]);
-        }
-      }
-    }
+            push_row(u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
+        });
     grid.sync();
     if (JAC) {  // engine.cpp:81-82: re-sync snapshot rows that moved
-      const unsigned nr = ld_volatile(&cnt[3 + gn]);
+      const unsigned nr = ld_volatile(&cnt[4 + gn]);
       for (uint64_t k = gwarp; k < nr; k += nw) {
-        const uint64_t row = uint64_t(r.q.rows[gn][k]) * r.Jp;
+        const uint64_t row = uint64_t(rows_n[k]) * Jp;
         const uint4* sp4 = reinterpret_cast<const uint4*>(r.regs + row);
         uint4* dp4 = reinterpret_cast<uint4*>(r.snap + row);
-        for (uint32_t j = lane; j < r.Jp / 16; j += 32) dp4[j] = __ldcg(sp4 + j);
+        for (uint32_t j = lane; j < Jp / 16; j += 32) dp4[j] = __ldcg(sp4 + j);
       }
       if (CNT)
         for (uint64_t i = gtid; i < tb_words; i += gthreads) r.tbits[i] = 0;
@@ -548,12 +608,22 @@ __global__ void __launch_bounds__(kThreads) k_argmax(const double* __restrict__ 
     last = atomicAdd(&ra.ctl->argmax_done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    Best t{0.0, 0xFFFFFFFFu, 0xFFFFFFFFu};
-    for (uint32_t k = 0; k < gridDim.x; ++k)
-      t = best_of(t, Best{ld_volatile(ra.blk_score + k), ld_volatile(ra.blk_arg + k),
-                          ld_volatile(ra.blk_min + k)});
+  if (!last) return;
+  __threadfence();
+  Best t{0.0, 0xFFFFFFFFu, 0xFFFFFFFFu};
+  for (uint32_t k = threadIdx.x; k < gridDim.x; k += blockDim.x)
+    t = best_of(t, Best{__ldcg(ra.blk_score + k), __ldcg(ra.blk_arg + k), __ldcg(ra.blk_min + k)});
+  for (int o = 16; o; o >>= 1) {
+    Best x{__shfl_xor_sync(0xffffffffu, t.s, o), __shfl_xor_sync(0xffffffffu, t.v, o),
+           __shfl_xor_sync(0xffffffffu, t.minu, o)};
+    t = best_of(t, x);
+  }
+  __syncthreads();
+  if (lane_id() == 0) sb[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    t = sb[0];
+    for (int w = 1; w < kWarps; ++w) t = best_of(t, sb[w]);
     uint32_t choice = t.v;
     if (choice == 0xFFFFFFFFu) {  // saturated: smallest uncommitted id
       ra.ctl->saturated = 1;
@@ -572,10 +642,23 @@ struct CasArgs {
   uint32_t seed;
 };
 
+// Clear the fresh bits of the rows listed in one generation.
+__device__ __forceinline__ void clear_rows(uint32_t* f, const uint32_t* rows, unsigned nr,
+                                           uint32_t W32, uint64_t gwarp, uint64_t nw,
+                                           unsigned lane) {
+  for (uint64_t k = gwarp; k < nr; k += nw) {
+    const uint64_t row = uint64_t(__ldcg(rows + k)) * W32;
+    for (uint32_t w = lane; w < W32; w += 32) f[row + w] = 0;
+  }
+}
+
 // commit_seed + cascade (engine.cpp:106-144): level-synchronous BFS of fresh
 // VISITED bits along forward items; cand = fresh_u & live & ~vis_v.  Post:
-// VISITED_j(v) <=> v reachable from a committed seed in sample j.
+// VISITED_j(v) <=> v reachable from a committed seed in sample j.  One grid
+// barrier per level: level L reads fresh[L%3], writes fresh[(L+1)%3] and
+// clears the rows of level L-1 in fresh[(L+2)%3]; queues rotate mod 4.
 __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
+  __shared__ WarpStage stage[kWarps];
   cg::grid_group grid = cg::this_grid();
   const RankDev& r = a.r;
   unsigned int* cnt = r.q.counts;
@@ -584,10 +667,11 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
   const uint64_t gwarp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   const uint32_t W32 = r.W32;
+  WarpStage& ws = stage[threadIdx.x >> 5];
   unsigned long long marked = 0;
 
   if (gwarp == 0) {
-    if (lane < 9) cnt[lane] = 0;
+    if (lane < 16) cnt[lane] = 0;
     __syncwarp();
     const uint32_t s = a.choice ? ld_volatile(a.choice) : a.seed;
     if (lane == 0) {
@@ -614,58 +698,49 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
     __syncwarp();
     if (any && lane == 0)
       push_row(s, base + 1, r.lstamp, r.fwd.row_chunk, r.q.rows[1], r.q.chunks[1], &cnt[1],
-               &cnt[4]);
+               &cnt[5]);
   }
   grid.sync();
 
   uint32_t L = 1;
   for (;; ++L) {
-    const int g = L % 3, gn = (L + 1) % 3, gr = (L + 2) % 3;
+    const int g = L % 4, gn = (L + 1) % 4, gr = (L + 2) % 4, gp = (L + 3) % 4;
+    uint32_t* fcur = r.fresh[L % 3];
+    uint32_t* fnxt = r.fresh[(L + 1) % 3];
+    uint32_t* fprev = r.fresh[(L + 2) % 3];
     const uint32_t nc = ld_volatile(&cnt[g]);
-    if (nc == 0) break;
+    if (nc == 0) {  // done: clear what the last two levels left behind
+      clear_rows(fcur, r.q.rows[g], ld_volatile(&cnt[4 + g]), W32, gwarp, nw, lane);
+      clear_rows(fprev, r.q.rows[gp], ld_volatile(&cnt[4 + gp]), W32, gwarp, nw, lane);
+      break;
+    }
     if (gwarp == 0 && lane == 0) {
       cnt[gr] = 0;
-      cnt[3 + gr] = 0;
-      cnt[6 + gr] = 0;
+      cnt[4 + gr] = 0;
+      cnt[8 + gr] = 0;
     }
-    const uint32_t* fcur = r.fresh[L & 1];
-    uint32_t* fnxt = r.fresh[(L + 1) & 1];
+    clear_rows(fprev, r.q.rows[gp], ld_volatile(&cnt[4 + gp]), W32, gwarp, nw, lane);
     const uint32_t stamp = base + L + 1;
-    for (;;) {
-      unsigned ci = 0;
-      if (lane == 0) ci = atomicAdd(&cnt[6 + g], 1u);
-      ci = __shfl_sync(0xffffffffu, ci, 0);
-      if (ci >= nc) break;
-      const uint32_t c = r.q.chunks[g][ci];
-      const uint32_t u = r.fwd.chunk_row[c];
-      const uint64_t beg = r.fwd.chunk_beg[c], end = r.fwd.chunk_beg[c + 1];
-      for (uint64_t i = beg + lane; i < end; i += 32) {
-        const uint32_t b = r.fwd.batch[i];
-        uint32_t cand = __ldcg(fcur + uint64_t(u) * W32 + b) & r.fwd.mask[i];
-        if (!cand) continue;
-        const uint32_t v = r.fwd.other[i];
-        uint32_t* vw = r.vis + uint64_t(v) * W32 + b;
-        cand &= ~__ldcg(vw);
-        if (!cand) continue;
-        const uint32_t nb = cand & ~atomicOr(vw, cand);
-        if (!nb) continue;
-        int8_t* rb = r.regs + uint64_t(v) * r.Jp + b * 32;
-        for (uint32_t t = nb; t; t &= t - 1) rb[__ffs(t) - 1] = -1;
-        atomicOr(fnxt + uint64_t(v) * W32 + b, nb);
-        marked += __popc(nb);
-        if (atomicExch(&r.dstamp[v], base) != base) r.dirty[atomicAdd(&r.ctl->dirty_count, 1u)] = v;
-        push_row(v, stamp, r.lstamp, r.fwd.row_chunk, r.q.rows[gn], r.q.chunks[gn], &cnt[gn],
-                 &cnt[3 + gn]);
-      }
-    }
-    grid.sync();
-    // engine.cpp:137-139: clear the consumed fresh rows.
-    const unsigned nr = ld_volatile(&cnt[3 + g]);
-    uint32_t* fc = r.fresh[L & 1];
-    for (uint64_t k = gwarp; k < nr; k += nw) {
-      const uint64_t row = uint64_t(r.q.rows[g][k]) * W32;
-      for (uint32_t w = lane; w < W32; w += 32) fc[row + w] = 0;
-    }
+    uint32_t* rows_n = r.q.rows[gn];
+    uint32_t* chunks_n = r.q.chunks[gn];
+    for_frontier_items(r.fwd, r.q.chunks[g], nc, &cnt[8 + g], ws, [&](uint32_t u, uint64_t i) {
+      const uint32_t b = __ldg(r.fwd.batch + i);
+      uint32_t cand = __ldcg(fcur + uint64_t(u) * W32 + b) & __ldg(r.fwd.mask + i);
+      if (!cand) return;
+      const uint32_t v = __ldg(r.fwd.other + i);
+      uint32_t* vw = r.vis + uint64_t(v) * W32 + b;
+      cand &= ~__ldcg(vw);
+      if (!cand) return;
+      const uint32_t nb = cand & ~atomicOr(vw, cand);
+      if (!nb) return;
+      int8_t* rb = r.regs + uint64_t(v) * r.Jp + b * 32;
+      for (uint32_t t = nb; t; t &= t - 1) rb[__ffs(t) - 1] = -1;
+      atomicOr(fnxt + uint64_t(v) * W32 + b, nb);
+      marked += __popc(nb);
+      if (ld_volatile(&r.dstamp[v]) != base && atomicExch(&r.dstamp[v], base) != base)
+        r.dirty[atomicAdd(&r.ctl->dirty_count, 1u)] = v;
+      push_row(v, stamp, r.lstamp, r.fwd.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
+    });
     grid.sync();
   }
   for (int o = 16; o; o >>= 1) marked += __shfl_xor_sync(0xffffffffu, marked, o);
@@ -831,6 +906,11 @@ int coop_grid(int which, int variant) {
     const void* fn = which == 0 ? sim_kernel(variant) : (const void*)k_cascade;
     DFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kThreads, 0));
     if (per < 1) per = 1;
+    // Tunables (blocks per SM): a smaller cascade grid makes its per-level
+    // grid barrier cheaper; frontiers there are usually small.
+    const char* env = getenv(which == 0 ? "DFS_SIM_BPS" : "DFS_CAS_BPS");
+    int want = env ? atoi(env) : (which == 0 ? per : 2);
+    if (want >= 1 && want < per) per = want;
     g[slot] = per * num_sms();
   }
   return g[slot];

@@ -132,6 +132,7 @@ void Context::alloc_rank(RankDev& r, uint32_t tau) {
   r.vis = as<uint32_t>(arena_.get(p + "vis", nn * r.W32 * 4));
   r.fresh[0] = as<uint32_t>(arena_.get(p + "fresh0", nn * r.W32 * 4));
   r.fresh[1] = as<uint32_t>(arena_.get(p + "fresh1", nn * r.W32 * 4));
+  r.fresh[2] = as<uint32_t>(arena_.get(p + "fresh2", nn * r.W32 * 4));
   r.lstamp = as<uint32_t>(arena_.get(p + "lstamp", nn * 4));
   r.dstamp = as<uint32_t>(arena_.get(p + "dstamp", nn * 4));
   r.dirty = as<uint32_t>(arena_.get(p + "dirty", nn * 4));
@@ -193,6 +194,7 @@ void Context::reset_rank_state(RankDev& r) {
   DFS_CUDA(cudaMemsetAsync(r.vis, 0, nn * r.W32 * 4, stream_));
   DFS_CUDA(cudaMemsetAsync(r.fresh[0], 0, nn * r.W32 * 4, stream_));
   DFS_CUDA(cudaMemsetAsync(r.fresh[1], 0, nn * r.W32 * 4, stream_));
+  DFS_CUDA(cudaMemsetAsync(r.fresh[2], 0, nn * r.W32 * 4, stream_));
   DFS_CUDA(cudaMemsetAsync(r.lstamp, 0, nn * 4, stream_));
   DFS_CUDA(cudaMemsetAsync(r.dstamp, 0, nn * 4, stream_));
   DFS_CUDA(cudaMemsetAsync(r.regs, 0, nn * r.Jp, stream_));
@@ -258,7 +260,7 @@ void Context::prepare(const RunConfig& cfg, const HostGraph* host_w_src) {
     build_items(r, 1);
     const std::string p = "r" + std::to_string(t) + ".q.";
     const uint64_t cap = std::max<uint64_t>(std::max(r.fwd.chunks, r.rev.chunks), 1);
-    for (int gi = 0; gi < 3; ++gi) {
+    for (int gi = 0; gi < kGens; ++gi) {
       r.q.chunks[gi] = as<uint32_t>(arena_.get(p + "c" + std::to_string(gi), cap * 4));
       r.q.rows[gi] = as<uint32_t>(arena_.get(p + "r" + std::to_string(gi),
                                              std::max<uint32_t>(g_.n, 1) * 4));
