@@ -57,6 +57,7 @@ struct Items {
   uint64_t count = 0;
   uint64_t chunks = 0;
   uint64_t* row_off = nullptr;     // n+1 item offsets per row
+  uint32_t* row = nullptr;         // count (row of each item: flat full-pass sweeps)
   uint32_t* other = nullptr;       // count
   uint32_t* mask = nullptr;        // count
   uint8_t* batch = nullptr;        // count

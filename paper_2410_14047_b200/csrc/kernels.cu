@@ -142,7 +142,7 @@ __global__ void k_items(uint64_t npos, int dir, const uint32_t* __restrict__ ted
                         const uint32_t* __restrict__ x, uint32_t J, uint32_t Jp, int fasst,
                         uint32_t* __restrict__ cnt, const uint64_t* __restrict__ pos_off,
                         uint32_t* __restrict__ it_other, uint32_t* __restrict__ it_mask,
-                        uint8_t* __restrict__ it_batch) {
+                        uint8_t* __restrict__ it_batch, uint32_t* __restrict__ it_row) {
   extern __shared__ uint32_t sx[];
   for (uint32_t i = threadIdx.x; i < Jp; i += blockDim.x) sx[i] = x[i];
   __syncthreads();
@@ -158,6 +158,7 @@ __global__ void k_items(uint64_t npos, int dir, const uint32_t* __restrict__ ted
       if (hi > lo) {
         uint64_t o = WRITE ? pos_off[p] : 0;
         const uint32_t other = WRITE ? (dir ? src[e] : adj[e]) : 0;
+        const uint32_t rowv = WRITE ? (dir ? adj[e] : src[e]) : 0;
         for (uint32_t b = lo >> 5; b <= (hi - 1) >> 5; ++b) {
           uint32_t mk = 0;
           const uint32_t* xb = sx + b * 32;
@@ -166,6 +167,7 @@ __global__ void k_items(uint64_t npos, int dir, const uint32_t* __restrict__ ted
           if (mk) {
             if (WRITE) {
               it_other[o] = other;
+              it_row[o] = rowv;
               it_mask[o] = mk;
               it_batch[o] = uint8_t(b);
               ++o;
@@ -334,6 +336,54 @@ __device__ __forceinline__ void for_frontier_items(const Items& it, const uint32
   }
 }
 
+// One reverse item staged for the merge: fields + src/dst words (issued
+// before any is consumed so a thread keeps several loads in flight).
+struct SimItem {
+  uint32_t u, mk, b;
+  unsigned long long* dp;
+  unsigned long long sv[4], dv[4];
+};
+
+__device__ __forceinline__ void sim_fields(SimItem& it, const Items& rev, uint64_t i) {
+  it.u = __ldg(rev.other + i);
+  it.mk = __ldg(rev.mask + i);
+  it.b = __ldg(rev.batch + i);
+}
+
+__device__ __forceinline__ void sim_data(SimItem& it, const int8_t* srow, int8_t* regs,
+                                         uint32_t Jp) {
+  const unsigned long long* sp = reinterpret_cast<const unsigned long long*>(srow + it.b * 32);
+  it.dp = reinterpret_cast<unsigned long long*>(regs + uint64_t(it.u) * Jp + it.b * 32);
+#pragma unroll
+  for (int wv = 0; wv < 4; ++wv)
+    if ((it.mk >> (8 * wv)) & 0xFFu) {
+      it.sv[wv] = __ldcg(sp + wv);
+      it.dv[wv] = __ldcg(it.dp + wv);
+    }
+}
+
+// Lock-free byte max (engine.cpp:22-53 semantics) of the staged words.
+__device__ __forceinline__ bool sim_merge(SimItem& it) {
+  bool changed = false;
+#pragma unroll
+  for (int wv = 0; wv < 4; ++wv) {
+    const uint32_t m8 = (it.mk >> (8 * wv)) & 0xFFu;
+    if (!m8) continue;
+    unsigned long long d = it.dv[wv];
+    unsigned long long nv = merge8(d, it.sv[wv], m8);
+    while (nv != d) {
+      const unsigned long long old = atomicCAS(it.dp + wv, d, nv);
+      if (old == d) {
+        changed = true;
+        break;
+      }
+      d = old;
+      nv = merge8(d, it.sv[wv], m8);
+    }
+  }
+  return changed;
+}
+
 struct SimArgs {
   RankDev r;
   int cap;
@@ -348,8 +398,11 @@ struct SimArgs {
 // reads the snapshot and re-syncs changed rows after each sweep, which
 // reproduces the reference's sweep count exactly.  CNT = 1 (Jacobi only)
 // tallies the reference-schedule work units of SURVEY.md §8(d).
+#ifndef DFS_SIM_MINB
+#define DFS_SIM_MINB 3
+#endif
 template <int JAC, int CNT>
-__global__ void __launch_bounds__(kThreads) k_simulate(SimArgs a) {
+__global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) {
   if (a.gate && ld_volatile(a.gate) != a.want) return;  // grid-uniform
   __shared__ WarpStage stage[kWarps];
   cg::grid_group grid = cg::this_grid();
@@ -395,53 +448,62 @@ __global__ void __launch_bounds__(kThreads) k_simulate(SimArgs a) {
     const uint32_t stamp = base + s;
     uint32_t* rows_n = r.q.rows[gn];
     uint32_t* chunks_n = r.q.chunks[gn];
-    for_frontier_items(
-        r.rev, s == 1 ? nullptr : r.q.chunks[g], nc, &cnt[8 + g], ws,
-        [&](uint32_t v, uint64_t i) {
-          const uint32_t u = __ldg(r.rev.other + i);
-          const uint32_t mk = __ldg(r.rev.mask + i);
-          const uint32_t b = __ldg(r.rev.batch + i);
-          const unsigned long long* sp =
-              reinterpret_cast<const unsigned long long*>(srcm + uint64_t(v) * Jp + b * 32);
-          unsigned long long* dp =
-              reinterpret_cast<unsigned long long*>(r.regs + uint64_t(u) * Jp + b * 32);
-          unsigned long long sv[4], dv[4];
-#pragma unroll
-          for (int wv = 0; wv < 4; ++wv)  // issue all loads first (MLP)
-            if ((mk >> (8 * wv)) & 0xFFu) {
-              sv[wv] = __ldcg(sp + wv);
-              dv[wv] = __ldcg(dp + wv);
-            }
-          bool changed = false;
-#pragma unroll
-          for (int wv = 0; wv < 4; ++wv) {
-            const uint32_t m8 = (mk >> (8 * wv)) & 0xFFu;
-            if (!m8) continue;
-            unsigned long long d = dv[wv];
-            unsigned long long nv = merge8(d, sv[wv], m8);
-            while (nv != d) {
-              const unsigned long long old = atomicCAS(dp + wv, d, nv);
-              if (old == d) {
-                changed = true;
-                break;
-              }
-              d = old;
-              nv = merge8(d, sv[wv], m8);
-            }
-          }
-          upd += __popc(mk);
+    // Large frontiers (and sweep 1): flat pass over all items, rows filtered
+    // by their change stamp, two items in flight per thread.  Small ones: the
+    // chunk frontier.  Count mode keeps the exact frontier schedule.
+    const bool full = !CNT && (s == 1 || uint64_t(nc) * 4 > r.rev.chunks);
+    if (full) {
+      const uint32_t need = base + s - 1;  // changed in sweep s-1 (or later)
+      const uint64_t cntI = r.rev.count;
+      for (uint64_t i = gtid; i < cntI; i += 2 * gthreads) {
+        const uint64_t i1 = i + gthreads;
+        const uint32_t va = __ldg(r.rev.row + i);
+        const uint32_t vb = i1 < cntI ? __ldg(r.rev.row + i1) : 0;
+        const bool pa = s == 1 || __ldcg(r.lstamp + va) >= need;
+        const bool pb = i1 < cntI && (s == 1 || __ldcg(r.lstamp + vb) >= need);
+        SimItem A, B;
+        if (pa) sim_fields(A, r.rev, i);
+        if (pb) sim_fields(B, r.rev, i1);
+        if (pa) sim_data(A, srcm + uint64_t(va) * Jp, r.regs, Jp);
+        if (pb) sim_data(B, srcm + uint64_t(vb) * Jp, r.regs, Jp);
+        if (pa) {
+          upd += __popc(A.mk);
           ++nitems;
-          if (CNT) {
-            // E: first item of its edge (items of one edge are consecutive, same u)
-            if (i == r.rev.row_off[v] || r.rev.other[i - 1] != u) ++nedges;
-            // T: distinct (u, b) touched in this sweep
-            const uint64_t bit = uint64_t(u) * r.W32 + b;
-            const uint32_t m1 = 1u << (bit & 31);
-            if (!(atomicOr(&r.tbits[bit >> 5], m1) & m1)) ++ntouched;
-          }
-          if (changed)
-            push_row(u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
-        });
+          if (sim_merge(A))
+            push_row(A.u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &cnt[gn],
+                     &cnt[4 + gn]);
+        }
+        if (pb) {
+          upd += __popc(B.mk);
+          ++nitems;
+          if (sim_merge(B))
+            push_row(B.u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &cnt[gn],
+                     &cnt[4 + gn]);
+        }
+      }
+    } else {
+      for_frontier_items(
+          r.rev, s == 1 ? nullptr : r.q.chunks[g], nc, &cnt[8 + g], ws,
+          [&](uint32_t v, uint64_t i) {
+            SimItem A;
+            sim_fields(A, r.rev, i);
+            sim_data(A, srcm + uint64_t(v) * Jp, r.regs, Jp);
+            const bool changed = sim_merge(A);
+            upd += __popc(A.mk);
+            ++nitems;
+            if (CNT) {
+              // E: first item of its edge (items of one edge are consecutive, same u)
+              if (i == r.rev.row_off[v] || r.rev.other[i - 1] != A.u) ++nedges;
+              // T: distinct (u, b) touched in this sweep
+              const uint64_t bit = uint64_t(A.u) * r.W32 + A.b;
+              const uint32_t m1 = 1u << (bit & 31);
+              if (!(atomicOr(&r.tbits[bit >> 5], m1) & m1)) ++ntouched;
+            }
+            if (changed)
+              push_row(A.u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &cnt[gn],
+                       &cnt[4 + gn]);
+          });
+    }
     grid.sync();
     if (JAC) {  // engine.cpp:81-82: re-sync snapshot rows that moved
       const unsigned nr = ld_volatile(&cnt[4 + gn]);
@@ -723,7 +785,7 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
     const uint32_t stamp = base + L + 1;
     uint32_t* rows_n = r.q.rows[gn];
     uint32_t* chunks_n = r.q.chunks[gn];
-    for_frontier_items(r.fwd, r.q.chunks[g], nc, &cnt[8 + g], ws, [&](uint32_t u, uint64_t i) {
+    auto visit = [&](uint32_t u, uint64_t i) {
       const uint32_t b = __ldg(r.fwd.batch + i);
       uint32_t cand = __ldcg(fcur + uint64_t(u) * W32 + b) & __ldg(r.fwd.mask + i);
       if (!cand) return;
@@ -740,7 +802,14 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
       if (ld_volatile(&r.dstamp[v]) != base && atomicExch(&r.dstamp[v], base) != base)
         r.dirty[atomicAdd(&r.ctl->dirty_count, 1u)] = v;
       push_row(v, stamp, r.lstamp, r.fwd.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
-    });
+    };
+    if (uint64_t(nc) * 4 > r.fwd.chunks) {  // large frontier: flat pass over all items
+      const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+      const uint64_t gthreads = uint64_t(gridDim.x) * blockDim.x;
+      for (uint64_t i = gtid; i < r.fwd.count; i += gthreads) visit(__ldg(r.fwd.row + i), i);
+    } else {
+      for_frontier_items(r.fwd, r.q.chunks[g], nc, &cnt[8 + g], ws, visit);
+    }
     grid.sync();
   }
   for (int o = 16; o; o >>= 1) marked += __shfl_xor_sync(0xffffffffu, marked, o);
@@ -858,10 +927,11 @@ void launch_items_pass(const DevGraph& g, const uint32_t* w, const RankDev& r, i
   if (write)
     k_items<1><<<grid, kThreads, smem, s>>>(g.m, dir, g.tedge, g.adj, g.src, g.ehash, w, r.x, r.J,
                                             r.Jp, fasst, cnt, pos_off, it.other, it.mask,
-                                            it.batch);
+                                            it.batch, it.row);
   else
     k_items<0><<<grid, kThreads, smem, s>>>(g.m, dir, g.tedge, g.adj, g.src, g.ehash, w, r.x, r.J,
-                                            r.Jp, fasst, cnt, pos_off, nullptr, nullptr, nullptr);
+                                            r.Jp, fasst, cnt, pos_off, nullptr, nullptr, nullptr,
+                                            nullptr);
   DFS_CUDA(cudaGetLastError());
   ++g_launches;
 }
@@ -909,7 +979,7 @@ int coop_grid(int which, int variant) {
     // Tunables (blocks per SM): a smaller cascade grid makes its per-level
     // grid barrier cheaper; frontiers there are usually small.
     const char* env = getenv(which == 0 ? "DFS_SIM_BPS" : "DFS_CAS_BPS");
-    int want = env ? atoi(env) : (which == 0 ? per : 2);
+    int want = env ? atoi(env) : per;
     if (want >= 1 && want < per) per = want;
     g[slot] = per * num_sms();
   }

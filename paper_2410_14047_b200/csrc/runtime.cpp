@@ -170,6 +170,7 @@ void Context::build_items(RankDev& r, int dir) {
   sync();
   const size_t ic = std::max<uint64_t>(it.count, 1);
   it.other = as<uint32_t>(arena_.get(p + "other", ic * 4));
+  it.row = as<uint32_t>(arena_.get(p + "row", ic * 4));
   it.mask = as<uint32_t>(arena_.get(p + "mask", ic * 4));
   it.batch = as<uint8_t>(arena_.get(p + "batch", ic));
   it.row_off = as<uint64_t>(arena_.get(p + "row_off", (size_t(n) + 1) * 8));
