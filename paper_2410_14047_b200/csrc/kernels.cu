@@ -336,6 +336,35 @@ __device__ __forceinline__ void for_frontier_items(const Items& it, const uint32
   }
 }
 
+constexpr unsigned long long kNeg8 = 0x8080808080808080ull;  // "no contribution"
+constexpr uint32_t kPullMaxJp = 4096;  // pull accumulators live in shared memory
+
+// Shared-memory running max of the live bytes of one source word.
+__device__ __forceinline__ void acc_max(unsigned long long* a, unsigned long long sv, uint32_t m8) {
+  const uint32_t blo = expand4(m8 & 15u), bhi = expand4(m8 >> 4);
+  const uint32_t slo = (uint32_t(sv) & blo) | (0x80808080u & ~blo);
+  const uint32_t shi = (uint32_t(sv >> 32) & bhi) | (0x80808080u & ~bhi);
+  unsigned long long old = *a;
+  for (;;) {
+    const unsigned long long nv =
+        (static_cast<unsigned long long>(__vmaxs4(uint32_t(old >> 32), shi)) << 32) |
+        __vmaxs4(uint32_t(old), slo);
+    if (nv == old) return;
+    const unsigned long long prev = atomicCAS(a, old, nv);
+    if (prev == old) return;
+    old = prev;
+  }
+}
+
+// dst = max(dst, a) bytewise with VISITED dst absorbing (a already masked).
+__device__ __forceinline__ unsigned long long merge8_full(unsigned long long d,
+                                                          unsigned long long a) {
+  const uint32_t lo = __vmaxs4(uint32_t(d), uint32_t(a)) | __vcmpeq4(uint32_t(d), 0xFFFFFFFFu);
+  const uint32_t hi =
+      __vmaxs4(uint32_t(d >> 32), uint32_t(a >> 32)) | __vcmpeq4(uint32_t(d >> 32), 0xFFFFFFFFu);
+  return (static_cast<unsigned long long>(hi) << 32) | lo;
+}
+
 // One reverse item staged for the merge: fields + src/dst words (issued
 // before any is consumed so a thread keeps several loads in flight).
 struct SimItem {
@@ -415,6 +444,17 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) 
   const uint64_t gwarp = gtid >> 5;
   const uint64_t nw = gthreads >> 5;
   WarpStage& ws = stage[threadIdx.x >> 5];
+  // Pull accumulator: Jp bytes of running maxima + touched-batch bits per warp.
+  extern __shared__ unsigned long long dyn_smem[];
+  const uint32_t W32 = r.W32;
+  const bool pull_ok = r.Jp <= kPullMaxJp;
+  unsigned long long* acc = dyn_smem + (threadIdx.x >> 5) * (kPullMaxJp / 8 + 8);
+  uint32_t* touched = reinterpret_cast<uint32_t*>(acc + r.Jp / 8);
+  if (pull_ok) {
+    for (uint32_t w = lane; w < r.Jp / 8; w += 32) acc[w] = kNeg8;
+    if (lane < 4) touched[lane] = 0;
+    __syncwarp();
+  }
   if (gwarp == 0 && lane < 16) cnt[lane] = 0;
   if (JAC) {  // SimulateBuffers::reset (engine.cpp:9-15): snapshot := registers
     const uint64_t n16 = uint64_t(r.n) * r.Jp / 16;
@@ -451,35 +491,74 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) 
     // Large frontiers (and sweep 1): flat pass over all items, rows filtered
     // by their change stamp, two items in flight per thread.  Small ones: the
     // chunk frontier.  Count mode keeps the exact frontier schedule.
-    const bool full = !CNT && (s == 1 || uint64_t(nc) * 4 > r.rev.chunks);
-    if (full) {
-      const uint32_t need = base + s - 1;  // changed in sweep s-1 (or later)
-      const uint64_t cntI = r.rev.count;
-      for (uint64_t i = gtid; i < cntI; i += 2 * gthreads) {
-        const uint64_t i1 = i + gthreads;
-        const uint32_t va = __ldg(r.rev.row + i);
-        const uint32_t vb = i1 < cntI ? __ldg(r.rev.row + i1) : 0;
-        const bool pa = s == 1 || __ldcg(r.lstamp + va) >= need;
-        const bool pb = i1 < cntI && (s == 1 || __ldcg(r.lstamp + vb) >= need);
-        SimItem A, B;
-        if (pa) sim_fields(A, r.rev, i);
-        if (pb) sim_fields(B, r.rev, i1);
-        if (pa) sim_data(A, srcm + uint64_t(va) * Jp, r.regs, Jp);
-        if (pb) sim_data(B, srcm + uint64_t(vb) * Jp, r.regs, Jp);
-        if (pa) {
-          upd += __popc(A.mk);
+    // Large frontiers (and sweep 1) run PULL-style over row-owned forward
+    // chunks: a warp gathers the sources of one destination row chunk into a
+    // shared-memory accumulator and writes each touched word once (plain store
+    // when it owns the row, CAS otherwise), so out-hub rows see one update per
+    // chunk instead of one contended CAS per item.  Small frontiers push.
+    // Count mode keeps the exact push frontier of the reference schedule.
+    const bool pull = !CNT && pull_ok && (s == 1 || uint64_t(nc) * 4 > r.rev.chunks);
+    if (pull) {
+      const uint32_t need = base + s - 1;  // source changed in sweep s-1 (or later)
+      for (uint64_t c = gwarp; c < r.fwd.chunks; c += nw) {
+        const uint32_t u = r.fwd.chunk_row[c];
+        const uint64_t beg = r.fwd.chunk_beg[c], end = r.fwd.chunk_beg[c + 1];
+        for (uint64_t i = beg + lane; i < end; i += 32) {
+          const uint32_t v = __ldg(r.fwd.other + i);
+          if (s > 1 && __ldcg(r.lstamp + v) < need) continue;
+          const uint32_t mk = __ldg(r.fwd.mask + i);
+          const uint32_t b = __ldg(r.fwd.batch + i);
+          const unsigned long long* sp =
+              reinterpret_cast<const unsigned long long*>(srcm + uint64_t(v) * Jp + b * 32);
+          unsigned long long sv[4];
+#pragma unroll
+          for (int wv = 0; wv < 4; ++wv)
+            if ((mk >> (8 * wv)) & 0xFFu) sv[wv] = __ldcg(sp + wv);
+#pragma unroll
+          for (int wv = 0; wv < 4; ++wv) {
+            const uint32_t m8 = (mk >> (8 * wv)) & 0xFFu;
+            if (m8) acc_max(&acc[b * 4 + wv], sv[wv], m8);
+          }
+          atomicOr(&touched[b >> 5], 1u << (b & 31));
+          upd += __popc(mk);
           ++nitems;
-          if (sim_merge(A))
-            push_row(A.u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &cnt[gn],
-                     &cnt[4 + gn]);
         }
-        if (pb) {
-          upd += __popc(B.mk);
-          ++nitems;
-          if (sim_merge(B))
-            push_row(B.u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &cnt[gn],
-                     &cnt[4 + gn]);
+        __syncwarp();
+        const bool owner = r.fwd.row_chunk[u + 1] - r.fwd.row_chunk[u] == 1;
+        unsigned long long* drow = reinterpret_cast<unsigned long long*>(r.regs + uint64_t(u) * Jp);
+        bool changed = false;
+        for (uint32_t b = lane; b < W32; b += 32) {
+          if (!((touched[b >> 5] >> (b & 31)) & 1u)) continue;
+#pragma unroll
+          for (int wv = 0; wv < 4; ++wv) {
+            const unsigned long long a = acc[b * 4 + wv];
+            if (a == kNeg8) continue;
+            acc[b * 4 + wv] = kNeg8;
+            unsigned long long* dp = drow + b * 4 + wv;
+            unsigned long long d = __ldcg(dp);
+            unsigned long long nv = merge8_full(d, a);
+            if (nv == d) continue;
+            if (owner) {
+              *dp = nv;
+              changed = true;
+            } else {
+              while (nv != d) {
+                const unsigned long long old = atomicCAS(dp, d, nv);
+                if (old == d) {
+                  changed = true;
+                  break;
+                }
+                d = old;
+                nv = merge8_full(d, a);
+              }
+            }
+          }
         }
+        __syncwarp();
+        if (lane < 4) touched[lane] = 0;
+        __syncwarp();
+        if (__any_sync(0xffffffffu, changed) && lane == 0)
+          push_row(u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
       }
     } else {
       for_frontier_items(
@@ -731,6 +810,13 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
   const uint32_t W32 = r.W32;
   WarpStage& ws = stage[threadIdx.x >> 5];
   unsigned long long marked = 0;
+  extern __shared__ uint32_t cas_smem[];
+  const bool pull_ok = r.Jp <= kPullMaxJp;
+  uint32_t* cacc = cas_smem + (threadIdx.x >> 5) * (kPullMaxJp / 32);
+  if (pull_ok) {
+    for (uint32_t w = lane; w < W32; w += 32) cacc[w] = 0;
+    __syncwarp();
+  }
 
   if (gwarp == 0) {
     if (lane < 16) cnt[lane] = 0;
@@ -803,10 +889,57 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
         r.dirty[atomicAdd(&r.ctl->dirty_count, 1u)] = v;
       push_row(v, stamp, r.lstamp, r.fwd.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
     };
-    if (uint64_t(nc) * 4 > r.fwd.chunks) {  // large frontier: flat pass over all items
-      const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-      const uint64_t gthreads = uint64_t(gridDim.x) * blockDim.x;
-      for (uint64_t i = gtid; i < r.fwd.count; i += gthreads) visit(__ldg(r.fwd.row + i), i);
+    if (pull_ok && uint64_t(nc) * 4 > r.fwd.chunks) {
+      // Large frontier: bottom-up (pull) level over row-owned reverse chunks.
+      // A warp ORs the fresh bits of all in-neighbours of one target row into
+      // a shared accumulator, then claims the unvisited ones with one update
+      // per batch word (direction-optimising BFS, Beamer et al.).
+      for (uint64_t c = gwarp; c < r.rev.chunks; c += nw) {
+        const uint32_t v = r.rev.chunk_row[c];
+        const uint64_t beg = r.rev.chunk_beg[c], end = r.rev.chunk_beg[c + 1];
+        bool any = false;
+        for (uint64_t i = beg + lane; i < end; i += 32) {
+          const uint32_t b = __ldg(r.rev.batch + i);
+          const uint32_t f =
+              __ldcg(fcur + uint64_t(__ldg(r.rev.other + i)) * W32 + b) & __ldg(r.rev.mask + i);
+          if (f) {
+            atomicOr(&cacc[b], f);
+            any = true;
+          }
+        }
+        if (!__any_sync(0xffffffffu, any)) continue;
+        __syncwarp();
+        const bool owner = r.rev.row_chunk[v + 1] - r.rev.row_chunk[v] == 1;
+        bool got = false;
+        for (uint32_t b = lane; b < W32; b += 32) {
+          uint32_t a = cacc[b];
+          if (!a) continue;
+          cacc[b] = 0;
+          uint32_t* vw = r.vis + uint64_t(v) * W32 + b;
+          a &= ~__ldcg(vw);
+          if (!a) continue;
+          uint32_t nb;
+          if (owner) {
+            nb = a;
+            *vw = __ldcg(vw) | a;
+          } else {
+            nb = a & ~atomicOr(vw, a);
+            if (!nb) continue;
+          }
+          int8_t* rb = r.regs + uint64_t(v) * r.Jp + b * 32;
+          for (uint32_t t = nb; t; t &= t - 1) rb[__ffs(t) - 1] = -1;
+          if (owner) fnxt[uint64_t(v) * W32 + b] |= nb;
+          else atomicOr(fnxt + uint64_t(v) * W32 + b, nb);
+          marked += __popc(nb);
+          got = true;
+        }
+        __syncwarp();
+        if (__any_sync(0xffffffffu, got) && lane == 0) {
+          if (ld_volatile(&r.dstamp[v]) != base && atomicExch(&r.dstamp[v], base) != base)
+            r.dirty[atomicAdd(&r.ctl->dirty_count, 1u)] = v;
+          push_row(v, stamp, r.lstamp, r.fwd.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
+        }
+      }
     } else {
       for_frontier_items(r.fwd, r.q.chunks[g], nc, &cnt[8 + g], ws, visit);
     }
@@ -960,6 +1093,9 @@ void launch_fill(const RankDev& r, const unsigned int* gate, unsigned int want, 
   ++g_launches;
 }
 
+constexpr size_t kSimSmem = size_t(kWarps) * (kPullMaxJp / 8 + 8) * 8;
+constexpr size_t kCasSmem = size_t(kWarps) * (kPullMaxJp / 32) * 4;
+
 static const void* sim_kernel(int variant) {
   switch (variant) {
     case 0: return (const void*)k_simulate<0, 0>;
@@ -974,7 +1110,12 @@ int coop_grid(int which, int variant) {
   if (!g[slot]) {
     int per = 0;
     const void* fn = which == 0 ? sim_kernel(variant) : (const void*)k_cascade;
-    DFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kThreads, 0));
+    if (which == 0)
+      DFS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSimSmem));
+    else
+      DFS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kCasSmem));
+    DFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kThreads,
+                                                           which == 0 ? kSimSmem : kCasSmem));
     if (per < 1) per = 1;
     // Tunables (blocks per SM): a smaller cascade grid makes its per-level
     // grid barrier cheaper; frontiers there are usually small.
@@ -992,7 +1133,7 @@ void launch_simulate(const RankDev& r, int jacobi, int count, int cap, const uns
   void* args[] = {&a};
   const int variant = jacobi ? (count ? 2 : 1) : 0;
   DFS_CUDA(cudaLaunchCooperativeKernel(sim_kernel(variant), dim3(coop_grid(0, variant)),
-                                       dim3(kThreads), args, 0, s));
+                                       dim3(kThreads), args, kSimSmem, s));
   ++g_launches;
 }
 
@@ -1025,7 +1166,7 @@ void launch_cascade(const RankDev& r, const unsigned int* choice, uint32_t seed,
   CasArgs a{r, choice, seed};
   void* args[] = {&a};
   DFS_CUDA(cudaLaunchCooperativeKernel((void*)k_cascade, dim3(coop_grid(1)), dim3(kThreads), args,
-                                       0, s));
+                                       kCasSmem, s));
   ++g_launches;
 }
 
