@@ -64,7 +64,13 @@ struct Items {
   uint32_t* chunk_row = nullptr;   // chunks
   uint64_t* chunk_beg = nullptr;   // chunks+1
   uint32_t* row_chunk = nullptr;   // n+1 first chunk of each row
+  // chunk ids split by row size: rows with <= kSmallRow items (one chunk,
+  // processed item-parallel) and larger rows (processed warp-per-chunk pull)
+  uint32_t* small = nullptr;
+  uint32_t* big = nullptr;
+  uint32_t nsmall = 0, nbig = 0;
 };
+constexpr uint32_t kSmallRow = 32;
 
 // Device-resident control block of one rank (sample-space partition tau).
 struct RankCtl {
@@ -159,6 +165,8 @@ void launch_items_pass(const DevGraph& g, const uint32_t* w, const RankDev& r, i
 void launch_row_offsets(const DevGraph& g, int dir, const uint64_t* pos_off, Items& it,
                         uint32_t* row_cnt, cudaStream_t s);
 void launch_chunk_write(uint32_t n, Items& it, const uint64_t* row_chunk64, cudaStream_t s);
+// Split chunk ids into it.small / it.big (counts written to cnt2[0..1]).
+void launch_split_chunks(Items& it, unsigned int* cnt2, cudaStream_t s);
 // Fill registers (VISITED kept, pads VISITED).  gate: run only if *gate == want.
 void launch_fill(const RankDev& r, const unsigned int* gate, unsigned int want, cudaStream_t s);
 // Persistent cooperative simulate to convergence.  jacobi != 0 reproduces the

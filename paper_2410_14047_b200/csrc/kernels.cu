@@ -214,6 +214,32 @@ __global__ void k_chunk_write(uint32_t n, const uint64_t* __restrict__ row_chunk
   }
 }
 
+__global__ void k_split_chunks(uint64_t chunks, const uint32_t* __restrict__ chunk_row,
+                               const uint64_t* __restrict__ row_off, uint32_t* __restrict__ small,
+                               uint32_t* __restrict__ big, unsigned int* cnt2) {
+  for (uint64_t c0 = uint64_t(blockIdx.x) * blockDim.x; c0 < chunks;
+       c0 += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t c = c0 + threadIdx.x;
+    bool isb = false, valid = c < chunks;
+    if (valid) {
+      const uint32_t r = chunk_row[c];
+      isb = row_off[r + 1] - row_off[r] > kSmallRow;
+    }
+    const unsigned mb = __ballot_sync(0xffffffffu, valid && isb);
+    const unsigned ms = __ballot_sync(0xffffffffu, valid && !isb);
+    unsigned bb = 0, bs = 0;
+    if (lane_id() == 0) {
+      if (mb) bb = atomicAdd(&cnt2[1], __popc(mb));
+      if (ms) bs = atomicAdd(&cnt2[0], __popc(ms));
+    }
+    bb = __shfl_sync(0xffffffffu, bb, 0);
+    bs = __shfl_sync(0xffffffffu, bs, 0);
+    const unsigned below = (1u << lane_id()) - 1;
+    if (valid && isb) big[bb + __popc(mb & below)] = uint32_t(c);
+    if (valid && !isb) small[bs + __popc(ms & below)] = uint32_t(c);
+  }
+}
+
 // ---------------------------------------------------------------- fill
 // sketch.cpp:55-66: M[u][j] = clz64(fmix64(jkey[j] + u*golden)) unless VISITED.
 // One thread per 4 registers (one u32 store, coalesced across the warp).
@@ -500,7 +526,8 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) 
     const bool pull = !CNT && pull_ok && (s == 1 || uint64_t(nc) * 4 > r.rev.chunks);
     if (pull) {
       const uint32_t need = base + s - 1;  // source changed in sweep s-1 (or later)
-      for (uint64_t c = gwarp; c < r.fwd.chunks; c += nw) {
+      for (uint64_t k = gwarp; k < r.fwd.nbig; k += nw) {
+        const uint32_t c = r.fwd.big[k];
         const uint32_t u = r.fwd.chunk_row[c];
         const uint64_t beg = r.fwd.chunk_beg[c], end = r.fwd.chunk_beg[c + 1];
         for (uint64_t i = beg + lane; i < end; i += 32) {
@@ -560,6 +587,22 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) 
         if (__any_sync(0xffffffffu, changed) && lane == 0)
           push_row(u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
       }
+      // Small destination rows (<= kSmallRow items): item-parallel over the
+      // flattened chunks, one CAS per item on a lightly contended row.
+      for_frontier_items(r.fwd, r.fwd.small, r.fwd.nsmall, &cnt[8 + g], ws,
+                         [&](uint32_t u, uint64_t i) {
+        const uint32_t v = __ldg(r.fwd.other + i);
+        if (s > 1 && __ldcg(r.lstamp + v) < need) return;
+        SimItem A;
+        A.u = u;
+        A.mk = __ldg(r.fwd.mask + i);
+        A.b = __ldg(r.fwd.batch + i);
+        sim_data(A, srcm + uint64_t(v) * Jp, r.regs, Jp);
+        upd += __popc(A.mk);
+        ++nitems;
+        if (sim_merge(A))
+          push_row(u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
+      });
     } else {
       for_frontier_items(
           r.rev, s == 1 ? nullptr : r.q.chunks[g], nc, &cnt[8 + g], ws,
@@ -894,7 +937,8 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
       // A warp ORs the fresh bits of all in-neighbours of one target row into
       // a shared accumulator, then claims the unvisited ones with one update
       // per batch word (direction-optimising BFS, Beamer et al.).
-      for (uint64_t c = gwarp; c < r.rev.chunks; c += nw) {
+      for (uint64_t k = gwarp; k < r.rev.nbig; k += nw) {
+        const uint32_t c = r.rev.big[k];
         const uint32_t v = r.rev.chunk_row[c];
         const uint64_t beg = r.rev.chunk_beg[c], end = r.rev.chunk_beg[c + 1];
         bool any = false;
@@ -940,6 +984,26 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
           push_row(v, stamp, r.lstamp, r.fwd.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
         }
       }
+      // Small target rows: item-parallel, one atomicOr per newly reached word.
+      for_frontier_items(r.rev, r.rev.small, r.rev.nsmall, &cnt[8 + g], ws,
+                         [&](uint32_t v, uint64_t i) {
+        const uint32_t b = __ldg(r.rev.batch + i);
+        uint32_t cand =
+            __ldcg(fcur + uint64_t(__ldg(r.rev.other + i)) * W32 + b) & __ldg(r.rev.mask + i);
+        if (!cand) return;
+        uint32_t* vw = r.vis + uint64_t(v) * W32 + b;
+        cand &= ~__ldcg(vw);
+        if (!cand) return;
+        const uint32_t nb = cand & ~atomicOr(vw, cand);
+        if (!nb) return;
+        int8_t* rb = r.regs + uint64_t(v) * r.Jp + b * 32;
+        for (uint32_t t = nb; t; t &= t - 1) rb[__ffs(t) - 1] = -1;
+        atomicOr(fnxt + uint64_t(v) * W32 + b, nb);
+        marked += __popc(nb);
+        if (ld_volatile(&r.dstamp[v]) != base && atomicExch(&r.dstamp[v], base) != base)
+          r.dirty[atomicAdd(&r.ctl->dirty_count, 1u)] = v;
+        push_row(v, stamp, r.lstamp, r.fwd.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
+      });
     } else {
       for_frontier_items(r.fwd, r.q.chunks[g], nc, &cnt[8 + g], ws, visit);
     }
@@ -1080,6 +1144,14 @@ void launch_row_offsets(const DevGraph& g, int dir, const uint64_t* pos_off, Ite
 void launch_chunk_write(uint32_t n, Items& it, const uint64_t* row_chunk64, cudaStream_t s) {
   k_chunk_write<<<grid_for(uint64_t(n) + 1), kThreads, 0, s>>>(
       n, row_chunk64, it.row_off, it.row_chunk, it.chunk_row, it.chunk_beg, it.count);
+  DFS_CUDA(cudaGetLastError());
+  ++g_launches;
+}
+
+void launch_split_chunks(Items& it, unsigned int* cnt2, cudaStream_t s) {
+  if (!it.chunks) return;
+  k_split_chunks<<<grid_for(it.chunks), kThreads, 0, s>>>(it.chunks, it.chunk_row, it.row_off,
+                                                           it.small, it.big, cnt2);
   DFS_CUDA(cudaGetLastError());
   ++g_launches;
 }

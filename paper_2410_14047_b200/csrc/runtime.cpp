@@ -188,6 +188,16 @@ void Context::build_items(RankDev& r, int dir) {
   it.chunk_beg = as<uint64_t>(arena_.get(p + "chunk_beg", (it.chunks + 1) * 8));
   it.row_chunk = as<uint32_t>(arena_.get(p + "row_chunk", (size_t(n) + 1) * 4));
   launch_chunk_write(n, it, row_chunk64, stream_);
+  it.small = as<uint32_t>(arena_.get(p + "small", std::max<uint64_t>(it.chunks, 1) * 4));
+  it.big = as<uint32_t>(arena_.get(p + "big", std::max<uint64_t>(it.chunks, 1) * 4));
+  unsigned int* c2 = as<unsigned int>(arena_.get("tmp.split", 16));
+  DFS_CUDA(cudaMemsetAsync(c2, 0, 8, stream_));
+  launch_split_chunks(it, c2, stream_);
+  unsigned int hc[2];
+  DFS_CUDA(cudaMemcpyAsync(hc, c2, 8, cudaMemcpyDeviceToHost, stream_));
+  sync();
+  it.nsmall = hc[0];
+  it.nbig = hc[1];
 }
 
 void Context::reset_rank_state(RankDev& r) {
