@@ -14,6 +14,7 @@
 //  * the cascade (coverage removal) is a persistent level-synchronous bitset
 //    BFS over the forward items; the score is bit-exact via an integer sum.
 #include <cooperative_groups.h>
+#include <cooperative_groups/scan.h>
 #include <cub/cub.cuh>
 #include <cuda/std/functional>
 
@@ -287,6 +288,18 @@ __device__ __forceinline__ unsigned long long merge8(unsigned long long d, unsig
   return (static_cast<unsigned long long>(hi) << 32) | lo;
 }
 
+// Warp-aggregated append: the lanes that reach this call together reserve
+// their slots with one atomic (a same-address atomic per lane serialises at
+// the L2 slice and was the top stall of the first profiles).
+__device__ __forceinline__ unsigned agg_reserve(unsigned int* ctr, unsigned count) {
+  cg::coalesced_group grp = cg::coalesced_threads();
+  const unsigned excl = cg::exclusive_scan(grp, count);
+  unsigned base = 0;
+  const unsigned last = grp.size() - 1;
+  if (grp.thread_rank() == last) base = atomicAdd(ctr, excl + count);
+  return grp.shfl(base, last) + excl;
+}
+
 // Push of row u into the next generation (deduplicated by stamp): appends u
 // to rows[gn] and all of u's chunks to chunks[gn].
 __device__ __forceinline__ void push_row(uint32_t u, uint32_t stamp, uint32_t* lstamp,
@@ -295,13 +308,17 @@ __device__ __forceinline__ void push_row(uint32_t u, uint32_t stamp, uint32_t* l
                                          unsigned int* row_cnt) {
   if (ld_volatile(&lstamp[u]) == stamp) return;
   if (atomicExch(&lstamp[u], stamp) == stamp) return;
-  const unsigned ri = atomicAdd(row_cnt, 1u);
-  rows[ri] = u;
   const uint32_t c0 = row_chunk[u], c1 = row_chunk[u + 1];
-  if (c1 > c0) {
-    const unsigned ci = atomicAdd(chunk_cnt, c1 - c0);
-    for (uint32_t c = c0; c < c1; ++c) chunks[ci + (c - c0)] = c;
-  }
+  rows[agg_reserve(row_cnt, 1u)] = u;
+  const unsigned ci = agg_reserve(chunk_cnt, c1 - c0);
+  for (uint32_t c = c0; c < c1; ++c) chunks[ci + (c - c0)] = c;
+}
+
+__device__ __forceinline__ void push_dirty(uint32_t v, uint32_t base, uint32_t* dstamp,
+                                           uint32_t* dirty, unsigned int* dirty_count) {
+  if (ld_volatile(&dstamp[v]) == base) return;
+  if (atomicExch(&dstamp[v], base) == base) return;
+  dirty[agg_reserve(dirty_count, 1u)] = v;
 }
 
 // Per-warp staging for the flattened item distribution.
@@ -928,8 +945,7 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
       for (uint32_t t = nb; t; t &= t - 1) rb[__ffs(t) - 1] = -1;
       atomicOr(fnxt + uint64_t(v) * W32 + b, nb);
       marked += __popc(nb);
-      if (ld_volatile(&r.dstamp[v]) != base && atomicExch(&r.dstamp[v], base) != base)
-        r.dirty[atomicAdd(&r.ctl->dirty_count, 1u)] = v;
+      push_dirty(v, base, r.dstamp, r.dirty, &r.ctl->dirty_count);
       push_row(v, stamp, r.lstamp, r.fwd.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
     };
     if (pull_ok && uint64_t(nc) * 4 > r.fwd.chunks) {
@@ -979,8 +995,7 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
         }
         __syncwarp();
         if (__any_sync(0xffffffffu, got) && lane == 0) {
-          if (ld_volatile(&r.dstamp[v]) != base && atomicExch(&r.dstamp[v], base) != base)
-            r.dirty[atomicAdd(&r.ctl->dirty_count, 1u)] = v;
+          push_dirty(v, base, r.dstamp, r.dirty, &r.ctl->dirty_count);
           push_row(v, stamp, r.lstamp, r.fwd.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
         }
       }
@@ -1000,8 +1015,7 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
         for (uint32_t t = nb; t; t &= t - 1) rb[__ffs(t) - 1] = -1;
         atomicOr(fnxt + uint64_t(v) * W32 + b, nb);
         marked += __popc(nb);
-        if (ld_volatile(&r.dstamp[v]) != base && atomicExch(&r.dstamp[v], base) != base)
-          r.dirty[atomicAdd(&r.ctl->dirty_count, 1u)] = v;
+        push_dirty(v, base, r.dstamp, r.dirty, &r.ctl->dirty_count);
         push_row(v, stamp, r.lstamp, r.fwd.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
       });
     } else {
