@@ -87,6 +87,8 @@ struct RankCtl {
   // reference-schedule work counters (count mode):
   // E edges processed, B live 32-sim batches, T touched (row, batch) pairs
   unsigned long long cnt_edges, cnt_batches, cnt_touched, cnt_sweeps, cnt_convergences;
+  // solo-mode hand-back word: (launch tick << 32) | (resume sweep/level << 2) | code
+  unsigned long long release;
 };
 
 // Work queues used by the persistent simulate / cascade kernels.  Rotating

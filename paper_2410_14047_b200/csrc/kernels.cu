@@ -251,22 +251,24 @@ __global__ void k_fill(uint32_t n, uint32_t J, uint32_t Jp, const uint64_t* __re
   if (ctl && blockIdx.x == 0 && threadIdx.x == 0) ctl->dirty_count = 0;  // full rescore follows
   const uint32_t q = Jp >> 2;
   const uint32_t W32 = Jp >> 5;
-  const uint64_t total = uint64_t(n) * q;
-  for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
-       t += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t u = t / q;
-    const uint32_t j0 = uint32_t(t - u * q) * 4;
-    const uint32_t vb = vis[u * W32 + (j0 >> 5)] >> (j0 & 31);
+  // warp per row, lanes over 4-register words (coalesced u32 stores)
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t u = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; u < n; u += nw) {
     const uint64_t ug = u * kGolden;
-    uint32_t word = 0;
+    uint32_t* row = reinterpret_cast<uint32_t*>(regs + u * Jp);
+    for (uint32_t w = lane_id(); w < q; w += 32) {
+      const uint32_t j0 = w * 4;
+      const uint32_t vb = vis[u * W32 + (j0 >> 5)] >> (j0 & 31);
+      uint32_t word = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t j = j0 + k;
-      uint32_t byte = 0xFFu;
-      if (j < J && !((vb >> k) & 1u)) byte = uint32_t(__clzll(fmix64(__ldg(jkey + j) + ug)));
-      word |= byte << (8 * k);
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t j = j0 + k;
+        uint32_t byte = 0xFFu;
+        if (j < J && !((vb >> k) & 1u)) byte = uint32_t(__clzll(fmix64(__ldg(jkey + j) + ug)));
+        word |= byte << (8 * k);
+      }
+      row[w] = word;
     }
-    reinterpret_cast<uint32_t*>(regs)[t] = word;
   }
 }
 
@@ -380,6 +382,7 @@ __device__ __forceinline__ void for_frontier_items(const Items& it, const uint32
 }
 
 constexpr unsigned long long kNeg8 = 0x8080808080808080ull;  // "no contribution"
+constexpr uint32_t kSoloChunks = 64;  // frontier (chunks) a single block iterates alone
 constexpr uint32_t kPullMaxJp = 4096;  // pull accumulators live in shared memory
 
 // Shared-memory running max of the live bytes of one source word.
@@ -477,6 +480,7 @@ template <int JAC, int CNT>
 __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) {
   if (a.gate && ld_volatile(a.gate) != a.want) return;  // grid-uniform
   __shared__ WarpStage stage[kWarps];
+  __shared__ unsigned long long s_release;
   cg::grid_group grid = cg::this_grid();
   const RankDev& r = a.r;
   unsigned int* cnt = r.q.counts;
@@ -513,17 +517,15 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) 
   const int8_t* srcm = JAC ? r.snap : r.regs;
   const uint32_t Jp = r.Jp;
   unsigned long long upd = 0, nitems = 0, nedges = 0, ntouched = 0;
-  uint32_t s = 1;
-  int err = 0;
-  for (;; ++s) {
+
+  // One sweep.  solo: only block 0 participates (small frontier), barriers
+  // are block-level; otherwise the whole grid.
+  auto sweep = [&](uint32_t s, bool solo) {
     const int g = s % 3, gn = (s + 1) % 3, gr = (s + 2) % 3;
-    if (s > 1 && ld_volatile(&cnt[4 + g]) == 0) break;  // no row changed in sweep s-1
-    if (s > uint32_t(a.cap)) {
-      err = 1;
-      break;
-    }
+    const uint64_t my_warp = solo ? (threadIdx.x >> 5) : gwarp;
+    const uint64_t n_warps = solo ? kWarps : nw;
     const uint32_t nc = (s == 1) ? uint32_t(r.rev.chunks) : ld_volatile(&cnt[g]);
-    if (gwarp == 0 && lane == 0) {
+    if (my_warp == 0 && lane == 0) {
       cnt[gr] = 0;
       cnt[4 + gr] = 0;
       cnt[8 + gr] = 0;
@@ -531,19 +533,17 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) 
     const uint32_t stamp = base + s;
     uint32_t* rows_n = r.q.rows[gn];
     uint32_t* chunks_n = r.q.chunks[gn];
-    // Large frontiers (and sweep 1): flat pass over all items, rows filtered
-    // by their change stamp, two items in flight per thread.  Small ones: the
-    // chunk frontier.  Count mode keeps the exact frontier schedule.
     // Large frontiers (and sweep 1) run PULL-style over row-owned forward
     // chunks: a warp gathers the sources of one destination row chunk into a
     // shared-memory accumulator and writes each touched word once (plain store
     // when it owns the row, CAS otherwise), so out-hub rows see one update per
     // chunk instead of one contended CAS per item.  Small frontiers push.
     // Count mode keeps the exact push frontier of the reference schedule.
-    const bool pull = !CNT && pull_ok && (s == 1 || uint64_t(nc) * 4 > r.rev.chunks);
+    const bool pull =
+        !CNT && !solo && pull_ok && (s == 1 || uint64_t(nc) * 4 > r.rev.chunks);
     if (pull) {
       const uint32_t need = base + s - 1;  // source changed in sweep s-1 (or later)
-      for (uint64_t k = gwarp; k < r.fwd.nbig; k += nw) {
+      for (uint64_t k = my_warp; k < r.fwd.nbig; k += n_warps) {
         const uint32_t c = r.fwd.big[k];
         const uint32_t u = r.fwd.chunk_row[c];
         const uint64_t beg = r.fwd.chunk_beg[c], end = r.fwd.chunk_beg[c + 1];
@@ -575,12 +575,12 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) 
           if (!((touched[b >> 5] >> (b & 31)) & 1u)) continue;
 #pragma unroll
           for (int wv = 0; wv < 4; ++wv) {
-            const unsigned long long a = acc[b * 4 + wv];
-            if (a == kNeg8) continue;
+            const unsigned long long av = acc[b * 4 + wv];
+            if (av == kNeg8) continue;
             acc[b * 4 + wv] = kNeg8;
             unsigned long long* dp = drow + b * 4 + wv;
             unsigned long long d = __ldcg(dp);
-            unsigned long long nv = merge8_full(d, a);
+            unsigned long long nv = merge8_full(d, av);
             if (nv == d) continue;
             if (owner) {
               *dp = nv;
@@ -593,7 +593,7 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) 
                   break;
                 }
                 d = old;
-                nv = merge8_full(d, a);
+                nv = merge8_full(d, av);
               }
             }
           }
@@ -643,19 +643,99 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) 
                        &cnt[4 + gn]);
           });
     }
-    grid.sync();
-    if (JAC) {  // engine.cpp:81-82: re-sync snapshot rows that moved
-      const unsigned nr = ld_volatile(&cnt[4 + gn]);
-      for (uint64_t k = gwarp; k < nr; k += nw) {
-        const uint64_t row = uint64_t(rows_n[k]) * Jp;
-        const uint4* sp4 = reinterpret_cast<const uint4*>(r.regs + row);
-        uint4* dp4 = reinterpret_cast<uint4*>(r.snap + row);
-        for (uint32_t j = lane; j < Jp / 16; j += 32) dp4[j] = __ldcg(sp4 + j);
+  };
+  // engine.cpp:81-82: re-sync snapshot rows that moved (Jacobi schedule).
+  auto resync = [&](uint32_t s, bool solo) {
+    const int gn = (s + 1) % 3;
+    const unsigned nr = ld_volatile(&cnt[4 + gn]);
+    const uint64_t my_warp = solo ? (threadIdx.x >> 5) : gwarp;
+    const uint64_t n_warps = solo ? kWarps : nw;
+    for (uint64_t k = my_warp; k < nr; k += n_warps) {
+      const uint64_t row = uint64_t(__ldcg(r.q.rows[gn] + k)) * Jp;
+      const uint4* sp4 = reinterpret_cast<const uint4*>(r.regs + row);
+      uint4* dp4 = reinterpret_cast<uint4*>(r.snap + row);
+      for (uint32_t j = lane; j < Jp / 16; j += 32) dp4[j] = __ldcg(sp4 + j);
+    }
+    if (CNT) {
+      const uint64_t t0 = solo ? threadIdx.x : gtid, ts = solo ? blockDim.x : gthreads;
+      for (uint64_t i = t0; i < tb_words; i += ts) r.tbits[i] = 0;
+    }
+  };
+
+  uint32_t s = 1;
+  int err = 0;
+  for (;;) {
+    const int g = s % 3;
+    if (s > 1 && ld_volatile(&cnt[4 + g]) == 0) break;  // no row changed in sweep s-1
+    if (s > uint32_t(a.cap)) {
+      err = 1;
+      break;
+    }
+    if (s > 1 && ld_volatile(&cnt[g]) <= kSoloChunks) {
+      // Small frontier: block 0 iterates alone with block barriers; the rest
+      // of the grid parks until it hands back (grid barriers cost more than
+      // the work of a tail sweep).
+      if (blockIdx.x == 0) {
+        uint32_t code = 0;  // 0 resume grid mode at s, 1 converged, 2 cap exceeded
+        for (;;) {
+          const int gg = s % 3;
+          if (ld_volatile(&cnt[4 + gg]) == 0) {
+            code = 1;
+            break;
+          }
+          if (s > uint32_t(a.cap)) {
+            code = 2;
+            break;
+          }
+          if (ld_volatile(&cnt[gg]) > 4 * kSoloChunks) break;
+          sweep(s, true);
+          __syncthreads();
+          if (JAC) {
+            resync(s, true);
+            __syncthreads();
+          }
+          ++s;
+        }
+        if (threadIdx.x == 0) {
+          __threadfence();
+          atomicExch(&r.ctl->release,
+                     (static_cast<unsigned long long>(base) << 32) | (uint64_t(s) << 2) | code);
+        }
+        __syncthreads();
+        if (code == 1) break;
+        if (code == 2) {
+          err = 1;
+          break;
+        }
+      } else {
+        if (threadIdx.x == 0) {
+          unsigned long long rv;
+          for (;;) {
+            rv = ld_volatile(&r.ctl->release);
+            if ((rv >> 32) == base && uint32_t((rv >> 2) & 0x3FFFFFFFu) > s) break;
+            __nanosleep(256);
+          }
+          __threadfence();
+          s_release = rv;
+        }
+        __syncthreads();
+        const unsigned long long rv = s_release;
+        s = uint32_t((rv >> 2) & 0x3FFFFFFFu);
+        if ((rv & 3) == 1) break;
+        if ((rv & 3) == 2) {
+          err = 1;
+          break;
+        }
       }
-      if (CNT)
-        for (uint64_t i = gtid; i < tb_words; i += gthreads) r.tbits[i] = 0;
+      continue;
+    }
+    sweep(s, false);
+    grid.sync();
+    if (JAC) {
+      resync(s, false);
       grid.sync();
     }
+    ++s;
   }
   // Instrumentation: one atomic per warp.
   for (int o = 16; o; o >>= 1) {
@@ -860,6 +940,7 @@ __device__ __forceinline__ void clear_rows(uint32_t* f, const uint32_t* rows, un
 // clears the rows of level L-1 in fresh[(L+2)%3]; queues rotate mod 4.
 __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
   __shared__ WarpStage stage[kWarps];
+  __shared__ unsigned long long s_release;
   cg::grid_group grid = cg::this_grid();
   const RankDev& r = a.r;
   unsigned int* cnt = r.q.counts;
@@ -908,26 +989,22 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
       push_row(s, base + 1, r.lstamp, r.fwd.row_chunk, r.q.rows[1], r.q.chunks[1], &cnt[1],
                &cnt[5]);
   }
-  grid.sync();
 
-  uint32_t L = 1;
-  for (;; ++L) {
+  // One BFS level.  solo: only block 0 (small frontier, block barriers).
+  auto level = [&](uint32_t L, bool solo) {
     const int g = L % 4, gn = (L + 1) % 4, gr = (L + 2) % 4, gp = (L + 3) % 4;
-    uint32_t* fcur = r.fresh[L % 3];
+    const uint64_t my_warp = solo ? (threadIdx.x >> 5) : gwarp;
+    const uint64_t n_warps = solo ? kWarps : nw;
+    const uint32_t* fcur = r.fresh[L % 3];
     uint32_t* fnxt = r.fresh[(L + 1) % 3];
     uint32_t* fprev = r.fresh[(L + 2) % 3];
     const uint32_t nc = ld_volatile(&cnt[g]);
-    if (nc == 0) {  // done: clear what the last two levels left behind
-      clear_rows(fcur, r.q.rows[g], ld_volatile(&cnt[4 + g]), W32, gwarp, nw, lane);
-      clear_rows(fprev, r.q.rows[gp], ld_volatile(&cnt[4 + gp]), W32, gwarp, nw, lane);
-      break;
-    }
-    if (gwarp == 0 && lane == 0) {
+    if (my_warp == 0 && lane == 0) {
       cnt[gr] = 0;
       cnt[4 + gr] = 0;
       cnt[8 + gr] = 0;
     }
-    clear_rows(fprev, r.q.rows[gp], ld_volatile(&cnt[4 + gp]), W32, gwarp, nw, lane);
+    clear_rows(fprev, r.q.rows[gp], ld_volatile(&cnt[4 + gp]), W32, my_warp, n_warps, lane);
     const uint32_t stamp = base + L + 1;
     uint32_t* rows_n = r.q.rows[gn];
     uint32_t* chunks_n = r.q.chunks[gn];
@@ -948,12 +1025,12 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
       push_dirty(v, base, r.dstamp, r.dirty, &r.ctl->dirty_count);
       push_row(v, stamp, r.lstamp, r.fwd.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
     };
-    if (pull_ok && uint64_t(nc) * 4 > r.fwd.chunks) {
+    if (!solo && pull_ok && uint64_t(nc) * 4 > r.fwd.chunks) {
       // Large frontier: bottom-up (pull) level over row-owned reverse chunks.
       // A warp ORs the fresh bits of all in-neighbours of one target row into
       // a shared accumulator, then claims the unvisited ones with one update
       // per batch word (direction-optimising BFS, Beamer et al.).
-      for (uint64_t k = gwarp; k < r.rev.nbig; k += nw) {
+      for (uint64_t k = my_warp; k < r.rev.nbig; k += n_warps) {
         const uint32_t c = r.rev.big[k];
         const uint32_t v = r.rev.chunk_row[c];
         const uint64_t beg = r.rev.chunk_beg[c], end = r.rev.chunk_beg[c + 1];
@@ -1021,7 +1098,67 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
     } else {
       for_frontier_items(r.fwd, r.q.chunks[g], nc, &cnt[8 + g], ws, visit);
     }
-    grid.sync();
+  };
+  // Final clean-up: fresh bits left by the last two levels.
+  auto finish = [&](uint32_t L, bool solo) {
+    const int g = L % 4, gp = (L + 3) % 4;
+    const uint64_t my_warp = solo ? (threadIdx.x >> 5) : gwarp;
+    const uint64_t n_warps = solo ? kWarps : nw;
+    clear_rows(r.fresh[L % 3], r.q.rows[g], ld_volatile(&cnt[4 + g]), W32, my_warp, n_warps, lane);
+    clear_rows(r.fresh[(L + 2) % 3], r.q.rows[gp], ld_volatile(&cnt[4 + gp]), W32, my_warp,
+               n_warps, lane);
+  };
+
+  // Episodes: block 0 iterates small-frontier levels alone (the rest of the
+  // grid parks on a release word); large frontiers run grid-wide with one
+  // grid barrier per level.  Episode 0 starts right after the commit, so a
+  // tiny cascade never touches a grid barrier.
+  uint32_t L = 1, e = 0;
+  for (;;) {
+    uint32_t code = 0;
+    if (blockIdx.x == 0) {
+      __syncthreads();
+      for (;;) {
+        const uint32_t nc = ld_volatile(&cnt[L % 4]);
+        if (nc == 0) {
+          finish(L, true);
+          code = 1;
+          break;
+        }
+        if (nc > kSoloChunks) break;
+        level(L, true);
+        __syncthreads();
+        ++L;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicExch(&r.ctl->release, (static_cast<unsigned long long>(base) << 32) |
+                                        (uint64_t(e & 0xFFFu) << 20) | (uint64_t(L) << 2) | code);
+      }
+    } else {
+      if (threadIdx.x == 0) {
+        unsigned long long rv;
+        for (;;) {
+          rv = ld_volatile(&r.ctl->release);
+          if ((rv >> 32) == base && ((rv >> 20) & 0xFFFu) == (e & 0xFFFu)) break;
+          __nanosleep(256);
+        }
+        __threadfence();
+        s_release = rv;
+      }
+      __syncthreads();
+      L = uint32_t((s_release >> 2) & 0x3FFFFu);
+      code = uint32_t(s_release & 3u);
+    }
+    ++e;
+    if (code == 1) break;
+    for (;;) {  // grid-wide levels while the frontier is large
+      if (ld_volatile(&cnt[L % 4]) <= kSoloChunks) break;
+      level(L, false);
+      grid.sync();
+      ++L;
+    }
   }
   for (int o = 16; o; o >>= 1) marked += __shfl_xor_sync(0xffffffffu, marked, o);
   if (lane == 0 && marked) atomicAdd(&r.ctl->visited, marked);
@@ -1171,8 +1308,8 @@ void launch_split_chunks(Items& it, unsigned int* cnt2, cudaStream_t s) {
 }
 
 void launch_fill(const RankDev& r, const unsigned int* gate, unsigned int want, cudaStream_t s) {
-  const uint64_t total = uint64_t(r.n) * (r.Jp / 4);
-  if (!total) return;
+  const uint64_t total = uint64_t(r.n) * 32;
+  if (!r.n) return;
   k_fill<<<grid_for(total), kThreads, 0, s>>>(r.n, r.J, r.Jp, r.jkey, r.vis, r.regs, gate, want,
                                               r.ctl);
   DFS_CUDA(cudaGetLastError());
