@@ -9,7 +9,8 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libdifuser_b200.so")
+LIB_PATH = os.environ.get("DFS_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib",
+                                                     "libdifuser_b200.so")
 
 # Exported symbols (kept in sync with include/difuser_b200.h; checked by tests).
 SYMBOLS = [

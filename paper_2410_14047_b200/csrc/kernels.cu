@@ -334,7 +334,8 @@ struct WarpStage {
 // claims 32 frontier slots, the items of those chunks are flattened (warp
 // prefix sum of their sizes) and dealt to lanes 32 at a time, so lanes stay
 // busy even when most rows have only a handful of items (R-MAT tails) and
-// hub rows are spread over many warps.  f(row, item_index) per item.
+// hub rows are spread over many warps.  f(row_a, item_a, ok_a, row_b, item_b,
+// ok_b) per pair of items (two independent load chains in flight per lane).
 template <class F>
 __device__ __forceinline__ void for_frontier_items(const Items& it, const uint32_t* frontier,
                                                    uint32_t nc, unsigned int* work_ctr,
@@ -365,17 +366,31 @@ __device__ __forceinline__ void for_frontier_items(const Items& it, const uint32
     ws.row[lane] = row;
     ws.beg[lane] = beg;
     __syncwarp();
-    for (uint32_t t0 = 0; t0 < total; t0 += 32) {
-      const uint32_t t = t0 + lane;
-      if (t < total) {
+    // two items per lane per step (independent load chains in flight)
+    for (uint32_t t0 = 0; t0 < total; t0 += 64) {
+      const uint32_t ta = t0 + lane, tb = t0 + 32 + lane;
+      uint32_t rowa = 0, rowb = 0;
+      uint64_t ia = 0, ib = 0;
+      const bool oka = ta < total, okb = tb < total;
+      if (oka) {
         uint32_t lo = 0, hi = 31;
         while (lo < hi) {
           const uint32_t mid = (lo + hi) >> 1;
-          if (ws.incl[mid] > t) hi = mid; else lo = mid + 1;
+          if (ws.incl[mid] > ta) hi = mid; else lo = mid + 1;
         }
-        const uint32_t excl = lo ? ws.incl[lo - 1] : 0;
-        f(ws.row[lo], ws.beg[lo] + (t - excl));
+        rowa = ws.row[lo];
+        ia = ws.beg[lo] + (ta - (lo ? ws.incl[lo - 1] : 0));
       }
+      if (okb) {
+        uint32_t lo = 0, hi = 31;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (ws.incl[mid] > tb) hi = mid; else lo = mid + 1;
+        }
+        rowb = ws.row[lo];
+        ib = ws.beg[lo] + (tb - (lo ? ws.incl[lo - 1] : 0));
+      }
+      f(rowa, ia, oka, rowb, ib, okb);
     }
     __syncwarp();
   }
@@ -459,11 +474,59 @@ __device__ __forceinline__ bool sim_merge(SimItem& it) {
   return changed;
 }
 
+// Byte-max CAS loop on one destination word (engine.cpp:22-53 semantics).
+__device__ __forceinline__ bool cas_merge(unsigned long long* dp, unsigned long long d,
+                                          unsigned long long sv, uint32_t m8) {
+  unsigned long long nv = merge8(d, sv, m8);
+  while (nv != d) {
+    const unsigned long long old = atomicCAS(dp, d, nv);
+    if (old == d) return true;
+    d = old;
+    nv = merge8(d, sv, m8);
+  }
+  return false;
+}
+
+// Two items: the first live 8-sim word of each is loaded together (thin IC
+// windows rarely have more), remaining words follow one by one.
+__device__ __forceinline__ void sim_pair(uint32_t ua, uint32_t mka, uint32_t bba, bool pa,
+                                         const int8_t* sa, uint32_t ub, uint32_t mkb, uint32_t bbb,
+                                         bool pb, const int8_t* sb, int8_t* regs, uint32_t Jp,
+                                         bool& ca, bool& cb) {
+  const int wa = pa ? (__ffs(mka) - 1) >> 3 : 0, wb = pb ? (__ffs(mkb) - 1) >> 3 : 0;
+  const unsigned long long* spa = reinterpret_cast<const unsigned long long*>(sa + bba * 32);
+  const unsigned long long* spb = reinterpret_cast<const unsigned long long*>(sb + bbb * 32);
+  unsigned long long* dpa = reinterpret_cast<unsigned long long*>(regs + uint64_t(ua) * Jp + bba * 32);
+  unsigned long long* dpb = reinterpret_cast<unsigned long long*>(regs + uint64_t(ub) * Jp + bbb * 32);
+  unsigned long long s0 = 0, d0 = 0, s1 = 0, d1 = 0;
+  if (pa) {
+    s0 = __ldcg(spa + wa);
+    d0 = __ldcg(dpa + wa);
+  }
+  if (pb) {
+    s1 = __ldcg(spb + wb);
+    d1 = __ldcg(dpb + wb);
+  }
+  ca = pa && cas_merge(dpa + wa, d0, s0, (mka >> (8 * wa)) & 0xFFu);
+  cb = pb && cas_merge(dpb + wb, d1, s1, (mkb >> (8 * wb)) & 0xFFu);
+  if (pa)
+    for (int w = wa + 1; w < 4; ++w) {
+      const uint32_t m8 = (mka >> (8 * w)) & 0xFFu;
+      if (m8) ca |= cas_merge(dpa + w, __ldcg(dpa + w), __ldcg(spa + w), m8);
+    }
+  if (pb)
+    for (int w = wb + 1; w < 4; ++w) {
+      const uint32_t m8 = (mkb >> (8 * w)) & 0xFFu;
+      if (m8) cb |= cas_merge(dpb + w, __ldcg(dpb + w), __ldcg(spb + w), m8);
+    }
+}
+
 struct SimArgs {
   RankDev r;
   int cap;
   const unsigned int* gate;
   unsigned int want;
+  int dbg;  // experiments only (DFS_DBG): bit0 skip big-row pull, bit1 skip small rows
 };
 
 // Persistent simulate-to-convergence (engine.cpp:57-96 semantics).  Sweep s
@@ -533,6 +596,8 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) 
     const uint32_t stamp = base + s;
     uint32_t* rows_n = r.q.rows[gn];
     uint32_t* chunks_n = r.q.chunks[gn];
+    if ((a.dbg & 4) && blockIdx.x == 0 && threadIdx.x == 0)
+      printf("simulate s=%u nc=%u solo=%d t=%lld\n", s, nc, int(solo), (long long)clock64());
     // Large frontiers (and sweep 1) run PULL-style over row-owned forward
     // chunks: a warp gathers the sources of one destination row chunk into a
     // shared-memory accumulator and writes each touched word once (plain store
@@ -543,7 +608,7 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) 
         !CNT && !solo && pull_ok && (s == 1 || uint64_t(nc) * 4 > r.rev.chunks);
     if (pull) {
       const uint32_t need = base + s - 1;  // source changed in sweep s-1 (or later)
-      for (uint64_t k = my_warp; k < r.fwd.nbig; k += n_warps) {
+      for (uint64_t k = my_warp; k < ((a.dbg & 1) ? 0 : r.fwd.nbig); k += n_warps) {
         const uint32_t c = r.fwd.big[k];
         const uint32_t u = r.fwd.chunk_row[c];
         const uint64_t beg = r.fwd.chunk_beg[c], end = r.fwd.chunk_beg[c + 1];
@@ -606,40 +671,82 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) 
       }
       // Small destination rows (<= kSmallRow items): item-parallel over the
       // flattened chunks, one CAS per item on a lightly contended row.
-      for_frontier_items(r.fwd, r.fwd.small, r.fwd.nsmall, &cnt[8 + g], ws,
-                         [&](uint32_t u, uint64_t i) {
-        const uint32_t v = __ldg(r.fwd.other + i);
-        if (s > 1 && __ldcg(r.lstamp + v) < need) return;
-        SimItem A;
-        A.u = u;
-        A.mk = __ldg(r.fwd.mask + i);
-        A.b = __ldg(r.fwd.batch + i);
-        sim_data(A, srcm + uint64_t(v) * Jp, r.regs, Jp);
-        upd += __popc(A.mk);
-        ++nitems;
-        if (sim_merge(A))
-          push_row(u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
+      for_frontier_items(r.fwd, r.fwd.small, (a.dbg & 2) ? 0 : r.fwd.nsmall, &cnt[8 + g], ws,
+                         [&](uint32_t ua, uint64_t ia, bool pa, uint32_t ub, uint64_t ib, bool pb) {
+        const uint32_t va = pa ? __ldg(r.fwd.other + ia) : 0;
+        const uint32_t vb = pb ? __ldg(r.fwd.other + ib) : 0;
+        SimItem A, B;
+        if (pa) {
+          A.u = ua;
+          A.mk = __ldg(r.fwd.mask + ia);
+          A.b = __ldg(r.fwd.batch + ia);
+        }
+        if (pb) {
+          B.u = ub;
+          B.mk = __ldg(r.fwd.mask + ib);
+          B.b = __ldg(r.fwd.batch + ib);
+        }
+        if (s > 1) {
+          const uint32_t sta = pa ? __ldcg(r.lstamp + va) : 0;
+          const uint32_t stb = pb ? __ldcg(r.lstamp + vb) : 0;
+          pa = pa && sta >= need;
+          pb = pb && stb >= need;
+        }
+        bool ca, cb;
+        sim_pair(ua, A.mk, A.b, pa, srcm + uint64_t(va) * Jp, ub, B.mk, B.b, pb,
+                 srcm + uint64_t(vb) * Jp, r.regs, Jp, ca, cb);
+        if (pa) {
+          upd += __popc(A.mk);
+          ++nitems;
+        }
+        if (pb) {
+          upd += __popc(B.mk);
+          ++nitems;
+        }
+        if (ca)
+          push_row(ua, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
+        if (cb)
+          push_row(ub, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
       });
     } else {
       for_frontier_items(
           r.rev, s == 1 ? nullptr : r.q.chunks[g], nc, &cnt[8 + g], ws,
-          [&](uint32_t v, uint64_t i) {
-            SimItem A;
-            sim_fields(A, r.rev, i);
-            sim_data(A, srcm + uint64_t(v) * Jp, r.regs, Jp);
-            const bool changed = sim_merge(A);
-            upd += __popc(A.mk);
-            ++nitems;
-            if (CNT) {
-              // E: first item of its edge (items of one edge are consecutive, same u)
-              if (i == r.rev.row_off[v] || r.rev.other[i - 1] != A.u) ++nedges;
-              // T: distinct (u, b) touched in this sweep
-              const uint64_t bit = uint64_t(A.u) * r.W32 + A.b;
-              const uint32_t m1 = 1u << (bit & 31);
-              if (!(atomicOr(&r.tbits[bit >> 5], m1) & m1)) ++ntouched;
+          [&](uint32_t va, uint64_t ia, bool pa, uint32_t vb, uint64_t ib, bool pb) {
+            SimItem A, B;
+            if (pa) sim_fields(A, r.rev, ia);
+            if (pb) sim_fields(B, r.rev, ib);
+            bool ca, cb;
+            sim_pair(A.u, A.mk, A.b, pa, srcm + uint64_t(va) * Jp, B.u, B.mk, B.b, pb,
+                     srcm + uint64_t(vb) * Jp, r.regs, Jp, ca, cb);
+            if (pa) {
+              upd += __popc(A.mk);
+              ++nitems;
             }
-            if (changed)
+            if (pb) {
+              upd += __popc(B.mk);
+              ++nitems;
+            }
+            if (CNT) {
+#pragma unroll
+              for (int q = 0; q < 2; ++q) {
+                const bool p = q ? pb : pa;
+                if (!p) continue;
+                const uint64_t i = q ? ib : ia;
+                const uint32_t v = q ? vb : va;
+                const SimItem& X = q ? B : A;
+                // E: first item of its edge (items of one edge are consecutive, same u)
+                if (i == r.rev.row_off[v] || r.rev.other[i - 1] != X.u) ++nedges;
+                // T: distinct (u, b) touched in this sweep
+                const uint64_t bit = uint64_t(X.u) * r.W32 + X.b;
+                const uint32_t m1 = 1u << (bit & 31);
+                if (!(atomicOr(&r.tbits[bit >> 5], m1) & m1)) ++ntouched;
+              }
+            }
+            if (ca)
               push_row(A.u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &cnt[gn],
+                       &cnt[4 + gn]);
+            if (cb)
+              push_row(B.u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &cnt[gn],
                        &cnt[4 + gn]);
           });
     }
@@ -921,6 +1028,7 @@ struct CasArgs {
   RankDev r;
   const unsigned int* choice;
   uint32_t seed;
+  int dbg;  // experiments only (DFS_DBG bit 2): per-level trace
 };
 
 // Clear the fresh bits of the rows listed in one generation.
@@ -1005,17 +1113,16 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
       cnt[8 + gr] = 0;
     }
     clear_rows(fprev, r.q.rows[gp], ld_volatile(&cnt[4 + gp]), W32, my_warp, n_warps, lane);
+    if ((a.dbg & 4) && blockIdx.x == 0 && threadIdx.x == 0)
+      printf("cascade L=%u nc=%u rows=%u solo=%d pull=%d t=%lld\n", L, nc, ld_volatile(&cnt[4 + g]),
+             int(solo), int(!solo && pull_ok && uint64_t(nc) * 4 > r.fwd.chunks),
+             (long long)clock64());
     const uint32_t stamp = base + L + 1;
     uint32_t* rows_n = r.q.rows[gn];
     uint32_t* chunks_n = r.q.chunks[gn];
-    auto visit = [&](uint32_t u, uint64_t i) {
-      const uint32_t b = __ldg(r.fwd.batch + i);
-      uint32_t cand = __ldcg(fcur + uint64_t(u) * W32 + b) & __ldg(r.fwd.mask + i);
-      if (!cand) return;
-      const uint32_t v = __ldg(r.fwd.other + i);
+    // Claim newly reached registers of target row v in batch b.
+    auto claim = [&](uint32_t v, uint32_t b, uint32_t cand) {
       uint32_t* vw = r.vis + uint64_t(v) * W32 + b;
-      cand &= ~__ldcg(vw);
-      if (!cand) return;
       const uint32_t nb = cand & ~atomicOr(vw, cand);
       if (!nb) return;
       int8_t* rb = r.regs + uint64_t(v) * r.Jp + b * 32;
@@ -1024,6 +1131,20 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
       marked += __popc(nb);
       push_dirty(v, base, r.dstamp, r.dirty, &r.ctl->dirty_count);
       push_row(v, stamp, r.lstamp, r.fwd.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
+    };
+    // Top-down pair: frontier row u -> targets of two forward items.
+    auto visit = [&](uint32_t ua, uint64_t ia, bool pa, uint32_t ub, uint64_t ib, bool pb) {
+      const uint32_t ba = pa ? __ldg(r.fwd.batch + ia) : 0, bb = pb ? __ldg(r.fwd.batch + ib) : 0;
+      const uint32_t ma = pa ? __ldg(r.fwd.mask + ia) : 0, mb = pb ? __ldg(r.fwd.mask + ib) : 0;
+      const uint32_t va = pa ? __ldg(r.fwd.other + ia) : 0, vb = pb ? __ldg(r.fwd.other + ib) : 0;
+      uint32_t ca = pa ? __ldcg(fcur + uint64_t(ua) * W32 + ba) & ma : 0;
+      uint32_t cb = pb ? __ldcg(fcur + uint64_t(ub) * W32 + bb) & mb : 0;
+      const uint32_t xa = ca ? __ldcg(r.vis + uint64_t(va) * W32 + ba) : 0;
+      const uint32_t xb = cb ? __ldcg(r.vis + uint64_t(vb) * W32 + bb) : 0;
+      ca &= ~xa;
+      cb &= ~xb;
+      if (ca) claim(va, ba, ca);
+      if (cb) claim(vb, bb, cb);
     };
     if (!solo && pull_ok && uint64_t(nc) * 4 > r.fwd.chunks) {
       // Large frontier: bottom-up (pull) level over row-owned reverse chunks.
@@ -1078,22 +1199,18 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
       }
       // Small target rows: item-parallel, one atomicOr per newly reached word.
       for_frontier_items(r.rev, r.rev.small, r.rev.nsmall, &cnt[8 + g], ws,
-                         [&](uint32_t v, uint64_t i) {
-        const uint32_t b = __ldg(r.rev.batch + i);
-        uint32_t cand =
-            __ldcg(fcur + uint64_t(__ldg(r.rev.other + i)) * W32 + b) & __ldg(r.rev.mask + i);
-        if (!cand) return;
-        uint32_t* vw = r.vis + uint64_t(v) * W32 + b;
-        cand &= ~__ldcg(vw);
-        if (!cand) return;
-        const uint32_t nb = cand & ~atomicOr(vw, cand);
-        if (!nb) return;
-        int8_t* rb = r.regs + uint64_t(v) * r.Jp + b * 32;
-        for (uint32_t t = nb; t; t &= t - 1) rb[__ffs(t) - 1] = -1;
-        atomicOr(fnxt + uint64_t(v) * W32 + b, nb);
-        marked += __popc(nb);
-        push_dirty(v, base, r.dstamp, r.dirty, &r.ctl->dirty_count);
-        push_row(v, stamp, r.lstamp, r.fwd.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
+                         [&](uint32_t va, uint64_t ia, bool pa, uint32_t vb, uint64_t ib, bool pb) {
+        const uint32_t ba = pa ? __ldg(r.rev.batch + ia) : 0, bb = pb ? __ldg(r.rev.batch + ib) : 0;
+        const uint32_t ma = pa ? __ldg(r.rev.mask + ia) : 0, mb = pb ? __ldg(r.rev.mask + ib) : 0;
+        const uint32_t ua = pa ? __ldg(r.rev.other + ia) : 0, ub = pb ? __ldg(r.rev.other + ib) : 0;
+        uint32_t ca = pa ? __ldcg(fcur + uint64_t(ua) * W32 + ba) & ma : 0;
+        uint32_t cb = pb ? __ldcg(fcur + uint64_t(ub) * W32 + bb) & mb : 0;
+        const uint32_t xa = ca ? __ldcg(r.vis + uint64_t(va) * W32 + ba) : 0;
+        const uint32_t xb = cb ? __ldcg(r.vis + uint64_t(vb) * W32 + bb) : 0;
+        ca &= ~xa;
+        cb &= ~xb;
+        if (ca) claim(va, ba, ca);
+        if (cb) claim(vb, bb, cb);
       });
     } else {
       for_frontier_items(r.fwd, r.q.chunks[g], nc, &cnt[8 + g], ws, visit);
@@ -1352,7 +1469,8 @@ int coop_grid(int which, int variant) {
 
 void launch_simulate(const RankDev& r, int jacobi, int count, int cap, const unsigned int* gate,
                      unsigned int want, cudaStream_t s) {
-  SimArgs a{r, cap, gate, want};
+  static const int dbg = getenv("DFS_DBG") ? atoi(getenv("DFS_DBG")) : 0;
+  SimArgs a{r, cap, gate, want, dbg};
   void* args[] = {&a};
   const int variant = jacobi ? (count ? 2 : 1) : 0;
   DFS_CUDA(cudaLaunchCooperativeKernel(sim_kernel(variant), dim3(coop_grid(0, variant)),
@@ -1386,7 +1504,8 @@ void launch_argmax(const double* scores, RunArrays& ra, uint32_t n, cudaStream_t
 }
 
 void launch_cascade(const RankDev& r, const unsigned int* choice, uint32_t seed, cudaStream_t s) {
-  CasArgs a{r, choice, seed};
+  static const int dbg = getenv("DFS_DBG") ? atoi(getenv("DFS_DBG")) : 0;
+  CasArgs a{r, choice, seed, dbg};
   void* args[] = {&a};
   DFS_CUDA(cudaLaunchCooperativeKernel((void*)k_cascade, dim3(coop_grid(1)), dim3(kThreads), args,
                                        kCasSmem, s));
