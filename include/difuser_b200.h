@@ -124,6 +124,17 @@ int dfs_last_stats(const dfs_ctx *ctx, dfs_stats *out);
  * dfs_prepare = make_plan + apply_weights + build_device_graph for all tau. */
 int dfs_prepare(dfs_ctx *ctx, const dfs_graph *g, const dfs_config *cfg);
 int dfs_plan(const dfs_ctx *ctx, uint32_t *x_sorted, uint32_t *order, int *degraded);
+/* One FASST partition per process (multi-GPU): this context builds only
+ * partition `rank` of `world` (= cfg->devices); stage calls then use tau 0.
+ * g == NULL reuses the resident graph (dfs_upload) instead of uploading.
+ * Replaces the per-thread worker setup of proj/src/runtime.cpp:64-82. */
+int dfs_prepare_partition(dfs_ctx *ctx, const dfs_graph *g, const dfs_config *cfg, uint32_t rank,
+                          uint32_t world);
+/* Row scores into a DEVICE buffer of n doubles (full = all rows, else the rows
+ * dirtied by the last cascade) — the send buffer of the score exchange. */
+int dfs_scores_device(dfs_ctx *ctx, uint32_t tau, int full, void *dst_device);
+/* Rebuild: fill + simulate + full rescore (runtime.cpp:139-153). */
+int dfs_rebuild(dfs_ctx *ctx, uint32_t tau);
 int dfs_device_graph_size(dfs_ctx *ctx, uint32_t tau, uint64_t *m_tau, uint32_t *words);
 int dfs_device_graph(dfs_ctx *ctx, uint32_t tau, uint64_t *offsets, uint32_t *adj,
                      uint64_t *mask);
@@ -137,6 +148,28 @@ int dfs_get_registers(dfs_ctx *ctx, uint32_t tau, int8_t *out_nJ);
 int dfs_set_registers(dfs_ctx *ctx, uint32_t tau, const int8_t *in_nJ);
 /* {updates, items, edges, batches, touched, sweeps, convergences, visited} */
 int dfs_rank_counters(dfs_ctx *ctx, uint32_t tau, uint64_t out[8]);
+
+/* ---- report formatting (report.cpp:9-41) for drivers that assemble the
+ * greedy loop themselves (multi-process path): same nlohmann dump(2) output. */
+typedef struct dfs_report_fields {
+  uint32_t k, r, devices;
+  const char *mode;
+  const char *weights;
+  double rebuild_eps;
+  uint64_t seed;
+  uint64_t n, m;
+  uint32_t steps; /* entries in seeds / seeds_dense / traj */
+  const uint64_t *seeds;
+  const uint32_t *seeds_dense;
+  const double *traj;
+  uint32_t rebuilds;
+  const uint32_t *rebuild_rounds;
+  int32_t saturated, degraded;
+  uint64_t reduced_elements, broadcast_elements, barriers;
+  int32_t with_timings;
+  double t_build, t_fill, t_simulate, t_select, t_cascade, t_total;
+} dfs_report_fields;
+int dfs_format_report(const dfs_report_fields *f, char **json_out);
 
 /* ---- verification oracles (oracle.cpp; host, not the hot path) ----------- */
 int dfs_influence(const dfs_graph *g, const uint32_t *seeds, uint32_t nseeds, uint32_t trials,

@@ -17,7 +17,7 @@ import numpy as np
 from . import _capi
 from ._capi import Config, Stats, check, lib
 
-__all__ = [
+__all__ = ["_config", 
     "Graph", "edge_hash", "graph_from_text", "greedy_exact", "influence", "is_sampled",
     "load_graph", "random_value_at", "run", "run_json", "save_cache", "generate", "Context",
 ]

@@ -22,7 +22,8 @@ SYMBOLS = [
     "dfs_last_stats", "dfs_prepare", "dfs_plan", "dfs_device_graph_size", "dfs_device_graph",
     "dfs_fill", "dfs_simulate", "dfs_scores", "dfs_commit_cascade", "dfs_visited_count",
     "dfs_get_registers", "dfs_set_registers", "dfs_influence", "dfs_greedy_exact",
-    "dfs_ctx_stream", "dfs_graph_pin", "dfs_rank_counters",
+    "dfs_ctx_stream", "dfs_graph_pin", "dfs_rank_counters", "dfs_prepare_partition",
+    "dfs_scores_device", "dfs_rebuild", "dfs_format_report",
 ]
 
 
@@ -42,6 +43,19 @@ class Stats(C.Structure):
                                           "cnt_convergences", "launches")] + \
                [("sim_active", C.c_double), ("sim_launches", C.c_uint32), ("n", C.c_uint32),
                 ("m", C.c_uint64)]
+
+
+class ReportFields(C.Structure):
+    _fields_ = [("k", C.c_uint32), ("r", C.c_uint32), ("devices", C.c_uint32),
+                ("mode", C.c_char_p), ("weights", C.c_char_p), ("rebuild_eps", C.c_double),
+                ("seed", C.c_uint64), ("n", C.c_uint64), ("m", C.c_uint64), ("steps", C.c_uint32),
+                ("seeds", C.c_void_p), ("seeds_dense", C.c_void_p), ("traj", C.c_void_p),
+                ("rebuilds", C.c_uint32), ("rebuild_rounds", C.c_void_p),
+                ("saturated", C.c_int32), ("degraded", C.c_int32),
+                ("reduced_elements", C.c_uint64), ("broadcast_elements", C.c_uint64),
+                ("barriers", C.c_uint64), ("with_timings", C.c_int32)] + \
+               [(f, C.c_double) for f in ("t_build", "t_fill", "t_simulate", "t_select",
+                                          "t_cascade", "t_total")]
 
 
 class DfsError(RuntimeError):
@@ -102,6 +116,10 @@ def lib():
         "dfs_ctx_stream": (i32, [vp, pp]),
         "dfs_graph_pin": (i32, [vp]),
         "dfs_rank_counters": (i32, [vp, u32, vp]),
+        "dfs_prepare_partition": (i32, [vp, vp, C.POINTER(Config), u32, u32]),
+        "dfs_scores_device": (i32, [vp, u32, i32, vp]),
+        "dfs_rebuild": (i32, [vp, u32]),
+        "dfs_format_report": (i32, [C.POINTER(ReportFields), C.POINTER(C.c_void_p)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

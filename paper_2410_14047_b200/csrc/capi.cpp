@@ -284,6 +284,27 @@ int dfs_prepare(dfs_ctx* ctx, const dfs_graph* g, const dfs_config* cfg) {
     ctx->c->prepare(rc, &g->g);
   });
 }
+int dfs_prepare_partition(dfs_ctx* ctx, const dfs_graph* g, const dfs_config* cfg,
+                          uint32_t rank, uint32_t world) {
+  return guard([&] {
+    need(ctx, "ctx");
+    dfs::RunConfig rc = to_config(cfg);
+    if (g) ctx->c->upload(g->g);  // g == NULL: use the resident graph
+    ctx->c->prepare(rc, g ? &g->g : nullptr, rank, world);
+  });
+}
+int dfs_scores_device(dfs_ctx* ctx, uint32_t tau, int full, void* dst) {
+  return guard([&] {
+    need(ctx, "ctx");
+    ctx->c->stage_scores_device(tau, full, static_cast<double*>(dst));
+  });
+}
+int dfs_rebuild(dfs_ctx* ctx, uint32_t tau) {
+  return guard([&] {
+    need(ctx, "ctx");
+    ctx->c->stage_rebuild(tau);
+  });
+}
 int dfs_plan(const dfs_ctx* ctx, uint32_t* x_sorted, uint32_t* order, int* degraded) {
   return guard([&] {
     need(ctx, "ctx");
@@ -378,6 +399,30 @@ int dfs_rank_counters(dfs_ctx* ctx, uint32_t tau, uint64_t out[8]) {
     need(ctx, "ctx");
     need(out, "out");
     ctx->c->stage_counters(tau, out);
+  });
+}
+
+int dfs_format_report(const dfs_report_fields* f, char** json_out) {
+  return guard([&] {
+    need(f, "fields");
+    need(json_out, "json_out");
+    dfs::Report rep;
+    dfs_config c{f->k, f->r, f->devices, f->mode, f->weights, f->rebuild_eps, f->seed, 256, 0, 0};
+    rep.config = to_config(&c);
+    rep.n = f->n;
+    rep.m = f->m;
+    rep.seeds.assign(f->seeds, f->seeds + f->steps);
+    rep.seeds_dense.assign(f->seeds_dense, f->seeds_dense + f->steps);
+    rep.score_trajectory.assign(f->traj, f->traj + f->steps);
+    rep.rebuilds = f->rebuilds;
+    if (f->rebuilds) rep.rebuild_rounds.assign(f->rebuild_rounds, f->rebuild_rounds + f->rebuilds);
+    rep.saturated = f->saturated != 0;
+    rep.degraded_plan = f->degraded != 0;
+    rep.reduced_elements = f->reduced_elements;
+    rep.broadcast_elements = f->broadcast_elements;
+    rep.barriers = f->barriers;
+    rep.timings = {f->t_build, f->t_fill, f->t_simulate, f->t_select, f->t_cascade, f->t_total, 0};
+    *json_out = dup_string(dfs::report_to_json(rep, f->with_timings != 0));
   });
 }
 

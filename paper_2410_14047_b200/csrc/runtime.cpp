@@ -217,7 +217,8 @@ void Context::reset_rank_state(RankDev& r) {
   sync();
 }
 
-void Context::prepare(const RunConfig& cfg, const HostGraph* host_w_src) {
+void Context::prepare(const RunConfig& cfg, const HostGraph* host_w_src, uint32_t part_rank,
+                      uint32_t part_world) {
   if (!has_graph()) throw Error(kRuntime, "no graph uploaded");
   DFS_CUDA(cudaSetDevice(device_));
   // runtime.cpp:38-42, then gen_random_vector (sampling.cpp:8), make_plan
@@ -263,13 +264,17 @@ void Context::prepare(const RunConfig& cfg, const HostGraph* host_w_src) {
     }
   }
   // ---- per-rank state and sampled items (fasst.cpp:50-88, build phase)
-  ranks_.assign(cfg.mu, RankDev{});
-  for (uint32_t t = 0; t < cfg.mu; ++t) {
+  if (part_world && (part_world != cfg.mu || part_rank >= part_world))
+    throw Error(kInvalid, "partition rank/world must match devices");
+  const uint32_t first = part_world ? part_rank : 0;
+  const uint32_t count = part_world ? 1 : cfg.mu;
+  ranks_.assign(count, RankDev{});
+  for (uint32_t t = 0; t < count; ++t) {
     RankDev& r = ranks_[t];
-    alloc_rank(r, t);
+    alloc_rank(r, first + t);
     build_items(r, 0);
     build_items(r, 1);
-    const std::string p = "r" + std::to_string(t) + ".q.";
+    const std::string p = "r" + std::to_string(first + t) + ".q.";
     const uint64_t cap = std::max<uint64_t>(std::max(r.fwd.chunks, r.rev.chunks), 1);
     for (int gi = 0; gi < kGens; ++gi) {
       r.q.chunks[gi] = as<uint32_t>(arena_.get(p + "c" + std::to_string(gi), cap * 4));
@@ -500,6 +505,28 @@ void Context::stage_counters(uint32_t tau, uint64_t out[8]) {
   const uint64_t v[8] = {c.updates,     c.items_processed, c.cnt_edges,        c.cnt_batches,
                          c.cnt_touched, c.cnt_sweeps,      c.cnt_convergences, c.visited};
   for (int i = 0; i < 8; ++i) out[i] = v[i];
+}
+
+void Context::stage_scores_device(uint32_t tau, int full, double* dst) {
+  check_tau(tau, ranks_.size());
+  launch_score(ranks_[tau], full, nullptr, 0, stream_);
+  if (dst)
+    DFS_CUDA(cudaMemcpyAsync(dst, ranks_[tau].scores, size_t(g_.n) * 8, cudaMemcpyDeviceToDevice,
+                             stream_));
+  sync();
+}
+
+void Context::stage_rebuild(uint32_t tau) {
+  check_tau(tau, ranks_.size());
+  launch_fill(ranks_[tau], nullptr, 0, stream_);
+  launch_simulate(ranks_[tau], cfg_.jacobi, 0, cfg_.sim_cap, nullptr, 0, stream_);
+  launch_score(ranks_[tau], 1, nullptr, 0, stream_);
+  RankCtl c{};
+  DFS_CUDA(cudaMemcpyAsync(&c, ranks_[tau].ctl, sizeof c, cudaMemcpyDeviceToHost, stream_));
+  sync();
+  if (c.error)
+    throw Error(kRuntime, "simulate did not converge within " + std::to_string(cfg_.sim_cap) +
+                              " iterations; register monotonicity must be broken");
 }
 
 void Context::stage_get_registers(uint32_t tau, int8_t* out) {

@@ -84,7 +84,10 @@ class Context {
   bool has_graph() const { return g_.n > 0; }
 
   // Plan + weights + per-rank sampled items (the reference's "build" phase).
-  void prepare(const RunConfig& cfg, const HostGraph* host_w_src = nullptr);
+  // part_world > 0: this context holds only partition part_rank of
+  // part_world (= cfg.mu) — one FASST partition per GPU/process.
+  void prepare(const RunConfig& cfg, const HostGraph* host_w_src = nullptr,
+               uint32_t part_rank = 0, uint32_t part_world = 0);
   // Full greedy run on the resident graph.
   Report run(const RunConfig& cfg, const HostGraph* host_w_src = nullptr);
 
@@ -96,6 +99,9 @@ class Context {
   uint64_t stage_commit_cascade(uint32_t tau, uint32_t seed);
   uint64_t stage_visited(uint32_t tau);
   void stage_counters(uint32_t tau, uint64_t out[8]);
+  // Multi-process round pieces (device pointers; no host round-trip).
+  void stage_scores_device(uint32_t tau, int full, double* dst);
+  void stage_rebuild(uint32_t tau);
   void stage_get_registers(uint32_t tau, int8_t* out);
   void stage_set_registers(uint32_t tau, const int8_t* in);
   void stage_device_graph(uint32_t tau, std::vector<uint64_t>& off, std::vector<uint32_t>& adj,

@@ -214,3 +214,66 @@ def test_python_smoke_mirror(D):
     assert "timings" not in quiet
     assert quiet["seeds"] == rep["seeds"]
     assert set(rep["timings"]) == {"build", "fill", "simulate", "select", "cascade", "total"}
+
+
+def test_partition_contexts_match_reference(D, golden):
+    """The multi-process path's per-partition C-ABI (dfs_prepare_partition,
+    dfs_scores_device, dfs_rebuild, commit/cascade) driven for mu partitions on
+    one GPU, with the exchange done locally in the binomial order."""
+    import ctypes as C
+    import torch
+    from paper_2410_14047_b200 import _capi, _config
+    from paper_2410_14047_b200.dist import binomial_sum, select_seed
+    runs = golden["runs"]
+    for case in [c for c in runs["cases"] if c["config"]["devices"] in (2, 3, 4)]:
+        cfg = dict(case["config"])
+        g = _graph(D, runs["graphs"][case["graph"]])
+        mu, k, r = cfg["devices"], cfg["k"], cfg["r"]
+        ctxs = [D.Context(0) for _ in range(mu)]
+        bufs = []
+        for t, cx in enumerate(ctxs):
+            c = _config(k, r, mu, cfg.get("mode", "fasst"), cfg["weights"],
+                        cfg.get("rebuild_eps", 0.01), cfg.get("seed", 0))
+            _capi.check(_capi.lib().dfs_prepare_partition(cx._h, g._h, C.byref(c), t, mu))
+            _capi.check(_capi.lib().dfs_rebuild(cx._h, 0))
+            b = torch.empty(g.n, dtype=torch.float64, device="cuda")
+            _capi.check(_capi.lib().dfs_scores_device(cx._h, 0, 1, C.c_void_p(b.data_ptr())))
+            bufs.append(b)
+        committed = torch.zeros(g.n, dtype=torch.bool, device="cuda")
+        want = json.loads(case["json"])
+        old, seeds, traj, rb = 0.0, [], [], []
+        rebuilt = True
+        for step in range(k):
+            if not rebuilt:
+                for cx, b in zip(ctxs, bufs):
+                    _capi.check(_capi.lib().dfs_scores_device(cx._h, 0, 0, C.c_void_p(b.data_ptr())))
+            rebuilt = False
+            s, _ = select_seed(binomial_sum(torch.stack(bufs)), committed, 0, 1)
+            committed[s] = True
+            covered = sum(cx.commit_cascade(0, s) for cx in ctxs)
+            score = covered / r
+            seeds.append(s)
+            traj.append(score)
+            if step + 1 < k and (score - old) > cfg.get("rebuild_eps", 0.01) * score:
+                for cx, b in zip(ctxs, bufs):
+                    _capi.check(_capi.lib().dfs_rebuild(cx._h, 0))
+                    _capi.check(_capi.lib().dfs_scores_device(cx._h, 0, 1, C.c_void_p(b.data_ptr())))
+                rebuilt = True
+                old = score
+                rb.append(step)
+        assert seeds == want["seeds_dense"], cfg
+        assert traj == want["score_trajectory"], cfg
+        assert rb == want["rebuild_rounds"], cfg
+
+
+def test_dist_runner_single_rank_report(D, ctx, golden):
+    """DistRunner (the multi-process driver) at world=1 produces the reference
+    report byte-for-byte."""
+    from paper_2410_14047_b200.dist import DistRunner
+    runs = golden["runs"]
+    for case in [c for c in runs["cases"] if c["config"]["devices"] == 1][:6]:
+        cfg = dict(case["config"])
+        cfg.pop("devices")
+        g = _graph(D, runs["graphs"][case["graph"]])
+        got = DistRunner(ctx, g, 0, 1).run(**cfg)
+        assert got == case["json"], case["config"]
