@@ -18,3 +18,10 @@ lines = [(r[0], r[1], int(r[wi])) for r in rows if r and r[0].isdigit() and r[wi
 tot = sum(x[2] for x in lines) or 1
 for ln, src, w in sorted(lines, key=lambda x: -x[2])[:top]:
     print(f"{100 * w / tot:5.1f}%  L{ln:>5s}  {src.strip()[:100]}")
+
+ii = hdr.index("Instructions Executed")
+lines2 = [(r[0], r[1], int(r[ii])) for r in rows if r and r[0].isdigit() and r[ii].isdigit()]
+tot2 = sum(x[2] for x in lines2) or 1
+print("\n# top lines by warp instructions executed")
+for ln, src, w in sorted(lines2, key=lambda x: -x[2])[:top]:
+    print(f"{100 * w / tot2:5.1f}%  L{ln:>5s}  {src.strip()[:100]}")
