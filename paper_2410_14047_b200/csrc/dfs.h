@@ -69,6 +69,9 @@ struct Items {
   uint32_t* small = nullptr;
   uint32_t* big = nullptr;
   uint32_t nsmall = 0, nbig = 0;
+  // flat list of the item indices of small rows (flat full passes)
+  uint32_t* small_items = nullptr;
+  uint64_t nsmall_items = 0;
 };
 constexpr uint32_t kSmallRow = 32;
 
@@ -169,6 +172,8 @@ void launch_row_offsets(const DevGraph& g, int dir, const uint64_t* pos_off, Ite
 void launch_chunk_write(uint32_t n, Items& it, const uint64_t* row_chunk64, cudaStream_t s);
 // Split chunk ids into it.small / it.big (counts written to cnt2[0..1]).
 void launch_split_chunks(Items& it, unsigned int* cnt2, cudaStream_t s);
+// it.small_items <- item indices of the chunks in it.small (count in *cnt).
+void launch_small_items(Items& it, unsigned long long* cnt, cudaStream_t s);
 // Fill registers (VISITED kept, pads VISITED).  gate: run only if *gate == want.
 void launch_fill(const RankDev& r, const unsigned int* gate, unsigned int want, cudaStream_t s);
 // Persistent cooperative simulate to convergence.  jacobi != 0 reproduces the
@@ -178,6 +183,7 @@ void launch_simulate(const RankDev& r, int jacobi, int count, int cap, const uns
                      unsigned int want, cudaStream_t s);
 // Number of kernels this library launched (all launchers), for gpu_launches.
 unsigned long long launches();
+void dump_trace();  // debug (DFS_DBG bit 2)
 // Row scores: full = all rows, else the dirty list of the last cascade.
 void launch_score(const RankDev& r, int full, const unsigned int* gate, unsigned int want,
                   cudaStream_t s);

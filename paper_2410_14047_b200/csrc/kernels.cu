@@ -18,6 +18,7 @@
 #include <cub/cub.cuh>
 #include <cuda/std/functional>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "dfs.h"
@@ -33,7 +34,23 @@ void cuda_check(cudaError_t e, const char* what) {
                 std::string("CUDA error: ") + cudaGetErrorString(e) + " at " + what);
 }
 
+// Debug trace (DFS_DBG bit 2): (kind, index, frontier, clock) records written
+// by block 0 thread 0; dumped by dump_trace().  Not used on the timed path.
+__device__ unsigned long long g_trace[8192][4];
+__device__ unsigned int g_trace_n;
+
 namespace {
+
+__device__ __forceinline__ void trace(unsigned long long kind, unsigned long long idx,
+                                      unsigned long long nc) {
+  const unsigned k = atomicAdd(&g_trace_n, 1u);
+  if (k < 8192) {
+    g_trace[k][0] = kind;
+    g_trace[k][1] = idx;
+    g_trace[k][2] = nc;
+    g_trace[k][3] = clock64();
+  }
+}
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
@@ -241,6 +258,35 @@ __global__ void k_split_chunks(uint64_t chunks, const uint32_t* __restrict__ chu
   }
 }
 
+// Item indices of small chunks (each small row is one chunk of <= kSmallRow
+// items): warp per 32 chunks, warp-aggregated append keeps rows contiguous.
+__global__ void k_small_items(uint32_t nsmall, const uint32_t* __restrict__ small,
+                              const uint64_t* __restrict__ chunk_beg, uint32_t* __restrict__ out,
+                              unsigned long long* cnt) {
+  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t k0 = ((uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 32; k0 < nsmall;
+       k0 += nw * 32) {
+    const uint64_t k = k0 + lane_id();
+    uint64_t beg = 0;
+    uint32_t len = 0;
+    if (k < nsmall) {
+      const uint32_t c = small[k];
+      beg = chunk_beg[c];
+      len = uint32_t(chunk_beg[c + 1] - beg);
+    }
+    uint32_t incl = len;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane_id() >= unsigned(o)) incl += t;
+    }
+    unsigned long long base = 0;
+    if (lane_id() == 31) base = atomicAdd(cnt, (unsigned long long)incl);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    const uint64_t o = base + incl - len;
+    for (uint32_t j = 0; j < len; ++j) out[o + j] = uint32_t(beg + j);
+  }
+}
+
 // ---------------------------------------------------------------- fill
 // sketch.cpp:55-66: M[u][j] = clz64(fmix64(jkey[j] + u*golden)) unless VISITED.
 // One thread per 4 registers (one u32 store, coalesced across the warp).
@@ -339,17 +385,22 @@ struct WarpStage {
 template <class F>
 __device__ __forceinline__ void for_frontier_items(const Items& it, const uint32_t* frontier,
                                                    uint32_t nc, unsigned int* work_ctr,
-                                                   WarpStage& ws, F&& f) {
+                                                   WarpStage& ws, uint64_t n_warps, F&& f) {
   const unsigned lane = lane_id();
+  // Chunks claimed per warp: 32 when the frontier is large (tiny R-MAT rows
+  // keep lanes busy), fewer when it is small so that a few full chunks
+  // (<= 128 items each) are spread over many warps instead of serialised.
+  const uint64_t per = n_warps ? nc / n_warps : nc;
+  const uint32_t G = per >= 32 ? 32u : (per < 1 ? 1u : uint32_t(per));
   for (;;) {
     unsigned b0 = 0;
-    if (lane == 0) b0 = atomicAdd(work_ctr, 32u);
+    if (lane == 0) b0 = atomicAdd(work_ctr, G);
     b0 = __shfl_sync(0xffffffffu, b0, 0);
     if (b0 >= nc) break;
     const uint32_t idx = b0 + lane;
     uint32_t row = 0, cntc = 0;
     unsigned long long beg = 0;
-    if (idx < nc) {
+    if (lane < G && idx < nc) {
       const uint32_t c = frontier ? __ldcg(frontier + idx) : idx;
       row = it.chunk_row[c];
       beg = it.chunk_beg[c];
@@ -397,7 +448,7 @@ __device__ __forceinline__ void for_frontier_items(const Items& it, const uint32
 }
 
 constexpr unsigned long long kNeg8 = 0x8080808080808080ull;  // "no contribution"
-constexpr uint32_t kSoloChunks = 64;  // frontier (chunks) a single block iterates alone
+constexpr uint32_t kSoloChunks = 16;  // frontier (chunks) a single block iterates alone
 constexpr uint32_t kPullMaxJp = 4096;  // pull accumulators live in shared memory
 
 // Shared-memory running max of the live bytes of one source word.
@@ -527,6 +578,7 @@ struct SimArgs {
   const unsigned int* gate;
   unsigned int want;
   int dbg;  // experiments only (DFS_DBG): bit0 skip big-row pull, bit1 skip small rows
+  int pull_f;  // pull when frontier chunks * pull_f > total chunks (DFS_SIM_PULL, default 4)
 };
 
 // Persistent simulate-to-convergence (engine.cpp:57-96 semantics).  Sweep s
@@ -592,12 +644,12 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) 
       cnt[gr] = 0;
       cnt[4 + gr] = 0;
       cnt[8 + gr] = 0;
+      *reinterpret_cast<unsigned long long*>(&cnt[12 + 2 * ((s + 1) & 1)]) = 0;  // next sweep's
     }
     const uint32_t stamp = base + s;
     uint32_t* rows_n = r.q.rows[gn];
     uint32_t* chunks_n = r.q.chunks[gn];
-    if ((a.dbg & 4) && blockIdx.x == 0 && threadIdx.x == 0)
-      printf("simulate s=%u nc=%u solo=%d t=%lld\n", s, nc, int(solo), (long long)clock64());
+    if ((a.dbg & 4) && blockIdx.x == 0 && threadIdx.x == 0) trace(solo ? 1 : 0, s, nc);
     // Large frontiers (and sweep 1) run PULL-style over row-owned forward
     // chunks: a warp gathers the sources of one destination row chunk into a
     // shared-memory accumulator and writes each touched word once (plain store
@@ -605,31 +657,54 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) 
     // chunk instead of one contended CAS per item.  Small frontiers push.
     // Count mode keeps the exact push frontier of the reference schedule.
     const bool pull =
-        !CNT && !solo && pull_ok && (s == 1 || uint64_t(nc) * 4 > r.rev.chunks);
+        !CNT && !solo && pull_ok && (s == 1 || uint64_t(nc) * a.pull_f > r.rev.chunks);
     if (pull) {
       const uint32_t need = base + s - 1;  // source changed in sweep s-1 (or later)
       for (uint64_t k = my_warp; k < ((a.dbg & 1) ? 0 : r.fwd.nbig); k += n_warps) {
         const uint32_t c = r.fwd.big[k];
         const uint32_t u = r.fwd.chunk_row[c];
         const uint64_t beg = r.fwd.chunk_beg[c], end = r.fwd.chunk_beg[c + 1];
-        for (uint64_t i = beg + lane; i < end; i += 32) {
-          const uint32_t v = __ldg(r.fwd.other + i);
-          if (s > 1 && __ldcg(r.lstamp + v) < need) continue;
-          const uint32_t mk = __ldg(r.fwd.mask + i);
-          const uint32_t b = __ldg(r.fwd.batch + i);
+        // A chunk has <= 4*32 items: each lane stages its (up to) 4 items'
+        // fields, stamps and first live source word before any is consumed.
+        uint32_t vq[4], mq[4], bq[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint64_t i = beg + lane + 32 * q;
+          const bool act = i < end;
+          vq[q] = act ? __ldg(r.fwd.other + i) : 0;
+          mq[q] = act ? __ldg(r.fwd.mask + i) : 0;
+          bq[q] = act ? __ldg(r.fwd.batch + i) : 0;
+        }
+        if (s > 1) {
+          uint32_t st[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) st[q] = mq[q] ? __ldcg(r.lstamp + vq[q]) : 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (st[q] < need) mq[q] = 0;
+        }
+        unsigned long long s0[4];
+        int w0[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          w0[q] = mq[q] ? (__ffs(mq[q]) - 1) >> 3 : 0;
+          s0[q] = mq[q] ? __ldcg(reinterpret_cast<const unsigned long long*>(
+                              srcm + uint64_t(vq[q]) * Jp + bq[q] * 32) + w0[q])
+                        : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (!mq[q]) continue;
+          const uint32_t b = bq[q];
+          acc_max(&acc[b * 4 + w0[q]], s0[q], (mq[q] >> (8 * w0[q])) & 0xFFu);
           const unsigned long long* sp =
-              reinterpret_cast<const unsigned long long*>(srcm + uint64_t(v) * Jp + b * 32);
-          unsigned long long sv[4];
-#pragma unroll
-          for (int wv = 0; wv < 4; ++wv)
-            if ((mk >> (8 * wv)) & 0xFFu) sv[wv] = __ldcg(sp + wv);
-#pragma unroll
-          for (int wv = 0; wv < 4; ++wv) {
-            const uint32_t m8 = (mk >> (8 * wv)) & 0xFFu;
-            if (m8) acc_max(&acc[b * 4 + wv], sv[wv], m8);
+              reinterpret_cast<const unsigned long long*>(srcm + uint64_t(vq[q]) * Jp + b * 32);
+          for (int wv = w0[q] + 1; wv < 4; ++wv) {
+            const uint32_t m8 = (mq[q] >> (8 * wv)) & 0xFFu;
+            if (m8) acc_max(&acc[b * 4 + wv], __ldcg(sp + wv), m8);
           }
           atomicOr(&touched[b >> 5], 1u << (b & 31));
-          upd += __popc(mk);
+          upd += __popc(mq[q]);
           ++nitems;
         }
         __syncwarp();
@@ -671,46 +746,74 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) 
       }
       // Small destination rows (<= kSmallRow items): item-parallel over the
       // flattened chunks, one CAS per item on a lightly contended row.
-      for_frontier_items(r.fwd, r.fwd.small, (a.dbg & 2) ? 0 : r.fwd.nsmall, &cnt[8 + g], ws,
-                         [&](uint32_t ua, uint64_t ia, bool pa, uint32_t ub, uint64_t ib, bool pb) {
-        const uint32_t va = pa ? __ldg(r.fwd.other + ia) : 0;
-        const uint32_t vb = pb ? __ldg(r.fwd.other + ib) : 0;
-        SimItem A, B;
-        if (pa) {
-          A.u = ua;
-          A.mk = __ldg(r.fwd.mask + ia);
-          A.b = __ldg(r.fwd.batch + ia);
+      {
+        const uint64_t nsi = (a.dbg & 2) ? 0 : r.fwd.nsmall_items;
+        // dynamic: a warp claims 128 items at a time (balances the big-row tail)
+        for (;;) {
+          unsigned long long k0 = 0;
+          if (lane == 0)
+            k0 = atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[12 + 2 * (s & 1)]), 128ull);
+          k0 = __shfl_sync(0xffffffffu, k0, 0);
+          if (k0 >= nsi) break;
+          // four items per lane, every load stage issued for all four first
+          uint64_t iq[4];
+          uint32_t uq[4], vq[4], mq[4], bq[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint64_t kk = k0 + lane + 32 * q;
+            iq[q] = kk < nsi ? __ldg(r.fwd.small_items + kk) : 0;
+            mq[q] = kk < nsi ? 1u : 0u;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uq[q] = mq[q] ? __ldg(r.fwd.row + iq[q]) : 0;
+            vq[q] = mq[q] ? __ldg(r.fwd.other + iq[q]) : 0;
+            bq[q] = mq[q] ? __ldg(r.fwd.batch + iq[q]) : 0;
+            mq[q] = mq[q] ? __ldg(r.fwd.mask + iq[q]) : 0;
+          }
+          if (s > 1) {
+            uint32_t st[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) st[q] = mq[q] ? __ldcg(r.lstamp + vq[q]) : 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (st[q] < need) mq[q] = 0;
+          }
+          unsigned long long s0[4], d0[4];
+          int w0[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            w0[q] = mq[q] ? (__ffs(mq[q]) - 1) >> 3 : 0;
+            s0[q] = mq[q] ? __ldcg(reinterpret_cast<const unsigned long long*>(
+                                srcm + uint64_t(vq[q]) * Jp + bq[q] * 32) + w0[q])
+                          : 0;
+            d0[q] = mq[q] ? __ldcg(reinterpret_cast<const unsigned long long*>(
+                                r.regs + uint64_t(uq[q]) * Jp + bq[q] * 32) + w0[q])
+                          : 0;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (!mq[q]) continue;
+            unsigned long long* dp =
+                reinterpret_cast<unsigned long long*>(r.regs + uint64_t(uq[q]) * Jp + bq[q] * 32);
+            const unsigned long long* sp = reinterpret_cast<const unsigned long long*>(
+                srcm + uint64_t(vq[q]) * Jp + bq[q] * 32);
+            bool ch = cas_merge(dp + w0[q], d0[q], s0[q], (mq[q] >> (8 * w0[q])) & 0xFFu);
+            for (int wv = w0[q] + 1; wv < 4; ++wv) {
+              const uint32_t m8 = (mq[q] >> (8 * wv)) & 0xFFu;
+              if (m8) ch |= cas_merge(dp + wv, __ldcg(dp + wv), __ldcg(sp + wv), m8);
+            }
+            upd += __popc(mq[q]);
+            ++nitems;
+            if (ch)
+              push_row(uq[q], stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &cnt[gn],
+                       &cnt[4 + gn]);
+          }
         }
-        if (pb) {
-          B.u = ub;
-          B.mk = __ldg(r.fwd.mask + ib);
-          B.b = __ldg(r.fwd.batch + ib);
-        }
-        if (s > 1) {
-          const uint32_t sta = pa ? __ldcg(r.lstamp + va) : 0;
-          const uint32_t stb = pb ? __ldcg(r.lstamp + vb) : 0;
-          pa = pa && sta >= need;
-          pb = pb && stb >= need;
-        }
-        bool ca, cb;
-        sim_pair(ua, A.mk, A.b, pa, srcm + uint64_t(va) * Jp, ub, B.mk, B.b, pb,
-                 srcm + uint64_t(vb) * Jp, r.regs, Jp, ca, cb);
-        if (pa) {
-          upd += __popc(A.mk);
-          ++nitems;
-        }
-        if (pb) {
-          upd += __popc(B.mk);
-          ++nitems;
-        }
-        if (ca)
-          push_row(ua, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
-        if (cb)
-          push_row(ub, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
-      });
+      }
     } else {
       for_frontier_items(
-          r.rev, s == 1 ? nullptr : r.q.chunks[g], nc, &cnt[8 + g], ws,
+          r.rev, s == 1 ? nullptr : r.q.chunks[g], nc, &cnt[8 + g], ws, n_warps,
           [&](uint32_t va, uint64_t ia, bool pa, uint32_t vb, uint64_t ib, bool pb) {
             SimItem A, B;
             if (pa) sim_fields(A, r.rev, ia);
@@ -1029,6 +1132,7 @@ struct CasArgs {
   const unsigned int* choice;
   uint32_t seed;
   int dbg;  // experiments only (DFS_DBG bit 2): per-level trace
+  int pull_f;  // bottom-up when frontier chunks * pull_f > total (DFS_CAS_PULL, default 8)
 };
 
 // Clear the fresh bits of the rows listed in one generation.
@@ -1113,10 +1217,7 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
       cnt[8 + gr] = 0;
     }
     clear_rows(fprev, r.q.rows[gp], ld_volatile(&cnt[4 + gp]), W32, my_warp, n_warps, lane);
-    if ((a.dbg & 4) && blockIdx.x == 0 && threadIdx.x == 0)
-      printf("cascade L=%u nc=%u rows=%u solo=%d pull=%d t=%lld\n", L, nc, ld_volatile(&cnt[4 + g]),
-             int(solo), int(!solo && pull_ok && uint64_t(nc) * 4 > r.fwd.chunks),
-             (long long)clock64());
+    if ((a.dbg & 4) && blockIdx.x == 0 && threadIdx.x == 0) trace(2 + (solo ? 1 : 0), L, nc);
     const uint32_t stamp = base + L + 1;
     uint32_t* rows_n = r.q.rows[gn];
     uint32_t* chunks_n = r.q.chunks[gn];
@@ -1146,7 +1247,7 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
       if (ca) claim(va, ba, ca);
       if (cb) claim(vb, bb, cb);
     };
-    if (!solo && pull_ok && uint64_t(nc) * 4 > r.fwd.chunks) {
+    if (!solo && pull_ok && uint64_t(nc) * a.pull_f > r.fwd.chunks) {
       // Large frontier: bottom-up (pull) level over row-owned reverse chunks.
       // A warp ORs the fresh bits of all in-neighbours of one target row into
       // a shared accumulator, then claims the unvisited ones with one update
@@ -1156,15 +1257,24 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
         const uint32_t v = r.rev.chunk_row[c];
         const uint64_t beg = r.rev.chunk_beg[c], end = r.rev.chunk_beg[c + 1];
         bool any = false;
-        for (uint64_t i = beg + lane; i < end; i += 32) {
-          const uint32_t b = __ldg(r.rev.batch + i);
-          const uint32_t f =
-              __ldcg(fcur + uint64_t(__ldg(r.rev.other + i)) * W32 + b) & __ldg(r.rev.mask + i);
-          if (f) {
-            atomicOr(&cacc[b], f);
+        uint32_t uq[4], mq[4], bq[4], fq[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint64_t i = beg + lane + 32 * q;
+          const bool act = i < end;
+          uq[q] = act ? __ldg(r.rev.other + i) : 0;
+          mq[q] = act ? __ldg(r.rev.mask + i) : 0;
+          bq[q] = act ? __ldg(r.rev.batch + i) : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          fq[q] = mq[q] ? __ldcg(fcur + uint64_t(uq[q]) * W32 + bq[q]) & mq[q] : 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (fq[q]) {
+            atomicOr(&cacc[bq[q]], fq[q]);
             any = true;
           }
-        }
         if (!__any_sync(0xffffffffu, any)) continue;
         __syncwarp();
         const bool owner = r.rev.row_chunk[v + 1] - r.rev.row_chunk[v] == 1;
@@ -1198,7 +1308,7 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
         }
       }
       // Small target rows: item-parallel, one atomicOr per newly reached word.
-      for_frontier_items(r.rev, r.rev.small, r.rev.nsmall, &cnt[8 + g], ws,
+      for_frontier_items(r.rev, r.rev.small, r.rev.nsmall, &cnt[8 + g], ws, n_warps,
                          [&](uint32_t va, uint64_t ia, bool pa, uint32_t vb, uint64_t ib, bool pb) {
         const uint32_t ba = pa ? __ldg(r.rev.batch + ia) : 0, bb = pb ? __ldg(r.rev.batch + ib) : 0;
         const uint32_t ma = pa ? __ldg(r.rev.mask + ia) : 0, mb = pb ? __ldg(r.rev.mask + ib) : 0;
@@ -1213,7 +1323,7 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
         if (cb) claim(vb, bb, cb);
       });
     } else {
-      for_frontier_items(r.fwd, r.q.chunks[g], nc, &cnt[8 + g], ws, visit);
+      for_frontier_items(r.fwd, r.q.chunks[g], nc, &cnt[8 + g], ws, n_warps, visit);
     }
   };
   // Final clean-up: fresh bits left by the last two levels.
@@ -1312,6 +1422,21 @@ __global__ void k_round_end(RunArrays ra, RankCtl* const* ctls, uint32_t mu, uin
 // ================================================================= launchers
 static unsigned long long g_launches = 0;
 unsigned long long launches() { return g_launches; }
+
+void dump_trace() {
+  static unsigned long long h[8192][4];
+  unsigned int n = 0;
+  DFS_CUDA(cudaDeviceSynchronize());
+  DFS_CUDA(cudaMemcpyFromSymbol(&n, g_trace_n, sizeof n));
+  n = n > 8192 ? 8192 : n;
+  DFS_CUDA(cudaMemcpyFromSymbol(h, g_trace, sizeof(unsigned long long) * 4 * n));
+  static const char* names[] = {"sim", "sim-solo", "cas", "cas-solo"};
+  for (unsigned i = 0; i < n; ++i)
+    fprintf(stderr, "trace %-8s idx=%-4llu nc=%-8llu dt=%.1f us\n", names[h[i][0] & 3], h[i][1],
+            h[i][2], i ? (h[i][3] - h[i - 1][3]) / 1965.0 : 0.0);
+  unsigned int z = 0;
+  DFS_CUDA(cudaMemcpyToSymbol(g_trace_n, &z, sizeof z));
+}
 size_t graph_prepare_tmp_bytes(uint64_t m, uint32_t n) {
   size_t sort_bytes = 0, scan_bytes = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const uint32_t*)nullptr,
@@ -1424,6 +1549,14 @@ void launch_split_chunks(Items& it, unsigned int* cnt2, cudaStream_t s) {
   ++g_launches;
 }
 
+void launch_small_items(Items& it, unsigned long long* cnt, cudaStream_t s) {
+  if (!it.nsmall) return;
+  k_small_items<<<grid_for(uint64_t(it.nsmall)), kThreads, 0, s>>>(it.nsmall, it.small,
+                                                                   it.chunk_beg, it.small_items, cnt);
+  DFS_CUDA(cudaGetLastError());
+  ++g_launches;
+}
+
 void launch_fill(const RankDev& r, const unsigned int* gate, unsigned int want, cudaStream_t s) {
   const uint64_t total = uint64_t(r.n) * 32;
   if (!r.n) return;
@@ -1470,7 +1603,8 @@ int coop_grid(int which, int variant) {
 void launch_simulate(const RankDev& r, int jacobi, int count, int cap, const unsigned int* gate,
                      unsigned int want, cudaStream_t s) {
   static const int dbg = getenv("DFS_DBG") ? atoi(getenv("DFS_DBG")) : 0;
-  SimArgs a{r, cap, gate, want, dbg};
+  static const int pf = getenv("DFS_SIM_PULL") ? atoi(getenv("DFS_SIM_PULL")) : 4;
+  SimArgs a{r, cap, gate, want, dbg, pf};
   void* args[] = {&a};
   const int variant = jacobi ? (count ? 2 : 1) : 0;
   DFS_CUDA(cudaLaunchCooperativeKernel(sim_kernel(variant), dim3(coop_grid(0, variant)),
@@ -1505,7 +1639,8 @@ void launch_argmax(const double* scores, RunArrays& ra, uint32_t n, cudaStream_t
 
 void launch_cascade(const RankDev& r, const unsigned int* choice, uint32_t seed, cudaStream_t s) {
   static const int dbg = getenv("DFS_DBG") ? atoi(getenv("DFS_DBG")) : 0;
-  CasArgs a{r, choice, seed, dbg};
+  static const int pf = getenv("DFS_CAS_PULL") ? atoi(getenv("DFS_CAS_PULL")) : 8;
+  CasArgs a{r, choice, seed, dbg, pf};
   void* args[] = {&a};
   DFS_CUDA(cudaLaunchCooperativeKernel((void*)k_cascade, dim3(coop_grid(1)), dim3(kThreads), args,
                                        kCasSmem, s));

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <cstdlib>
 #include <numeric>
 
 #include "hash.cuh"
@@ -198,6 +199,14 @@ void Context::build_items(RankDev& r, int dir) {
   sync();
   it.nsmall = hc[0];
   it.nbig = hc[1];
+  it.small_items = as<uint32_t>(arena_.get(p + "small_items", std::max<uint64_t>(it.count, 1) * 4));
+  unsigned long long* c3 = as<unsigned long long>(arena_.get("tmp.split64", 16));
+  DFS_CUDA(cudaMemsetAsync(c3, 0, 8, stream_));
+  launch_small_items(it, c3, stream_);
+  unsigned long long hn = 0;
+  DFS_CUDA(cudaMemcpyAsync(&hn, c3, 8, cudaMemcpyDeviceToHost, stream_));
+  sync();
+  it.nsmall_items = hn;
 }
 
 void Context::reset_rank_state(RankDev& r) {
@@ -377,6 +386,7 @@ Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
   }
   size_t eend = mark();
   sync();
+  if (getenv("DFS_DBG") && (atoi(getenv("DFS_DBG")) & 4)) dump_trace();
 
   // ---- results
   Report rep;
