@@ -195,6 +195,11 @@ void launch_cascade(const RankDev& r, const unsigned int* choice, uint32_t seed,
                     cudaStream_t s);
 void launch_round_end(RunArrays& ra, RankCtl* const* ctls_dev, uint32_t mu, uint32_t k,
                       uint32_t r, double eps, cudaStream_t s);
-int coop_grid(int which, int variant = 0);  // 0 simulate, 1 cascade
+int coop_grid(int which, int variant = 0);  // 0 simulate, 1 cascade, 2 whole run
+// The whole greedy loop (after the build phase) as one persistent kernel.
+void launch_run(const RankDev* ranks_dev, uint32_t mu, uint32_t k, uint32_t R, uint32_t n,
+                double eps, int cap, int jacobi, int count, int K, RunArrays& ra,
+                const double* const* parts, RankCtl* const* ctls, double* reduced,
+                unsigned long long* phase_ns, cudaStream_t s);
 
 }  // namespace dfs

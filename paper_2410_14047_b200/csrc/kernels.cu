@@ -290,10 +290,10 @@ __global__ void k_small_items(uint32_t nsmall, const uint32_t* __restrict__ smal
 // ---------------------------------------------------------------- fill
 // sketch.cpp:55-66: M[u][j] = clz64(fmix64(jkey[j] + u*golden)) unless VISITED.
 // One thread per 4 registers (one u32 store, coalesced across the warp).
-__global__ void k_fill(uint32_t n, uint32_t J, uint32_t Jp, const uint64_t* __restrict__ jkey,
-                       const uint32_t* __restrict__ vis, int8_t* __restrict__ regs,
-                       const unsigned int* gate, unsigned int want, RankCtl* ctl) {
-  if (gate && ld_volatile(gate) != want) return;
+__device__ __forceinline__ void fill_body(uint32_t n, uint32_t J, uint32_t Jp,
+                                          const uint64_t* __restrict__ jkey,
+                                          const uint32_t* __restrict__ vis,
+                                          int8_t* __restrict__ regs, RankCtl* ctl) {
   if (ctl && blockIdx.x == 0 && threadIdx.x == 0) ctl->dirty_count = 0;  // full rescore follows
   const uint32_t q = Jp >> 2;
   const uint32_t W32 = Jp >> 5;
@@ -316,6 +316,13 @@ __global__ void k_fill(uint32_t n, uint32_t J, uint32_t Jp, const uint64_t* __re
       row[w] = word;
     }
   }
+}
+
+__global__ void k_fill(uint32_t n, uint32_t J, uint32_t Jp, const uint64_t* __restrict__ jkey,
+                       const uint32_t* __restrict__ vis, int8_t* __restrict__ regs,
+                       const unsigned int* gate, unsigned int want, RankCtl* ctl) {
+  if (gate && ld_volatile(gate) != want) return;
+  fill_body(n, J, Jp, jkey, vis, regs, ctl);
 }
 
 // ---------------------------------------------------------------- simulate
@@ -591,13 +598,17 @@ struct SimArgs {
 #ifndef DFS_SIM_MINB
 #define DFS_SIM_MINB 3
 #endif
+struct SimOpts {
+  int cap;
+  int dbg;
+  int pull_f;
+};
+
 template <int JAC, int CNT>
-__global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) {
-  if (a.gate && ld_volatile(a.gate) != a.want) return;  // grid-uniform
-  __shared__ WarpStage stage[kWarps];
-  __shared__ unsigned long long s_release;
-  cg::grid_group grid = cg::this_grid();
-  const RankDev& r = a.r;
+__device__ __forceinline__ void simulate_body(const RankDev& r, const SimOpts& a,
+                                              cg::grid_group& grid, WarpStage* stage,
+                                              unsigned long long& s_release,
+                                              unsigned long long* dyn_smem) {
   unsigned int* cnt = r.q.counts;
   const uint32_t base = ld_volatile(&r.ctl->tick);
   const unsigned lane = lane_id();
@@ -607,7 +618,6 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) 
   const uint64_t nw = gthreads >> 5;
   WarpStage& ws = stage[threadIdx.x >> 5];
   // Pull accumulator: Jp bytes of running maxima + touched-batch bits per warp.
-  extern __shared__ unsigned long long dyn_smem[];
   const uint32_t W32 = r.W32;
   const bool pull_ok = r.Jp <= kPullMaxJp;
   unsigned long long* acc = dyn_smem + (threadIdx.x >> 5) * (kPullMaxJp / 8 + 8);
@@ -976,6 +986,20 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) 
   }
 }
 
+template <int JAC, int CNT>
+__global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) {
+  if (a.gate && ld_volatile(a.gate) != a.want) return;  // grid-uniform
+  __shared__ WarpStage stage[kWarps];
+  __shared__ unsigned long long s_release;
+  __shared__ RankDev s_r;
+  extern __shared__ unsigned long long dyn_smem[];
+  if (threadIdx.x == 0) s_r = a.r;
+  __syncthreads();
+  cg::grid_group grid = cg::this_grid();
+  const SimOpts o{a.cap, a.dbg, a.pull_f};
+  simulate_body<JAC, CNT>(s_r, o, grid, stage, s_release, dyn_smem);
+}
+
 // ---------------------------------------------------------------- score
 // sketch.cpp:119-131: live = #non-VISITED, denom = sum 2^-M[j] (ascending j),
 // score = live*live / (denom*phi).  With every live register <= K and
@@ -983,10 +1007,10 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) 
 // below 2^53 * 2^-K, so the reference's double sum is exact and equals the
 // integer sum sum 2^(K-M[j]) scaled by 2^-K.  Rows with a
 // larger register fall back to the sequential double sum.
-__global__ void k_score(const int8_t* __restrict__ regs, uint32_t n, uint32_t J, uint32_t Jp,
-                        int K, int full, const uint32_t* __restrict__ rows, RankCtl* ctl,
-                        double* __restrict__ scores, const unsigned int* gate, unsigned int want) {
-  if (gate && ld_volatile(gate) != want) return;
+__device__ __forceinline__ void score_body(const int8_t* __restrict__ regs, uint32_t n, uint32_t J,
+                                           uint32_t Jp, int K, int full,
+                                           const uint32_t* __restrict__ rows, RankCtl* ctl,
+                                           double* __restrict__ scores) {
   const uint32_t nrows = full ? n : ld_volatile(&ctl->dirty_count);
   const unsigned lane = lane_id();
   const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
@@ -1033,10 +1057,17 @@ __global__ void k_score(const int8_t* __restrict__ regs, uint32_t n, uint32_t J,
   }
 }
 
+__global__ void k_score(const int8_t* __restrict__ regs, uint32_t n, uint32_t J, uint32_t Jp,
+                        int K, int full, const uint32_t* __restrict__ rows, RankCtl* ctl,
+                        double* __restrict__ scores, const unsigned int* gate, unsigned int want) {
+  if (gate && ld_volatile(gate) != want) return;
+  score_body(regs, n, J, Jp, K, full, rows, ctl, scores);
+}
+
 // ---------------------------------------------------------------- reduce/argmax
 // collectives.cpp:44-64: level k folds rank+2^k into rank (fixed order).
-__global__ void k_treesum(const double* const* __restrict__ parts, uint32_t mu, uint32_t n,
-                          double* __restrict__ out) {
+__device__ __forceinline__ void treesum_body(const double* const* __restrict__ parts,
+                                             uint32_t mu, uint32_t n, double* __restrict__ out) {
   for (uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n;
        v += uint64_t(gridDim.x) * blockDim.x) {
     double acc[64];
@@ -1045,6 +1076,11 @@ __global__ void k_treesum(const double* const* __restrict__ parts, uint32_t mu, 
       for (uint32_t t = 0; t + st < mu; t += 2 * st) acc[t] = __dadd_rn(acc[t], acc[t + st]);
     out[v] = acc[0];
   }
+}
+
+__global__ void k_treesum(const double* const* __restrict__ parts, uint32_t mu, uint32_t n,
+                          double* __restrict__ out) {
+  treesum_body(parts, mu, n, out);
 }
 
 struct Best {
@@ -1067,8 +1103,10 @@ __device__ __forceinline__ Best best_of(Best a, Best b) {
   return r;
 }
 
-__global__ void __launch_bounds__(kThreads) k_argmax(const double* __restrict__ scores,
-                                                     uint32_t n, RunArrays ra) {
+// Block partial of the argmax (runtime.cpp:95-119): best positive
+// uncommitted (score, id) and the smallest uncommitted id of this block.
+__device__ __forceinline__ void argmax_partial(const double* __restrict__ scores, uint32_t n,
+                                               const RunArrays& ra, Best* sb) {
   Best b{0.0, 0xFFFFFFFFu, 0xFFFFFFFFu};
   for (uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n;
        v += uint64_t(gridDim.x) * blockDim.x) {
@@ -1085,8 +1123,7 @@ __global__ void __launch_bounds__(kThreads) k_argmax(const double* __restrict__ 
            __shfl_xor_sync(0xffffffffu, b.minu, o)};
     b = best_of(b, x);
   }
-  __shared__ Best sb[kWarps];
-  __shared__ bool last;
+  __syncthreads();
   if (lane_id() == 0) sb[threadIdx.x >> 5] = b;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1095,14 +1132,13 @@ __global__ void __launch_bounds__(kThreads) k_argmax(const double* __restrict__ 
     ra.blk_score[blockIdx.x] = t.s;
     ra.blk_arg[blockIdx.x] = t.v;
     ra.blk_min[blockIdx.x] = t.minu;
-    __threadfence();
-    last = atomicAdd(&ra.ctl->argmax_done, 1u) == gridDim.x - 1;
   }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
+}
+
+// Combine nblk partials (one block): choice, committed mark, saturation.
+__device__ __forceinline__ void argmax_finish(uint32_t nblk, const RunArrays& ra, Best* sb) {
   Best t{0.0, 0xFFFFFFFFu, 0xFFFFFFFFu};
-  for (uint32_t k = threadIdx.x; k < gridDim.x; k += blockDim.x)
+  for (uint32_t k = threadIdx.x; k < nblk; k += blockDim.x)
     t = best_of(t, Best{__ldcg(ra.blk_score + k), __ldcg(ra.blk_arg + k), __ldcg(ra.blk_min + k)});
   for (int o = 16; o; o >>= 1) {
     Best x{__shfl_xor_sync(0xffffffffu, t.s, o), __shfl_xor_sync(0xffffffffu, t.v, o),
@@ -1124,6 +1160,21 @@ __global__ void __launch_bounds__(kThreads) k_argmax(const double* __restrict__ 
     ra.committed[choice] = 1;
     ra.ctl->argmax_done = 0;
   }
+}
+
+__global__ void __launch_bounds__(kThreads) k_argmax(const double* __restrict__ scores,
+                                                     uint32_t n, RunArrays ra) {
+  __shared__ Best sb[kWarps];
+  __shared__ bool last;
+  argmax_partial(scores, n, ra, sb);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&ra.ctl->argmax_done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  argmax_finish(gridDim.x, ra, sb);
 }
 
 // ---------------------------------------------------------------- cascade
@@ -1150,11 +1201,16 @@ __device__ __forceinline__ void clear_rows(uint32_t* f, const uint32_t* rows, un
 // VISITED_j(v) <=> v reachable from a committed seed in sample j.  One grid
 // barrier per level: level L reads fresh[L%3], writes fresh[(L+1)%3] and
 // clears the rows of level L-1 in fresh[(L+2)%3]; queues rotate mod 4.
-__global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
-  __shared__ WarpStage stage[kWarps];
-  __shared__ unsigned long long s_release;
-  cg::grid_group grid = cg::this_grid();
-  const RankDev& r = a.r;
+struct CasOpts {
+  const unsigned int* choice;
+  uint32_t seed;
+  int dbg;
+  int pull_f;
+};
+
+__device__ __forceinline__ void cascade_body(const RankDev& r, const CasOpts& a,
+                                             cg::grid_group& grid, WarpStage* stage,
+                                             unsigned long long& s_release, uint32_t* cas_smem) {
   unsigned int* cnt = r.q.counts;
   const uint32_t base = ld_volatile(&r.ctl->tick);
   const unsigned lane = lane_id();
@@ -1163,7 +1219,6 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
   const uint32_t W32 = r.W32;
   WarpStage& ws = stage[threadIdx.x >> 5];
   unsigned long long marked = 0;
-  extern __shared__ uint32_t cas_smem[];
   const bool pull_ok = r.Jp <= kPullMaxJp;
   uint32_t* cacc = cas_smem + (threadIdx.x >> 5) * (kPullMaxJp / 32);
   if (pull_ok) {
@@ -1395,9 +1450,21 @@ __global__ void __launch_bounds__(kThreads) k_cascade(CasArgs a) {
   }
 }
 
+__global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_cascade(CasArgs a) {
+  __shared__ WarpStage stage[kWarps];
+  __shared__ unsigned long long s_release;
+  __shared__ RankDev s_r;
+  extern __shared__ unsigned long long dyn_smem[];
+  if (threadIdx.x == 0) s_r = a.r;
+  __syncthreads();
+  cg::grid_group grid = cg::this_grid();
+  const CasOpts o{a.choice, a.seed, a.dbg, a.pull_f};
+  cascade_body(s_r, o, grid, stage, s_release, reinterpret_cast<uint32_t*>(dyn_smem));
+}
+
 // ---------------------------------------------------------------- round end
-__global__ void k_round_end(RunArrays ra, RankCtl* const* ctls, uint32_t mu, uint32_t k,
-                            uint32_t R, double eps) {
+__device__ __forceinline__ void round_end_body(const RunArrays& ra, RankCtl* const* ctls,
+                                               uint32_t mu, uint32_t k, uint32_t R, double eps) {
   if (threadIdx.x || blockIdx.x) return;
   unsigned long long covered = 0;  // collectives.cpp:96-113 (exact u64 sum)
   for (uint32_t t = 0; t < mu; ++t) covered += ld_volatile(&ctls[t]->visited);
@@ -1417,7 +1484,131 @@ __global__ void k_round_end(RunArrays ra, RankCtl* const* ctls, uint32_t mu, uin
   c->step = step + 1;
 }
 
+__global__ void k_round_end(RunArrays ra, RankCtl* const* ctls, uint32_t mu, uint32_t k,
+                            uint32_t R, double eps) {
+  round_end_body(ra, ctls, mu, k, R, eps);
+}
+
 }  // namespace
+
+// ---------------------------------------------------------------- whole run
+// The greedy loop of proj/src/runtime.cpp:87-154 as ONE persistent
+// cooperative kernel: fill -> simulate -> score, then K rounds of rescore ->
+// (binomial sum) -> argmax -> commit+cascade -> covered count / rebuild
+// decision -> (fill -> simulate -> score).  Every decision is read by all
+// blocks after a grid barrier, so the host launches once per run.  Phase
+// times are accumulated by block 0 from the global nanosecond timer.
+struct RunArgs {
+  const RankDev* ranks;  // device array [mu]
+  uint32_t mu, k, R, n;
+  double eps;
+  int cap, dbg, sim_pull_f, cas_pull_f, K;
+  RunArrays ra;
+  const double* const* parts;
+  RankCtl* const* ctls;
+  double* reduced;
+  unsigned long long* phase_ns;  // fill, simulate, select, cascade
+};
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Out-of-line phase bodies keep the register allocation of each phase local.
+template <int JAC, int CNT>
+__device__ __noinline__ void run_simulate(const RankDev& r, const SimOpts& o, WarpStage* stage,
+                                          unsigned long long& s_release,
+                                          unsigned long long* dyn) {
+  cg::grid_group grid = cg::this_grid();
+  simulate_body<JAC, CNT>(r, o, grid, stage, s_release, dyn);
+}
+__device__ __noinline__ void run_cascade(const RankDev& r, const CasOpts& o, WarpStage* stage,
+                                         unsigned long long& s_release, uint32_t* dyn) {
+  cg::grid_group grid = cg::this_grid();
+  cascade_body(r, o, grid, stage, s_release, dyn);
+}
+
+template <int JAC, int CNT>
+__global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
+  __shared__ WarpStage stage[kWarps];
+  __shared__ unsigned long long s_release;
+  __shared__ RankDev s_r;
+  __shared__ Best sb[kWarps];
+  extern __shared__ unsigned long long dyn_smem[];
+  cg::grid_group grid = cg::this_grid();
+  const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
+  unsigned long long t0 = timer ? global_ns() : 0;
+  auto phase = [&](int which) {
+    if (timer) {
+      const unsigned long long t1 = global_ns();
+      a.phase_ns[which] += t1 - t0;
+      t0 = t1;
+    }
+  };
+  auto load_rank = [&](uint32_t t) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_r = a.ranks[t];
+    __syncthreads();
+  };
+  const SimOpts so{a.cap, a.dbg, a.sim_pull_f};
+  auto rebuild = [&]() {  // fill -> simulate -> full rescore, every partition
+    for (uint32_t t = 0; t < a.mu; ++t) {
+      load_rank(t);
+      fill_body(s_r.n, s_r.J, s_r.Jp, s_r.jkey, s_r.vis, s_r.regs, s_r.ctl);
+    }
+    grid.sync();
+    phase(0);
+    for (uint32_t t = 0; t < a.mu; ++t) {
+      load_rank(t);
+      run_simulate<JAC, CNT>(s_r, so, stage, s_release, dyn_smem);
+      grid.sync();
+    }
+    phase(1);
+    for (uint32_t t = 0; t < a.mu; ++t) {
+      load_rank(t);
+      score_body(s_r.regs, s_r.n, s_r.J, s_r.Jp, a.K, 1, s_r.dirty, s_r.ctl, s_r.scores);
+    }
+    grid.sync();
+  };
+  rebuild();
+  bool rebuilt = true;
+  const double* argsrc = a.mu > 1 ? a.reduced : a.ranks[0].scores;
+  for (uint32_t step = 0; step < a.k; ++step) {
+    if (!rebuilt) {  // rows dirtied by the last cascade
+      for (uint32_t t = 0; t < a.mu; ++t) {
+        load_rank(t);
+        score_body(s_r.regs, s_r.n, s_r.J, s_r.Jp, a.K, 0, s_r.dirty, s_r.ctl, s_r.scores);
+      }
+      grid.sync();
+    }
+    rebuilt = false;
+    if (a.mu > 1) {
+      treesum_body(a.parts, a.mu, a.n, a.reduced);
+      grid.sync();
+    }
+    argmax_partial(argsrc, a.n, a.ra, sb);
+    grid.sync();
+    if (blockIdx.x == 0) argmax_finish(gridDim.x, a.ra, sb);
+    grid.sync();
+    phase(2);
+    for (uint32_t t = 0; t < a.mu; ++t) {
+      load_rank(t);
+      const CasOpts co{&a.ra.ctl->choice, 0, a.dbg, a.cas_pull_f};
+      run_cascade(s_r, co, stage, s_release, reinterpret_cast<uint32_t*>(dyn_smem));
+      grid.sync();
+    }
+    round_end_body(a.ra, a.ctls, a.mu, a.k, a.R, a.eps);
+    grid.sync();
+    phase(3);
+    if (step + 1 < a.k && ld_volatile(&a.ra.ctl->rebuild_now)) {
+      rebuild();
+      phase(2);
+      rebuilt = true;
+    }
+  }
+}
 
 // ================================================================= launchers
 static unsigned long long g_launches = 0;
@@ -1577,22 +1768,29 @@ static const void* sim_kernel(int variant) {
   }
 }
 
+static const void* run_kernel(int variant) {
+  switch (variant) {
+    case 0: return (const void*)k_run<0, 0>;
+    case 1: return (const void*)k_run<1, 0>;
+    default: return (const void*)k_run<1, 1>;
+  }
+}
+
 int coop_grid(int which, int variant) {
-  static int g[4] = {0, 0, 0, 0};
-  const int slot = which == 0 ? variant : 3;
+  static int g[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const int slot = which == 0 ? variant : which == 1 ? 3 : 4 + variant;
   if (!g[slot]) {
     int per = 0;
-    const void* fn = which == 0 ? sim_kernel(variant) : (const void*)k_cascade;
-    if (which == 0)
-      DFS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSimSmem));
-    else
-      DFS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kCasSmem));
-    DFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kThreads,
-                                                           which == 0 ? kSimSmem : kCasSmem));
+    const void* fn = which == 0   ? sim_kernel(variant)
+                     : which == 1 ? (const void*)k_cascade
+                                  : run_kernel(variant);
+    const size_t smem = which == 1 ? kCasSmem : kSimSmem;
+    DFS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    DFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kThreads, smem));
     if (per < 1) per = 1;
     // Tunables (blocks per SM): a smaller cascade grid makes its per-level
     // grid barrier cheaper; frontiers there are usually small.
-    const char* env = getenv(which == 0 ? "DFS_SIM_BPS" : "DFS_CAS_BPS");
+    const char* env = getenv(which == 1 ? "DFS_CAS_BPS" : "DFS_SIM_BPS");
     int want = env ? atoi(env) : per;
     if (want >= 1 && want < per) per = want;
     g[slot] = per * num_sms();
@@ -1651,6 +1849,21 @@ void launch_round_end(RunArrays& ra, RankCtl* const* ctls_dev, uint32_t mu, uint
                       double eps, cudaStream_t s) {
   k_round_end<<<1, 32, 0, s>>>(ra, ctls_dev, mu, k, r, eps);
   DFS_CUDA(cudaGetLastError());
+  ++g_launches;
+}
+
+void launch_run(const RankDev* ranks_dev, uint32_t mu, uint32_t k, uint32_t R, uint32_t n,
+                double eps, int cap, int jacobi, int count, int K, RunArrays& ra,
+                const double* const* parts, RankCtl* const* ctls, double* reduced,
+                unsigned long long* phase_ns, cudaStream_t s) {
+  static const int dbg = getenv("DFS_DBG") ? atoi(getenv("DFS_DBG")) : 0;
+  static const int spf = getenv("DFS_SIM_PULL") ? atoi(getenv("DFS_SIM_PULL")) : 4;
+  static const int cpf = getenv("DFS_CAS_PULL") ? atoi(getenv("DFS_CAS_PULL")) : 8;
+  RunArgs a{ranks_dev, mu, k, R, n, eps, cap, dbg, spf, cpf, K, ra, parts, ctls, reduced, phase_ns};
+  void* args[] = {&a};
+  const int variant = jacobi ? (count ? 2 : 1) : 0;
+  DFS_CUDA(cudaLaunchCooperativeKernel(run_kernel(variant), dim3(coop_grid(2, variant)),
+                                       dim3(kThreads), args, kSimSmem, s));
   ++g_launches;
 }
 

@@ -309,7 +309,7 @@ Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
   ra.seeds = as<uint32_t>(arena_.get("run.seeds", k * 4));
   ra.traj = as<double>(arena_.get("run.traj", k * 8));
   ra.rebuild_rounds = as<uint32_t>(arena_.get("run.rb", k * 4));
-  ra.nblk = 4 * 148;
+  ra.nblk = 2048;  // >= any cooperative grid (argmax partials)
   ra.blk_score = as<double>(arena_.get("run.bs", ra.nblk * 8));
   ra.blk_arg = as<uint32_t>(arena_.get("run.ba", ra.nblk * 4));
   ra.blk_min = as<uint32_t>(arena_.get("run.bm", ra.nblk * 4));
@@ -350,38 +350,53 @@ Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
   };
   std::vector<Span> spans;
 
-  size_t e0 = mark();
-  for (uint32_t t = 0; t < mu; ++t) launch_fill(ranks_[t], nullptr, 0, s);
-  size_t e1 = mark();
-  for (uint32_t t = 0; t < mu; ++t) launch_simulate(ranks_[t], cfg.jacobi, cfg.count, cfg.sim_cap, nullptr, 0, s);
-  size_t e2 = mark();
-  for (uint32_t t = 0; t < mu; ++t) launch_score(ranks_[t], 1, nullptr, 0, s);
-  spans.push_back({e0, e1, &pt.fill});
-  spans.push_back({e1, e2, &pt.simulate, -1});
-  size_t prev = e2;
-  for (uint32_t step = 0; step < k; ++step) {
-    // select: rescore dirty rows, binomial-order sum, argmax (runtime.cpp:88-122)
-    for (uint32_t t = 0; t < mu; ++t) launch_score(ranks_[t], 0, rebuild, 0, s);
-    if (mu > 1) launch_treesum(dparts, mu, n, ra.reduced, s);
-    launch_argmax(argmax_src, ra, n, s);
-    size_t a = mark();
-    spans.push_back({prev, a, &pt.select});
-    // commit + cascade (runtime.cpp:124-127) and the covered-count allreduce
-    for (uint32_t t = 0; t < mu; ++t) launch_cascade(ranks_[t], &ra.ctl->choice, 0, s);
-    launch_round_end(ra, dctl, mu, k, cfg.r, cfg.rebuild_eps, s);
-    size_t b = mark();
-    spans.push_back({a, b, &pt.cascade});
-    prev = b;
-    if (step + 1 < k) {  // eps-gated rebuild (runtime.cpp:139-153), predicated on device
-      for (uint32_t t = 0; t < mu; ++t) launch_fill(ranks_[t], rebuild, 1, s);
-      size_t c = mark();
-      for (uint32_t t = 0; t < mu; ++t)
-        launch_simulate(ranks_[t], cfg.jacobi, cfg.count, cfg.sim_cap, rebuild, 1, s);
-      size_t d = mark();
-      for (uint32_t t = 0; t < mu; ++t) launch_score(ranks_[t], 1, rebuild, 1, s);
-      spans.push_back({b, c, &pt.fill});
-      spans.push_back({c, d, &pt.simulate, int(step)});
-      prev = d;
+  // Default: the whole loop as one persistent kernel (launch_run).
+  // DFS_RUN_MODE=launches selects the per-phase launch sequence (same results).
+  static const bool multi = getenv("DFS_RUN_MODE") && std::string(getenv("DFS_RUN_MODE")) == "launches";
+  unsigned long long* phase_ns = as<unsigned long long>(arena_.get("run.phase", 8 * 8));
+  if (!multi) {
+    int lj = 0;
+    while ((1u << lj) < ranks_[0].J) ++lj;
+    RankDev* dranks = as<RankDev>(arena_.get("run.ranks", mu * sizeof(RankDev)));
+    DFS_CUDA(cudaMemcpyAsync(dranks, ranks_.data(), mu * sizeof(RankDev), cudaMemcpyHostToDevice, s));
+    DFS_CUDA(cudaMemsetAsync(phase_ns, 0, 8 * 8, s));
+    mark();
+    launch_run(dranks, mu, k, cfg.r, n, cfg.rebuild_eps, cfg.sim_cap, cfg.jacobi, cfg.count, 53 - lj,
+               ra, dparts, dctl, ra.reduced, phase_ns, s);
+  } else {
+    size_t e0 = mark();
+    for (uint32_t t = 0; t < mu; ++t) launch_fill(ranks_[t], nullptr, 0, s);
+    size_t e1 = mark();
+    for (uint32_t t = 0; t < mu; ++t) launch_simulate(ranks_[t], cfg.jacobi, cfg.count, cfg.sim_cap, nullptr, 0, s);
+    size_t e2 = mark();
+    for (uint32_t t = 0; t < mu; ++t) launch_score(ranks_[t], 1, nullptr, 0, s);
+    spans.push_back({e0, e1, &pt.fill});
+    spans.push_back({e1, e2, &pt.simulate, -1});
+    size_t prev = e2;
+    for (uint32_t step = 0; step < k; ++step) {
+      // select: rescore dirty rows, binomial-order sum, argmax (runtime.cpp:88-122)
+      for (uint32_t t = 0; t < mu; ++t) launch_score(ranks_[t], 0, rebuild, 0, s);
+      if (mu > 1) launch_treesum(dparts, mu, n, ra.reduced, s);
+      launch_argmax(argmax_src, ra, n, s);
+      size_t a = mark();
+      spans.push_back({prev, a, &pt.select});
+      // commit + cascade (runtime.cpp:124-127) and the covered-count allreduce
+      for (uint32_t t = 0; t < mu; ++t) launch_cascade(ranks_[t], &ra.ctl->choice, 0, s);
+      launch_round_end(ra, dctl, mu, k, cfg.r, cfg.rebuild_eps, s);
+      size_t b = mark();
+      spans.push_back({a, b, &pt.cascade});
+      prev = b;
+      if (step + 1 < k) {  // eps-gated rebuild (runtime.cpp:139-153), predicated on device
+        for (uint32_t t = 0; t < mu; ++t) launch_fill(ranks_[t], rebuild, 1, s);
+        size_t c = mark();
+        for (uint32_t t = 0; t < mu; ++t)
+          launch_simulate(ranks_[t], cfg.jacobi, cfg.count, cfg.sim_cap, rebuild, 1, s);
+        size_t d = mark();
+        for (uint32_t t = 0; t < mu; ++t) launch_score(ranks_[t], 1, rebuild, 1, s);
+        spans.push_back({b, c, &pt.fill});
+        spans.push_back({c, d, &pt.simulate, int(step)});
+        prev = d;
+      }
     }
   }
   size_t eend = mark();
@@ -431,6 +446,16 @@ Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
   rep.reduced_elements = uint64_t(k) * (uint64_t(n) + 1) * (mu - 1);
   rep.broadcast_elements = uint64_t(k) * 2 * (mu - 1);
   rep.barriers = uint64_t(k) * (8 + ceil_log2(mu));
+  if (!multi) {
+    unsigned long long hp[4];
+    DFS_CUDA(cudaMemcpy(hp, phase_ns, sizeof hp, cudaMemcpyDeviceToHost));
+    pt.fill += hp[0] * 1e-9;
+    pt.simulate += hp[1] * 1e-9;
+    pt.select += hp[2] * 1e-9;
+    pt.cascade += hp[3] * 1e-9;
+    rep.sim_active = hp[1] * 1e-9;
+    rep.sim_launches = (1 + rep.rebuilds) * mu;
+  }
   for (const Span& sp : spans) {
     float ms = 0;
     DFS_CUDA(cudaEventElapsedTime(&ms, ev[sp.a], ev[sp.b]));
