@@ -48,6 +48,9 @@ struct DevGraph {
   uint32_t* indeg = nullptr;  // n
   uint64_t* toff = nullptr;   // n+1 (transpose offsets by v)
   uint32_t* tedge = nullptr;  // m   (edge ids sorted by (v, e))
+  uint32_t* tsrc = nullptr;   // m   transposed order: source u of position p
+  uint32_t* thash = nullptr;  // m   transposed order: edge hash
+  uint32_t* tdst = nullptr;   // m   transposed order: target v (row)
 };
 
 // One direction of the sampled ("device") graph as sparse 32-sim items:
@@ -109,6 +112,7 @@ struct RankDev {
   uint32_t j_offset = 0;
   uint64_t reg_key = 0;
   uint32_t* x = nullptr;          // Jp sorted slice values (pads 0xFFFFFFFF)
+  uint32_t* xlut = nullptr;       // 4097: first slot with x >= k << 19 (FASST windows)
   uint64_t* jkey = nullptr;       // Jp register hash keys
   int8_t* regs = nullptr;         // n*Jp
   int8_t* snap = nullptr;         // n*Jp (Jacobi schedule only)
@@ -163,9 +167,18 @@ void scan_u32_u64(const uint32_t* in, uint64_t* out, uint64_t n, void* tmp, size
 // Sampled-item construction for one rank and direction (dir 0 = by source u
 // over the CSR, dir 1 = by target v over the transpose).  write = 0 counts
 // items per edge position into cnt; write = 1 emits them at pos_off.
-void launch_items_pass(const DevGraph& g, const uint32_t* w, const RankDev& r, int dir,
-                       int fasst, int write, uint32_t* cnt, const uint64_t* pos_off,
+void launch_items_pass(const DevGraph& g, const uint32_t* w, const uint32_t* tw, const RankDev& r,
+                       int dir, int fasst, int write, uint32_t* cnt, const uint64_t* pos_off,
                        Items& it, cudaStream_t s);
+// Weights in transposed order (kind 0 const, 1 wc, 2 gather of w).
+void launch_tweights(const DevGraph& g, int kind, uint32_t W, const uint32_t* w, uint32_t* tw,
+                     cudaStream_t s);
+// Reverse items from forward items (no sampling recomputation).
+void launch_xlut(const RankDev& r, cudaStream_t s);
+void launch_rev_counts(const DevGraph& g, const uint32_t* cnt_f, uint32_t* cnt_r, cudaStream_t s);
+void launch_rev_copy(const DevGraph& g, const uint32_t* cnt_f, const uint32_t* cnt_r,
+                     const uint64_t* pos_f, const uint64_t* pos_r, const Items& f, Items& rv,
+                     cudaStream_t s);
 // row_off[r] = pos_off[graph row start]; then per-row chunk counts.
 void launch_row_offsets(const DevGraph& g, int dir, const uint64_t* pos_off, Items& it,
                         uint32_t* row_cnt, cudaStream_t s);

@@ -126,8 +126,21 @@ __global__ void k_weights(uint64_t m, int kind, uint32_t W, const uint32_t* __re
 // with h on all bits above floor(log2 W), i.e. x lies in one aligned block of
 // size 2^(floor(log2 W)+1) around h; sorted order turns
 // that block into the contiguous slot range [lo, hi).
-__device__ __forceinline__ void edge_window(const uint32_t* sx, uint32_t J, uint32_t h,
-                                            uint32_t W, int fasst, uint32_t& lo, uint32_t& hi) {
+constexpr int kLutBits = 12;                 // slot LUT over the top 12 bits of x
+constexpr int kLutShift = 31 - kLutBits;     // 2^19-wide x buckets
+
+__device__ __forceinline__ uint32_t lower_bound_x(const uint32_t* sx, uint32_t J, uint64_t key) {
+  uint32_t a = 0, z = J;
+  while (a < z) {
+    const uint32_t mid = (a + z) >> 1;
+    if (uint64_t(sx[mid]) < key) a = mid + 1; else z = mid;
+  }
+  return a;
+}
+
+__device__ __forceinline__ void edge_window(const uint32_t* sx, const uint32_t* lut, uint32_t J,
+                                            uint32_t h, uint32_t W, int fasst, uint32_t& lo,
+                                            uint32_t& hi) {
   if (!fasst) {
     lo = 0;
     hi = J;
@@ -135,53 +148,55 @@ __device__ __forceinline__ void edge_window(const uint32_t* sx, uint32_t J, uint
   }
   const int b = 31 - __clz(W);  // W >= 1
   const uint64_t span = uint64_t(1) << (b + 1);
-  const uint64_t lx = (uint64_t(h) / span) * span;
+  const uint64_t lx = uint64_t(h) & ~(span - 1);
   const uint64_t hx = lx + span;  // exclusive
-  uint32_t a = 0, z = J;          // lower_bound(lx)
-  while (a < z) {
-    uint32_t mid = (a + z) >> 1;
-    if (uint64_t(sx[mid]) < lx) a = mid + 1; else z = mid;
+  if (b + 1 >= kLutShift) {       // block boundaries are LUT bucket boundaries: exact
+    lo = lut[lx >> kLutShift];
+    hi = (hx >> kLutShift) > (1u << kLutBits) ? J : lut[hx >> kLutShift];
+  } else {
+    lo = lower_bound_x(sx, J, lx);
+    hi = lower_bound_x(sx, J, hx);
   }
-  lo = a;
-  z = J;  // lower_bound(hx)
-  while (a < z) {
-    uint32_t mid = (a + z) >> 1;
-    if (uint64_t(sx[mid]) < hx) a = mid + 1; else z = mid;
-  }
-  hi = a;
 }
 
 // dir 0: positions = CSR edges (row = src u, other = adj v)
 // dir 1: positions = transpose (edge = tedge[p], row = adj v, other = src u)
+// Positions are edges in CSR order (dir 0: row = source u, other = target v)
+// or in transposed order (dir 1: row = v, other = u); every input array is
+// indexed by position, so both directions stream coalesced.
 template <int WRITE>
-__global__ void k_items(uint64_t npos, int dir, const uint32_t* __restrict__ tedge,
-                        const uint32_t* __restrict__ adj, const uint32_t* __restrict__ src,
-                        const uint32_t* __restrict__ ehash, const uint32_t* __restrict__ w,
-                        const uint32_t* __restrict__ x, uint32_t J, uint32_t Jp, int fasst,
-                        uint32_t* __restrict__ cnt, const uint64_t* __restrict__ pos_off,
-                        uint32_t* __restrict__ it_other, uint32_t* __restrict__ it_mask,
-                        uint8_t* __restrict__ it_batch, uint32_t* __restrict__ it_row) {
+__global__ void k_items(uint64_t npos, const uint32_t* __restrict__ p_hash,
+                        const uint32_t* __restrict__ p_w, const uint32_t* __restrict__ p_other,
+                        const uint32_t* __restrict__ p_row, const uint32_t* __restrict__ x,
+                        uint32_t J, uint32_t Jp, int fasst, uint32_t* __restrict__ cnt,
+                        const uint64_t* __restrict__ pos_off, uint32_t* __restrict__ it_other,
+                        uint32_t* __restrict__ it_mask, uint8_t* __restrict__ it_batch,
+                        uint32_t* __restrict__ it_row, const uint32_t* __restrict__ glut) {
   extern __shared__ uint32_t sx[];
+  uint32_t* lut = sx + Jp;  // lut[k] = lower_bound(x, k << kLutShift), k in [0, 2^kLutBits]
   for (uint32_t i = threadIdx.x; i < Jp; i += blockDim.x) sx[i] = x[i];
+  __syncthreads();
+  if (fasst)
+    for (uint32_t k = threadIdx.x; k <= (1u << kLutBits); k += blockDim.x) lut[k] = glut[k];
   __syncthreads();
   for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < npos;
        p += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t e = dir ? tedge[p] : uint32_t(p);
-    const uint32_t W = w[e];
+    const uint32_t W = p_w[p];
     uint32_t c = 0;
     if (W != 0) {  // fasst.cpp:71 — W = 0 never samples
-      const uint32_t h = ehash[e];
+      const uint32_t h = p_hash[p];
       uint32_t lo, hi;
-      edge_window(sx, J, h, W, fasst, lo, hi);
+      edge_window(sx, lut, J, h, W, fasst, lo, hi);
       if (hi > lo) {
         uint64_t o = WRITE ? pos_off[p] : 0;
-        const uint32_t other = WRITE ? (dir ? src[e] : adj[e]) : 0;
-        const uint32_t rowv = WRITE ? (dir ? adj[e] : src[e]) : 0;
+        const uint32_t other = WRITE ? p_other[p] : 0;
+        const uint32_t rowv = WRITE ? p_row[p] : 0;
         for (uint32_t b = lo >> 5; b <= (hi - 1) >> 5; ++b) {
+          // only slots inside the window can pass the test
           uint32_t mk = 0;
-          const uint32_t* xb = sx + b * 32;
-#pragma unroll 8
-          for (int i = 0; i < 32; ++i) mk |= uint32_t((xb[i] ^ h) < W) << i;  // sampling.hpp:37-39
+          const uint32_t i0 = max(lo, b * 32), i1 = min(hi, b * 32 + 32);
+          for (uint32_t i = i0; i < i1; ++i)
+            mk |= uint32_t((sx[i] ^ h) < W) << (i - b * 32);  // sampling.hpp:37-39
           if (mk) {
             if (WRITE) {
               it_other[o] = other;
@@ -197,6 +212,81 @@ __global__ void k_items(uint64_t npos, int dir, const uint32_t* __restrict__ ted
     }
     if (!WRITE) cnt[p] = c;
   }
+}
+
+// Reverse items are the forward items of each edge re-keyed by target:
+// rev count of transposed position p = fwd count of edge tedge[p].
+__global__ void k_xlut(const uint32_t* __restrict__ x, uint32_t J, uint32_t* __restrict__ lut) {
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k <= (1u << kLutBits);
+       k += gridDim.x * blockDim.x)
+    lut[k] = lower_bound_x(x, J, uint64_t(k) << kLutShift);
+}
+
+__global__ void k_gather_cnt(uint64_t m, const uint32_t* __restrict__ tedge,
+                             const uint32_t* __restrict__ cnt_f, uint32_t* __restrict__ cnt_r) {
+  for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < m;
+       p += uint64_t(gridDim.x) * blockDim.x)
+    cnt_r[p] = cnt_f[tedge[p]];
+}
+
+// Output-ordered (coalesced writes): transposed position p holds edge
+// tedge[p]; its forward items are gathered from pos_f[e].
+__global__ void k_rev_copy(uint64_t m, const uint32_t* __restrict__ tedge,
+                           const uint32_t* __restrict__ cnt_r, const uint64_t* __restrict__ pos_f,
+                           const uint64_t* __restrict__ pos_r, const uint32_t* __restrict__ f_row,
+                           const uint32_t* __restrict__ f_other, const uint32_t* __restrict__ f_mask,
+                           const uint8_t* __restrict__ f_batch, uint32_t* __restrict__ r_row,
+                           uint32_t* __restrict__ r_other, uint32_t* __restrict__ r_mask,
+                           uint8_t* __restrict__ r_batch) {
+  for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < m;
+       p += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t c = cnt_r[p];
+    if (!c) continue;
+    const uint64_t src = pos_f[tedge[p]], dst = pos_r[p];
+    for (uint32_t k = 0; k < c; ++k) {
+      r_row[dst + k] = f_other[src + k];   // row of a reverse item: target v
+      r_other[dst + k] = f_row[src + k];   // other: source u
+      r_mask[dst + k] = f_mask[src + k];
+      r_batch[dst + k] = f_batch[src + k];
+    }
+  }
+}
+
+__global__ void k_transpose_fields(uint64_t m, const uint32_t* __restrict__ tedge,
+                                   const uint32_t* __restrict__ src,
+                                   const uint32_t* __restrict__ adj,
+                                   const uint32_t* __restrict__ ehash, uint32_t* __restrict__ tsrc,
+                                   uint32_t* __restrict__ thash, uint32_t* __restrict__ tdst) {
+  for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < m;
+       p += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t e = tedge[p];
+    tsrc[p] = src[e];
+    thash[p] = ehash[e];
+    tdst[p] = adj[e];
+  }
+}
+
+// Weights in transposed order: const / wc from the target's in-degree, or a
+// gather of host-assigned weights.
+__global__ void k_tweights(uint64_t m, const uint32_t* __restrict__ tedge,
+                           const uint32_t* __restrict__ tdst, int kind, uint32_t W,
+                           const uint32_t* __restrict__ indeg, const uint32_t* __restrict__ w,
+                           uint32_t* __restrict__ tw) {
+  for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < m;
+       p += uint64_t(gridDim.x) * blockDim.x) {
+    uint32_t wv = W;
+    if (kind == 1)
+      wv = uint32_t(llround(__dmul_rn(__ddiv_rn(1.0, double(indeg[tdst[p]])), 2147483648.0)));
+    else if (kind == 2)
+      wv = w[tedge[p]];
+    tw[p] = wv;
+  }
+}
+
+__global__ void k_inverse(uint64_t m, const uint32_t* __restrict__ perm, uint32_t* __restrict__ inv) {
+  for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < m;
+       p += uint64_t(gridDim.x) * blockDim.x)
+    inv[perm[p]] = uint32_t(p);
 }
 
 __global__ void k_row_offsets(uint32_t n, const uint64_t* __restrict__ graph_off,
@@ -1677,11 +1767,23 @@ void launch_graph_prepare(DevGraph& g, void* tmp, size_t tmp_bytes, cudaStream_t
     size_t bytes = cub_bytes;
     DFS_CUDA(cub::DeviceRadixSort::SortPairs(cubtmp, bytes, g.adj, keys_out, iota, g.tedge, m, 0,
                                              end_bit, s));
+
   }
   // toff = exclusive scan of in-degrees (indeg[n] == 0 by the memset above)
   size_t bytes = cub_bytes;
   DFS_CUDA(cub::DeviceScan::ExclusiveScan(cubtmp, bytes, g.indeg, g.toff,
                                           cuda::std::plus<uint64_t>{}, uint64_t(0), g.n + 1, s));
+  if (m)
+    k_transpose_fields<<<grid_for(m), kThreads, 0, s>>>(m, g.tedge, g.src, g.adj, g.ehash, g.tsrc,
+                                                       g.thash, g.tdst);
+  DFS_CUDA(cudaGetLastError());
+  ++g_launches;
+}
+
+void launch_tweights(const DevGraph& g, int kind, uint32_t W, const uint32_t* w, uint32_t* tw,
+                     cudaStream_t s) {
+  if (!g.m) return;
+  k_tweights<<<grid_for(g.m), kThreads, 0, s>>>(g.m, g.tedge, g.tdst, kind, W, g.indeg, w, tw);
   DFS_CUDA(cudaGetLastError());
   ++g_launches;
 }
@@ -1693,26 +1795,53 @@ void launch_weights(const DevGraph& g, int kind, uint32_t W, uint32_t* w, cudaSt
   ++g_launches;
 }
 
-void launch_items_pass(const DevGraph& g, const uint32_t* w, const RankDev& r, int dir, int fasst,
-                       int write, uint32_t* cnt, const uint64_t* pos_off, Items& it,
-                       cudaStream_t s) {
+void launch_items_pass(const DevGraph& g, const uint32_t* w, const uint32_t* tw, const RankDev& r,
+                       int dir, int fasst, int write, uint32_t* cnt, const uint64_t* pos_off,
+                       Items& it, cudaStream_t s) {
   if (!g.m) return;
-  const size_t smem = size_t(r.Jp) * sizeof(uint32_t);
+  const size_t smem = (size_t(r.Jp) + (1u << kLutBits) + 1) * sizeof(uint32_t);
   static bool attr = false;
   if (!attr) {
     DFS_CUDA(cudaFuncSetAttribute(k_items<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
     DFS_CUDA(cudaFuncSetAttribute(k_items<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
     attr = true;
   }
-  const int grid = grid_for(g.m);
+  const uint32_t* ph = dir ? g.thash : g.ehash;
+  const uint32_t* pw = dir ? tw : w;
+  const uint32_t* po = dir ? g.tsrc : g.adj;
+  const uint32_t* pr = dir ? g.tdst : g.src;
+  const int grid = grid_for(g.m, kThreads * 4);  // fewer, longer-lived blocks (smem fill)
   if (write)
-    k_items<1><<<grid, kThreads, smem, s>>>(g.m, dir, g.tedge, g.adj, g.src, g.ehash, w, r.x, r.J,
-                                            r.Jp, fasst, cnt, pos_off, it.other, it.mask,
-                                            it.batch, it.row);
+    k_items<1><<<grid, kThreads, smem, s>>>(g.m, ph, pw, po, pr, r.x, r.J, r.Jp, fasst, cnt, pos_off,
+                                            it.other, it.mask, it.batch, it.row, r.xlut);
   else
-    k_items<0><<<grid, kThreads, smem, s>>>(g.m, dir, g.tedge, g.adj, g.src, g.ehash, w, r.x, r.J,
-                                            r.Jp, fasst, cnt, pos_off, nullptr, nullptr, nullptr,
-                                            nullptr);
+    k_items<0><<<grid, kThreads, smem, s>>>(g.m, ph, pw, po, pr, r.x, r.J, r.Jp, fasst, cnt, pos_off,
+                                            nullptr, nullptr, nullptr, nullptr, r.xlut);
+  DFS_CUDA(cudaGetLastError());
+  ++g_launches;
+}
+
+void launch_xlut(const RankDev& r, cudaStream_t s) {
+  k_xlut<<<(((1u << kLutBits) + 1) + kThreads - 1) / kThreads, kThreads, 0, s>>>(r.x, r.J, r.xlut);
+  DFS_CUDA(cudaGetLastError());
+  ++g_launches;
+}
+
+void launch_rev_counts(const DevGraph& g, const uint32_t* cnt_f, uint32_t* cnt_r, cudaStream_t s) {
+  if (!g.m) return;
+  k_gather_cnt<<<grid_for(g.m), kThreads, 0, s>>>(g.m, g.tedge, cnt_f, cnt_r);
+  DFS_CUDA(cudaGetLastError());
+  ++g_launches;
+}
+
+void launch_rev_copy(const DevGraph& g, const uint32_t* cnt_f, const uint32_t* cnt_r_,
+                     const uint64_t* pos_f, const uint64_t* pos_r, const Items& f, Items& rv,
+                     cudaStream_t s) {
+  if (!g.m) return;
+  (void)cnt_f;
+  k_rev_copy<<<grid_for(g.m), kThreads, 0, s>>>(g.m, g.tedge, cnt_r_, pos_f, pos_r, f.row,
+                                                f.other, f.mask, f.batch, rv.row, rv.other,
+                                                rv.mask, rv.batch);
   DFS_CUDA(cudaGetLastError());
   ++g_launches;
 }

@@ -105,6 +105,9 @@ void Context::upload(const HostGraph& hg) {
   g_.indeg = as<uint32_t>(arena_.get("g.indeg", n1 * 4));
   g_.toff = as<uint64_t>(arena_.get("g.toff", n1 * 8));
   g_.tedge = as<uint32_t>(arena_.get("g.tedge", m * 4));
+  g_.tsrc = as<uint32_t>(arena_.get("g.tsrc", m * 4));
+  g_.thash = as<uint32_t>(arena_.get("g.thash", m * 4));
+  g_.tdst = as<uint32_t>(arena_.get("g.tdst", m * 4));
   DFS_CUDA(cudaMemcpyAsync(g_.off, hg.offsets.data(), n1 * 8, cudaMemcpyHostToDevice, stream_));
   if (hg.m)
     DFS_CUDA(cudaMemcpyAsync(g_.adj, hg.adj.data(), hg.m * 4, cudaMemcpyHostToDevice, stream_));
@@ -127,6 +130,7 @@ void Context::alloc_rank(RankDev& r, uint32_t tau) {
   r.j_offset = tau * r.J;
   r.reg_key = derive_seed(cfg_.seed, kSeedTagRegisters);
   r.x = as<uint32_t>(arena_.get(p + "x", r.Jp * 4));
+  r.xlut = as<uint32_t>(arena_.get(p + "xlut", 4100 * 4));
   r.jkey = as<uint64_t>(arena_.get(p + "jkey", r.Jp * 8));
   r.regs = as<int8_t>(arena_.get(p + "regs", nn * r.Jp));
   r.snap = cfg_.jacobi ? as<int8_t>(arena_.get(p + "snap", nn * r.Jp)) : nullptr;
@@ -152,32 +156,20 @@ void Context::alloc_rank(RankDev& r, uint32_t tau) {
   }
   DFS_CUDA(cudaMemcpyAsync(r.x, xs.data(), r.Jp * 4, cudaMemcpyHostToDevice, stream_));
   DFS_CUDA(cudaMemcpyAsync(r.jkey, jk.data(), r.Jp * 8, cudaMemcpyHostToDevice, stream_));
+  launch_xlut(r, stream_);
   sync();  // host staging vectors go out of scope
 }
 
-void Context::build_items(RankDev& r, int dir) {
+// Chunk headers, small/big split and small-item list of one direction
+// (row offsets come from the per-position item offsets `pos`).
+void Context::finish_items(RankDev& r, int dir, const uint64_t* pos) {
   const std::string p = "r" + std::to_string(r.tau) + (dir ? ".rev." : ".fwd.");
   Items& it = dir ? r.rev : r.fwd;
-  const uint64_t m = g_.m;
   const uint32_t n = g_.n;
-  uint32_t* cnt = as<uint32_t>(arena_.get("tmp.cnt", (std::max<uint64_t>(m, n) + 2) * 4));
-  uint64_t* pos = as<uint64_t>(arena_.get("tmp.pos", (m + 2) * 8));
-  const size_t sb = scan_tmp_bytes(std::max<uint64_t>(m, n) + 2);
+  const size_t sb = scan_tmp_bytes(std::max<uint64_t>(g_.m, n) + 2);
   void* stmp = arena_.get("tmp.scan", sb);
-  DFS_CUDA(cudaMemsetAsync(cnt, 0, (m + 1) * 4, stream_));
-  launch_items_pass(g_, w_, r, dir, cfg_.fasst ? 1 : 0, 0, cnt, nullptr, it, stream_);
-  scan_u32_u64(cnt, pos, m, stmp, sb, stream_);
-  DFS_CUDA(cudaMemcpyAsync(&it.count, pos + m, 8, cudaMemcpyDeviceToHost, stream_));
-  sync();
-  const size_t ic = std::max<uint64_t>(it.count, 1);
-  it.other = as<uint32_t>(arena_.get(p + "other", ic * 4));
-  it.row = as<uint32_t>(arena_.get(p + "row", ic * 4));
-  it.mask = as<uint32_t>(arena_.get(p + "mask", ic * 4));
-  it.batch = as<uint8_t>(arena_.get(p + "batch", ic));
   it.row_off = as<uint64_t>(arena_.get(p + "row_off", (size_t(n) + 1) * 8));
-  launch_items_pass(g_, w_, r, dir, cfg_.fasst ? 1 : 0, 1, cnt, pos, it, stream_);
-  // per-row chunk counts (reuse cnt as row_cnt, n+1 entries with [n] = 0)
-  uint32_t* row_cnt = cnt;
+  uint32_t* row_cnt = as<uint32_t>(arena_.get("tmp.rowcnt", (size_t(n) + 2) * 4));
   DFS_CUDA(cudaMemsetAsync(row_cnt, 0, (size_t(n) + 1) * 4, stream_));
   launch_row_offsets(g_, dir, pos, it, row_cnt, stream_);
   uint64_t* row_chunk64 = as<uint64_t>(arena_.get("tmp.rowchunk", (size_t(n) + 2) * 8));
@@ -191,22 +183,61 @@ void Context::build_items(RankDev& r, int dir) {
   launch_chunk_write(n, it, row_chunk64, stream_);
   it.small = as<uint32_t>(arena_.get(p + "small", std::max<uint64_t>(it.chunks, 1) * 4));
   it.big = as<uint32_t>(arena_.get(p + "big", std::max<uint64_t>(it.chunks, 1) * 4));
-  unsigned int* c2 = as<unsigned int>(arena_.get("tmp.split", 16));
-  DFS_CUDA(cudaMemsetAsync(c2, 0, 8, stream_));
+  it.small_items = as<uint32_t>(arena_.get(p + "small_items", std::max<uint64_t>(it.count, 1) * 4));
+  unsigned int* c2 = as<unsigned int>(arena_.get("tmp.split", 32));
+  DFS_CUDA(cudaMemsetAsync(c2, 0, 32, stream_));
   launch_split_chunks(it, c2, stream_);
   unsigned int hc[2];
   DFS_CUDA(cudaMemcpyAsync(hc, c2, 8, cudaMemcpyDeviceToHost, stream_));
   sync();
   it.nsmall = hc[0];
   it.nbig = hc[1];
-  it.small_items = as<uint32_t>(arena_.get(p + "small_items", std::max<uint64_t>(it.count, 1) * 4));
-  unsigned long long* c3 = as<unsigned long long>(arena_.get("tmp.split64", 16));
-  DFS_CUDA(cudaMemsetAsync(c3, 0, 8, stream_));
+  unsigned long long* c3 = reinterpret_cast<unsigned long long*>(c2 + 4);
   launch_small_items(it, c3, stream_);
   unsigned long long hn = 0;
   DFS_CUDA(cudaMemcpyAsync(&hn, c3, 8, cudaMemcpyDeviceToHost, stream_));
   sync();
   it.nsmall_items = hn;
+}
+
+// Sampled items of one partition: forward items by evaluating the sampling
+// test once per (edge, batch) inside each edge's FASST window, then the
+// reverse items by re-keying the forward ones through the transpose.
+void Context::build_items(RankDev& r) {
+  const std::string p = "r" + std::to_string(r.tau) + ".";
+  const uint64_t m = g_.m;
+  const uint32_t n = g_.n;
+  uint32_t* cnt_f = as<uint32_t>(arena_.get("tmp.cntf", (m + 2) * 4));
+  uint32_t* cnt_r = as<uint32_t>(arena_.get("tmp.cntr", (m + 2) * 4));
+  uint64_t* pos_f = as<uint64_t>(arena_.get("tmp.posf", (m + 2) * 8));
+  uint64_t* pos_r = as<uint64_t>(arena_.get("tmp.posr", (m + 2) * 8));
+  const size_t sb = scan_tmp_bytes(std::max<uint64_t>(m, n) + 2);
+  void* stmp = arena_.get("tmp.scan", sb);
+  Items& f = r.fwd;
+  Items& rv = r.rev;
+  DFS_CUDA(cudaMemsetAsync(cnt_f, 0, (m + 1) * 4, stream_));
+  DFS_CUDA(cudaMemsetAsync(cnt_r, 0, (m + 1) * 4, stream_));
+  const int fa = cfg_.fasst ? 1 : 0;
+  launch_items_pass(g_, w_, tw_, r, 0, fa, 0, cnt_f, nullptr, f, stream_);
+  launch_items_pass(g_, w_, tw_, r, 1, fa, 0, cnt_r, nullptr, rv, stream_);
+  scan_u32_u64(cnt_f, pos_f, m, stmp, sb, stream_);
+  scan_u32_u64(cnt_r, pos_r, m, stmp, sb, stream_);
+  DFS_CUDA(cudaMemcpyAsync(&f.count, pos_f + m, 8, cudaMemcpyDeviceToHost, stream_));
+  sync();
+  rv.count = f.count;
+  const size_t ic = std::max<uint64_t>(f.count, 1);
+  for (int d = 0; d < 2; ++d) {
+    Items& it = d ? rv : f;
+    const std::string q = p + (d ? "rev." : "fwd.");
+    it.other = as<uint32_t>(arena_.get(q + "other", ic * 4));
+    it.row = as<uint32_t>(arena_.get(q + "row", ic * 4));
+    it.mask = as<uint32_t>(arena_.get(q + "mask", ic * 4));
+    it.batch = as<uint8_t>(arena_.get(q + "batch", ic));
+  }
+  launch_items_pass(g_, w_, tw_, r, 0, fa, 1, cnt_f, pos_f, f, stream_);
+  launch_items_pass(g_, w_, tw_, r, 1, fa, 1, cnt_r, pos_r, rv, stream_);
+  finish_items(r, 0, pos_f);
+  finish_items(r, 1, pos_r);
 }
 
 void Context::reset_rank_state(RankDev& r) {
@@ -259,16 +290,22 @@ void Context::prepare(const RunConfig& cfg, const HostGraph* host_w_src, uint32_
   for (uint32_t i = 0; i < cfg.r; ++i) x_[i] = x[order_[i]];
   // ---- weights (apply_weights, runtime.cpp:15-17)
   w_ = as<uint32_t>(arena_.get("g.w", std::max<uint64_t>(g_.m, 1) * 4));
+  tw_ = as<uint32_t>(arena_.get("g.tw", std::max<uint64_t>(g_.m, 1) * 4));
   switch (cfg.weights.kind) {
     case WeightKind::Constant:
       launch_weights(g_, 0, to_fixed_point(cfg.weights.a), w_, stream_);
+      launch_tweights(g_, 0, to_fixed_point(cfg.weights.a), w_, tw_, stream_);
       break;
-    case WeightKind::WeightedCascade: launch_weights(g_, 1, 0, w_, stream_); break;
+    case WeightKind::WeightedCascade:
+      launch_weights(g_, 1, 0, w_, stream_);
+      launch_tweights(g_, 1, 0, w_, tw_, stream_);
+      break;
     default: {
       if (!host_w_src) throw Error(kRuntime, "randomized weights need the host graph");
       std::vector<uint32_t> hw;
       assign_weights(*host_w_src, cfg.weights, derive_seed(cfg.seed, kSeedTagWeights), hw);
       DFS_CUDA(cudaMemcpyAsync(w_, hw.data(), g_.m * 4, cudaMemcpyHostToDevice, stream_));
+      launch_tweights(g_, 2, 0, w_, tw_, stream_);
       sync();
     }
   }
@@ -281,8 +318,7 @@ void Context::prepare(const RunConfig& cfg, const HostGraph* host_w_src, uint32_
   for (uint32_t t = 0; t < count; ++t) {
     RankDev& r = ranks_[t];
     alloc_rank(r, first + t);
-    build_items(r, 0);
-    build_items(r, 1);
+    build_items(r);
     const std::string p = "r" + std::to_string(first + t) + ".q.";
     const uint64_t cap = std::max<uint64_t>(std::max(r.fwd.chunks, r.rev.chunks), 1);
     for (int gi = 0; gi < kGens; ++gi) {

@@ -115,7 +115,8 @@ class Context {
   void sync();
 
  private:
-  void build_items(RankDev& r, int dir);
+  void build_items(RankDev& r);
+  void finish_items(RankDev& r, int dir, const uint64_t* pos);
   void alloc_rank(RankDev& r, uint32_t tau);
   void reset_rank_state(RankDev& r);
 
@@ -124,7 +125,8 @@ class Context {
   Arena arena_;
   DevGraph g_{};
   std::vector<uint64_t> orig_id_;
-  uint32_t* w_ = nullptr;  // weights of the prepared config
+  uint32_t* w_ = nullptr;   // weights of the prepared config (CSR order)
+  uint32_t* tw_ = nullptr;  // the same in transposed order
   RunConfig cfg_{};
   std::vector<uint32_t> x_, order_;
   bool degraded_ = false;
