@@ -116,6 +116,7 @@ struct RankDev {
   uint64_t* jkey = nullptr;       // Jp register hash keys
   int8_t* regs = nullptr;         // n*Jp
   int8_t* snap = nullptr;         // n*Jp (Jacobi schedule only)
+  int8_t* pristine = nullptr;     // n*Jp cached first fill (rebuilds copy it), optional
   uint32_t* vis = nullptr;        // n*W32 visited bitset
   uint32_t* fresh[3] = {nullptr, nullptr, nullptr};  // n*W32 cascade frontier bits
   uint32_t* lstamp = nullptr;     // n  queue-membership stamps
@@ -188,7 +189,8 @@ void launch_split_chunks(Items& it, unsigned int* cnt2, cudaStream_t s);
 // it.small_items <- item indices of the chunks in it.small (count in *cnt).
 void launch_small_items(Items& it, unsigned long long* cnt, cudaStream_t s);
 // Fill registers (VISITED kept, pads VISITED).  gate: run only if *gate == want.
-void launch_fill(const RankDev& r, const unsigned int* gate, unsigned int want, cudaStream_t s);
+void launch_fill(const RankDev& r, const unsigned int* gate, unsigned int want, cudaStream_t s,
+                 bool use_pristine = false);
 // Persistent cooperative simulate to convergence.  jacobi != 0 reproduces the
 // reference's snapshot schedule exactly (same sweep count); count != 0 (with
 // jacobi) also tallies the reference-schedule work units E/B/T/L.

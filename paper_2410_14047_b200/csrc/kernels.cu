@@ -380,39 +380,59 @@ __global__ void k_small_items(uint32_t nsmall, const uint32_t* __restrict__ smal
 // ---------------------------------------------------------------- fill
 // sketch.cpp:55-66: M[u][j] = clz64(fmix64(jkey[j] + u*golden)) unless VISITED.
 // One thread per 4 registers (one u32 store, coalesced across the warp).
+// use_pristine: registers are the cached first fill with VISITED re-applied
+// (fill values depend only on (u, j), so a rebuild need not rehash); else the
+// hashes are computed and, when a pristine buffer exists, cached.
 __device__ __forceinline__ void fill_body(uint32_t n, uint32_t J, uint32_t Jp,
                                           const uint64_t* __restrict__ jkey,
                                           const uint32_t* __restrict__ vis,
-                                          int8_t* __restrict__ regs, RankCtl* ctl) {
+                                          int8_t* __restrict__ regs, RankCtl* ctl,
+                                          int8_t* __restrict__ pristine, bool use_pristine) {
   if (ctl && blockIdx.x == 0 && threadIdx.x == 0) ctl->dirty_count = 0;  // full rescore follows
   const uint32_t q = Jp >> 2;
   const uint32_t W32 = Jp >> 5;
-  // warp per row, lanes over 4-register words (coalesced u32 stores)
   const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  if (use_pristine && pristine) {  // pure streaming copy, warp per row
+    for (uint64_t u = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; u < n; u += nw) {
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(pristine + u * Jp);
+      uint32_t* dst = reinterpret_cast<uint32_t*>(regs + u * Jp);
+      for (uint32_t w = lane_id(); w < q; w += 32) {
+        const uint32_t j0 = w * 4;
+        const uint32_t vb = (__ldcg(vis + u * W32 + (j0 >> 5)) >> (j0 & 31)) & 15u;
+        dst[w] = __ldcs(src + w) | (((vb * 0x00204081u) & 0x01010101u) * 0xFFu);
+      }
+    }
+    return;
+  }
+  // warp per row, lanes over 4-register words (coalesced u32 stores)
   for (uint64_t u = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; u < n; u += nw) {
     const uint64_t ug = u * kGolden;
     uint32_t* row = reinterpret_cast<uint32_t*>(regs + u * Jp);
+    uint32_t* prow = pristine ? reinterpret_cast<uint32_t*>(pristine + u * Jp) : nullptr;
     for (uint32_t w = lane_id(); w < q; w += 32) {
       const uint32_t j0 = w * 4;
       const uint32_t vb = vis[u * W32 + (j0 >> 5)] >> (j0 & 31);
-      uint32_t word = 0;
+      uint32_t word = 0, pw = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const uint32_t j = j0 + k;
-        uint32_t byte = 0xFFu;
-        if (j < J && !((vb >> k) & 1u)) byte = uint32_t(__clzll(fmix64(__ldg(jkey + j) + ug)));
-        word |= byte << (8 * k);
+        uint32_t h = 0xFFu;
+        if (j < J) h = uint32_t(__clzll(fmix64(__ldg(jkey + j) + ug)));
+        pw |= h << (8 * k);
+        word |= (((vb >> k) & 1u) ? 0xFFu : h) << (8 * k);
       }
       row[w] = word;
+      if (prow) prow[w] = pw;
     }
   }
 }
 
 __global__ void k_fill(uint32_t n, uint32_t J, uint32_t Jp, const uint64_t* __restrict__ jkey,
                        const uint32_t* __restrict__ vis, int8_t* __restrict__ regs,
-                       const unsigned int* gate, unsigned int want, RankCtl* ctl) {
+                       const unsigned int* gate, unsigned int want, RankCtl* ctl,
+                       int8_t* pristine, bool use_pristine) {
   if (gate && ld_volatile(gate) != want) return;
-  fill_body(n, J, Jp, jkey, vis, regs, ctl);
+  fill_body(n, J, Jp, jkey, vis, regs, ctl, pristine, use_pristine);
 }
 
 // ---------------------------------------------------------------- simulate
@@ -1643,11 +1663,14 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
     __syncthreads();
   };
   const SimOpts so{a.cap, a.dbg, a.sim_pull_f};
+  bool first_fill = true;  // the first fill ran as a separate full-occupancy launch
   auto rebuild = [&]() {  // fill -> simulate -> full rescore, every partition
-    for (uint32_t t = 0; t < a.mu; ++t) {
-      load_rank(t);
-      fill_body(s_r.n, s_r.J, s_r.Jp, s_r.jkey, s_r.vis, s_r.regs, s_r.ctl);
-    }
+    if (!first_fill)
+      for (uint32_t t = 0; t < a.mu; ++t) {
+        load_rank(t);
+        fill_body(s_r.n, s_r.J, s_r.Jp, s_r.jkey, s_r.vis, s_r.regs, s_r.ctl, s_r.pristine, true);
+      }
+    first_fill = false;
     grid.sync();
     phase(0);
     for (uint32_t t = 0; t < a.mu; ++t) {
@@ -1877,11 +1900,12 @@ void launch_small_items(Items& it, unsigned long long* cnt, cudaStream_t s) {
   ++g_launches;
 }
 
-void launch_fill(const RankDev& r, const unsigned int* gate, unsigned int want, cudaStream_t s) {
+void launch_fill(const RankDev& r, const unsigned int* gate, unsigned int want, cudaStream_t s,
+                 bool use_pristine) {
   const uint64_t total = uint64_t(r.n) * 32;
   if (!r.n) return;
   k_fill<<<grid_for(total), kThreads, 0, s>>>(r.n, r.J, r.Jp, r.jkey, r.vis, r.regs, gate, want,
-                                              r.ctl);
+                                              r.ctl, r.pristine, use_pristine);
   DFS_CUDA(cudaGetLastError());
   ++g_launches;
 }

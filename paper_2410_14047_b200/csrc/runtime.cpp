@@ -134,6 +134,13 @@ void Context::alloc_rank(RankDev& r, uint32_t tau) {
   r.jkey = as<uint64_t>(arena_.get(p + "jkey", r.Jp * 8));
   r.regs = as<int8_t>(arena_.get(p + "regs", nn * r.Jp));
   r.snap = cfg_.jacobi ? as<int8_t>(arena_.get(p + "snap", nn * r.Jp)) : nullptr;
+  {  // cached first fill, when HBM allows (rebuild fills become a copy)
+    size_t fr = 0, tot = 0;
+    DFS_CUDA(cudaMemGetInfo(&fr, &tot));
+    r.pristine = fr > 3 * nn * r.Jp + (size_t(2) << 30)
+                     ? as<int8_t>(arena_.get(p + "pristine", nn * r.Jp))
+                     : nullptr;
+  }
   r.vis = as<uint32_t>(arena_.get(p + "vis", nn * r.W32 * 4));
   r.fresh[0] = as<uint32_t>(arena_.get(p + "fresh0", nn * r.W32 * 4));
   r.fresh[1] = as<uint32_t>(arena_.get(p + "fresh1", nn * r.W32 * 4));
@@ -396,7 +403,10 @@ Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
     RankDev* dranks = as<RankDev>(arena_.get("run.ranks", mu * sizeof(RankDev)));
     DFS_CUDA(cudaMemcpyAsync(dranks, ranks_.data(), mu * sizeof(RankDev), cudaMemcpyHostToDevice, s));
     DFS_CUDA(cudaMemsetAsync(phase_ns, 0, 8 * 8, s));
-    mark();
+    const size_t f0 = mark();
+    for (uint32_t t = 0; t < mu; ++t) launch_fill(ranks_[t], nullptr, 0, s, false);
+    const size_t f1 = mark();
+    spans.push_back({f0, f1, &pt.fill});
     launch_run(dranks, mu, k, cfg.r, n, cfg.rebuild_eps, cfg.sim_cap, cfg.jacobi, cfg.count, 53 - lj,
                ra, dparts, dctl, ra.reduced, phase_ns, s);
   } else {
@@ -423,7 +433,7 @@ Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
       spans.push_back({a, b, &pt.cascade});
       prev = b;
       if (step + 1 < k) {  // eps-gated rebuild (runtime.cpp:139-153), predicated on device
-        for (uint32_t t = 0; t < mu; ++t) launch_fill(ranks_[t], rebuild, 1, s);
+        for (uint32_t t = 0; t < mu; ++t) launch_fill(ranks_[t], rebuild, 1, s, true);
         size_t c = mark();
         for (uint32_t t = 0; t < mu; ++t)
           launch_simulate(ranks_[t], cfg.jacobi, cfg.count, cfg.sim_cap, rebuild, 1, s);
