@@ -121,6 +121,7 @@ struct RankDev {
   uint32_t* fresh[3] = {nullptr, nullptr, nullptr};  // n*W32 cascade frontier bits
   uint32_t* lstamp = nullptr;     // n  queue-membership stamps
   uint32_t* dstamp = nullptr;     // n  dirty-row stamps
+  unsigned long long* cstamp = nullptr;  // n  cascade: (round << 32) | level stamp
   uint32_t* dirty = nullptr;      // n  rows to rescore
   uint32_t* tbits = nullptr;      // n*W32 bits: touched (row, batch) of a sweep (count mode)
   double* scores = nullptr;       // n

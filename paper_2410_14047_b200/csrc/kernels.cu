@@ -464,18 +464,36 @@ __device__ __forceinline__ unsigned agg_reserve(unsigned int* ctr, unsigned coun
   if (grp.thread_rank() == last) base = atomicAdd(ctr, excl + count);
   return grp.shfl(base, last) + excl;
 }
+__device__ __forceinline__ unsigned long long agg_reserve64(unsigned long long* ctr,
+                                                            unsigned long long count) {
+  cg::coalesced_group grp = cg::coalesced_threads();
+  const unsigned long long excl = cg::exclusive_scan(grp, count);
+  unsigned long long base = 0;
+  const unsigned last = grp.size() - 1;
+  if (grp.thread_rank() == last) base = atomicAdd(ctr, excl + count);
+  return grp.shfl(base, last) + excl;
+}
+
+// Queue generation counter: (rows << 32) | chunks, so one atomic reserves
+// both the row slot and the chunk slots of a pushed row.
+__device__ __forceinline__ uint32_t qchunks(const unsigned long long* qc, int g) {
+  return uint32_t(ld_volatile(&qc[g]));
+}
+__device__ __forceinline__ uint32_t qrows(const unsigned long long* qc, int g) {
+  return uint32_t(ld_volatile(&qc[g]) >> 32);
+}
 
 // Push of row u into the next generation (deduplicated by stamp): appends u
 // to rows[gn] and all of u's chunks to chunks[gn].
 __device__ __forceinline__ void push_row(uint32_t u, uint32_t stamp, uint32_t* lstamp,
                                          const uint32_t* row_chunk, uint32_t* rows,
-                                         uint32_t* chunks, unsigned int* chunk_cnt,
-                                         unsigned int* row_cnt) {
+                                         uint32_t* chunks, unsigned long long* qcg) {
   if (ld_volatile(&lstamp[u]) == stamp) return;
   if (atomicExch(&lstamp[u], stamp) == stamp) return;
   const uint32_t c0 = row_chunk[u], c1 = row_chunk[u + 1];
-  rows[agg_reserve(row_cnt, 1u)] = u;
-  const unsigned ci = agg_reserve(chunk_cnt, c1 - c0);
+  const unsigned long long o = agg_reserve64(qcg, (1ull << 32) | (c1 - c0));
+  rows[o >> 32] = u;
+  const uint32_t ci = uint32_t(o);
   for (uint32_t c = c0; c < c1; ++c) chunks[ci + (c - c0)] = c;
 }
 
@@ -484,6 +502,28 @@ __device__ __forceinline__ void push_dirty(uint32_t v, uint32_t base, uint32_t* 
   if (ld_volatile(&dstamp[v]) == base) return;
   if (atomicExch(&dstamp[v], base) == base) return;
   dirty[agg_reserve(dirty_count, 1u)] = v;
+}
+
+// Cascade bookkeeping of a row that just received new VISITED bits: one
+// 64-bit stamp (round base << 32 | level stamp) deduplicates both the dirty
+// list (rows to rescore after this cascade) and the next-level frontier.
+__device__ __forceinline__ void cascade_mark(uint32_t v, uint32_t base, uint32_t stamp,
+                                             unsigned long long* cstamp, uint32_t* dirty,
+                                             unsigned int* dirty_count, const uint32_t* row_chunk,
+                                             uint32_t* rows, uint32_t* chunks,
+                                             unsigned long long* qcg) {
+  const unsigned long long want = (static_cast<unsigned long long>(base) << 32) | stamp;
+  if (ld_volatile(&cstamp[v]) == want) return;
+  const unsigned long long old = atomicExch(&cstamp[v], want);
+  if (old == want) return;
+  if (uint32_t(old >> 32) != base) dirty[agg_reserve(dirty_count, 1u)] = v;
+  if (uint32_t(old) != stamp) {
+    const uint32_t c0 = row_chunk[v], c1 = row_chunk[v + 1];
+    const unsigned long long o = agg_reserve64(qcg, (1ull << 32) | (c1 - c0));
+    rows[o >> 32] = v;
+    const uint32_t ci = uint32_t(o);
+    for (uint32_t c = c0; c < c1; ++c) chunks[ci + (c - c0)] = c;
+  }
 }
 
 // Per-warp staging for the flattened item distribution.
@@ -720,6 +760,7 @@ __device__ __forceinline__ void simulate_body(const RankDev& r, const SimOpts& a
                                               unsigned long long& s_release,
                                               unsigned long long* dyn_smem) {
   unsigned int* cnt = r.q.counts;
+  unsigned long long* qc = reinterpret_cast<unsigned long long*>(r.q.counts);
   const uint32_t base = ld_volatile(&r.ctl->tick);
   const unsigned lane = lane_id();
   const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -759,10 +800,9 @@ __device__ __forceinline__ void simulate_body(const RankDev& r, const SimOpts& a
     const int g = s % 3, gn = (s + 1) % 3, gr = (s + 2) % 3;
     const uint64_t my_warp = solo ? (threadIdx.x >> 5) : gwarp;
     const uint64_t n_warps = solo ? kWarps : nw;
-    const uint32_t nc = (s == 1) ? uint32_t(r.rev.chunks) : ld_volatile(&cnt[g]);
+    const uint32_t nc = (s == 1) ? uint32_t(r.rev.chunks) : qchunks(qc, g);
     if (my_warp == 0 && lane == 0) {
-      cnt[gr] = 0;
-      cnt[4 + gr] = 0;
+      qc[gr] = 0;
       cnt[8 + gr] = 0;
       *reinterpret_cast<unsigned long long*>(&cnt[12 + 2 * ((s + 1) & 1)]) = 0;  // next sweep's
     }
@@ -862,7 +902,7 @@ __device__ __forceinline__ void simulate_body(const RankDev& r, const SimOpts& a
         if (lane < 4) touched[lane] = 0;
         __syncwarp();
         if (__any_sync(0xffffffffu, changed) && lane == 0)
-          push_row(u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
+          push_row(u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &qc[gn]);
       }
       // Small destination rows (<= kSmallRow items): item-parallel over the
       // flattened chunks, one CAS per item on a lightly contended row.
@@ -926,8 +966,7 @@ __device__ __forceinline__ void simulate_body(const RankDev& r, const SimOpts& a
             upd += __popc(mq[q]);
             ++nitems;
             if (ch)
-              push_row(uq[q], stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &cnt[gn],
-                       &cnt[4 + gn]);
+              push_row(uq[q], stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &qc[gn]);
           }
         }
       }
@@ -966,18 +1005,16 @@ __device__ __forceinline__ void simulate_body(const RankDev& r, const SimOpts& a
               }
             }
             if (ca)
-              push_row(A.u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &cnt[gn],
-                       &cnt[4 + gn]);
+              push_row(A.u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &qc[gn]);
             if (cb)
-              push_row(B.u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &cnt[gn],
-                       &cnt[4 + gn]);
+              push_row(B.u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &qc[gn]);
           });
     }
   };
   // engine.cpp:81-82: re-sync snapshot rows that moved (Jacobi schedule).
   auto resync = [&](uint32_t s, bool solo) {
     const int gn = (s + 1) % 3;
-    const unsigned nr = ld_volatile(&cnt[4 + gn]);
+    const unsigned nr = qrows(qc, gn);
     const uint64_t my_warp = solo ? (threadIdx.x >> 5) : gwarp;
     const uint64_t n_warps = solo ? kWarps : nw;
     for (uint64_t k = my_warp; k < nr; k += n_warps) {
@@ -996,12 +1033,12 @@ __device__ __forceinline__ void simulate_body(const RankDev& r, const SimOpts& a
   int err = 0;
   for (;;) {
     const int g = s % 3;
-    if (s > 1 && ld_volatile(&cnt[4 + g]) == 0) break;  // no row changed in sweep s-1
+    if (s > 1 && qrows(qc, g) == 0) break;  // no row changed in sweep s-1
     if (s > uint32_t(a.cap)) {
       err = 1;
       break;
     }
-    if (s > 1 && ld_volatile(&cnt[g]) <= kSoloChunks) {
+    if (s > 1 && qchunks(qc, g) <= kSoloChunks) {
       // Small frontier: block 0 iterates alone with block barriers; the rest
       // of the grid parks until it hands back (grid barriers cost more than
       // the work of a tail sweep).
@@ -1009,7 +1046,7 @@ __device__ __forceinline__ void simulate_body(const RankDev& r, const SimOpts& a
         uint32_t code = 0;  // 0 resume grid mode at s, 1 converged, 2 cap exceeded
         for (;;) {
           const int gg = s % 3;
-          if (ld_volatile(&cnt[4 + gg]) == 0) {
+          if (qrows(qc, gg) == 0) {
             code = 1;
             break;
           }
@@ -1017,7 +1054,7 @@ __device__ __forceinline__ void simulate_body(const RankDev& r, const SimOpts& a
             code = 2;
             break;
           }
-          if (ld_volatile(&cnt[gg]) > 4 * kSoloChunks) break;
+          if (qchunks(qc, gg) > 4 * kSoloChunks) break;
           sweep(s, true);
           __syncthreads();
           if (JAC) {
@@ -1322,6 +1359,7 @@ __device__ __forceinline__ void cascade_body(const RankDev& r, const CasOpts& a,
                                              cg::grid_group& grid, WarpStage* stage,
                                              unsigned long long& s_release, uint32_t* cas_smem) {
   unsigned int* cnt = r.q.counts;
+  unsigned long long* qc = reinterpret_cast<unsigned long long*>(r.q.counts);
   const uint32_t base = ld_volatile(&r.ctl->tick);
   const unsigned lane = lane_id();
   const uint64_t gwarp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -1343,7 +1381,6 @@ __device__ __forceinline__ void cascade_body(const RankDev& r, const CasOpts& a,
     if (lane == 0) {
       r.ctl->dirty_count = 1;
       r.dirty[0] = s;
-      r.dstamp[s] = base;
     }
     // engine.cpp:106-118: every non-VISITED register of s becomes fresh.
     bool any = false;
@@ -1362,9 +1399,15 @@ __device__ __forceinline__ void cascade_body(const RankDev& r, const CasOpts& a,
     }
     any = __any_sync(0xffffffffu, any);
     __syncwarp();
-    if (any && lane == 0)
-      push_row(s, base + 1, r.lstamp, r.fwd.row_chunk, r.q.rows[1], r.q.chunks[1], &cnt[1],
-               &cnt[5]);
+    if (lane == 0) {
+      r.cstamp[s] = (static_cast<unsigned long long>(base) << 32) | (any ? base + 1 : 0u);
+      if (any) {
+        const uint32_t c0 = r.fwd.row_chunk[s], c1 = r.fwd.row_chunk[s + 1];
+        qc[1] = (1ull << 32) | (c1 - c0);
+        r.q.rows[1][0] = s;
+        for (uint32_t c = c0; c < c1; ++c) r.q.chunks[1][c - c0] = c;
+      }
+    }
   }
 
   // One BFS level.  solo: only block 0 (small frontier, block barriers).
@@ -1375,13 +1418,12 @@ __device__ __forceinline__ void cascade_body(const RankDev& r, const CasOpts& a,
     const uint32_t* fcur = r.fresh[L % 3];
     uint32_t* fnxt = r.fresh[(L + 1) % 3];
     uint32_t* fprev = r.fresh[(L + 2) % 3];
-    const uint32_t nc = ld_volatile(&cnt[g]);
+    const uint32_t nc = qchunks(qc, g);
     if (my_warp == 0 && lane == 0) {
-      cnt[gr] = 0;
-      cnt[4 + gr] = 0;
+      qc[gr] = 0;
       cnt[8 + gr] = 0;
     }
-    clear_rows(fprev, r.q.rows[gp], ld_volatile(&cnt[4 + gp]), W32, my_warp, n_warps, lane);
+    clear_rows(fprev, r.q.rows[gp], qrows(qc, gp), W32, my_warp, n_warps, lane);
     if ((a.dbg & 4) && blockIdx.x == 0 && threadIdx.x == 0) trace(2 + (solo ? 1 : 0), L, nc);
     const uint32_t stamp = base + L + 1;
     uint32_t* rows_n = r.q.rows[gn];
@@ -1395,8 +1437,8 @@ __device__ __forceinline__ void cascade_body(const RankDev& r, const CasOpts& a,
       for (uint32_t t = nb; t; t &= t - 1) rb[__ffs(t) - 1] = -1;
       atomicOr(fnxt + uint64_t(v) * W32 + b, nb);
       marked += __popc(nb);
-      push_dirty(v, base, r.dstamp, r.dirty, &r.ctl->dirty_count);
-      push_row(v, stamp, r.lstamp, r.fwd.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
+      cascade_mark(v, base, stamp, r.cstamp, r.dirty, &r.ctl->dirty_count, r.fwd.row_chunk, rows_n,
+                   chunks_n, &qc[gn]);
     };
     // Top-down pair: frontier row u -> targets of two forward items.
     auto visit = [&](uint32_t ua, uint64_t ia, bool pa, uint32_t ub, uint64_t ib, bool pb) {
@@ -1431,6 +1473,11 @@ __device__ __forceinline__ void cascade_body(const RankDev& r, const CasOpts& a,
           mq[q] = act ? __ldg(r.rev.mask + i) : 0;
           bq[q] = act ? __ldg(r.rev.batch + i) : 0;
         }
+        // bottom-up: only simulations still unvisited at v look for a parent
+        const uint32_t* vrow = r.vis + uint64_t(v) * W32;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (mq[q]) mq[q] &= ~__ldcg(vrow + bq[q]);
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           fq[q] = mq[q] ? __ldcg(fcur + uint64_t(uq[q]) * W32 + bq[q]) & mq[q] : 0;
@@ -1467,10 +1514,9 @@ __device__ __forceinline__ void cascade_body(const RankDev& r, const CasOpts& a,
           got = true;
         }
         __syncwarp();
-        if (__any_sync(0xffffffffu, got) && lane == 0) {
-          push_dirty(v, base, r.dstamp, r.dirty, &r.ctl->dirty_count);
-          push_row(v, stamp, r.lstamp, r.fwd.row_chunk, rows_n, chunks_n, &cnt[gn], &cnt[4 + gn]);
-        }
+        if (__any_sync(0xffffffffu, got) && lane == 0)
+          cascade_mark(v, base, stamp, r.cstamp, r.dirty, &r.ctl->dirty_count, r.fwd.row_chunk,
+                       rows_n, chunks_n, &qc[gn]);
       }
       // Small target rows: item-parallel, one atomicOr per newly reached word.
       for_frontier_items(r.rev, r.rev.small, r.rev.nsmall, &cnt[8 + g], ws, n_warps,
@@ -1478,12 +1524,12 @@ __device__ __forceinline__ void cascade_body(const RankDev& r, const CasOpts& a,
         const uint32_t ba = pa ? __ldg(r.rev.batch + ia) : 0, bb = pb ? __ldg(r.rev.batch + ib) : 0;
         const uint32_t ma = pa ? __ldg(r.rev.mask + ia) : 0, mb = pb ? __ldg(r.rev.mask + ib) : 0;
         const uint32_t ua = pa ? __ldg(r.rev.other + ia) : 0, ub = pb ? __ldg(r.rev.other + ib) : 0;
-        uint32_t ca = pa ? __ldcg(fcur + uint64_t(ua) * W32 + ba) & ma : 0;
-        uint32_t cb = pb ? __ldcg(fcur + uint64_t(ub) * W32 + bb) & mb : 0;
-        const uint32_t xa = ca ? __ldcg(r.vis + uint64_t(va) * W32 + ba) : 0;
-        const uint32_t xb = cb ? __ldcg(r.vis + uint64_t(vb) * W32 + bb) : 0;
-        ca &= ~xa;
-        cb &= ~xb;
+        // bottom-up: unvisited simulations of the target first, then parents
+        const uint32_t xa = pa ? __ldcg(r.vis + uint64_t(va) * W32 + ba) : 0xFFFFFFFFu;
+        const uint32_t xb = pb ? __ldcg(r.vis + uint64_t(vb) * W32 + bb) : 0xFFFFFFFFu;
+        const uint32_t na = ma & ~xa, nb2 = mb & ~xb;
+        const uint32_t ca = na ? __ldcg(fcur + uint64_t(ua) * W32 + ba) & na : 0;
+        const uint32_t cb = nb2 ? __ldcg(fcur + uint64_t(ub) * W32 + bb) & nb2 : 0;
         if (ca) claim(va, ba, ca);
         if (cb) claim(vb, bb, cb);
       });
@@ -1496,8 +1542,8 @@ __device__ __forceinline__ void cascade_body(const RankDev& r, const CasOpts& a,
     const int g = L % 4, gp = (L + 3) % 4;
     const uint64_t my_warp = solo ? (threadIdx.x >> 5) : gwarp;
     const uint64_t n_warps = solo ? kWarps : nw;
-    clear_rows(r.fresh[L % 3], r.q.rows[g], ld_volatile(&cnt[4 + g]), W32, my_warp, n_warps, lane);
-    clear_rows(r.fresh[(L + 2) % 3], r.q.rows[gp], ld_volatile(&cnt[4 + gp]), W32, my_warp,
+    clear_rows(r.fresh[L % 3], r.q.rows[g], qrows(qc, g), W32, my_warp, n_warps, lane);
+    clear_rows(r.fresh[(L + 2) % 3], r.q.rows[gp], qrows(qc, gp), W32, my_warp,
                n_warps, lane);
   };
 
@@ -1511,7 +1557,7 @@ __device__ __forceinline__ void cascade_body(const RankDev& r, const CasOpts& a,
     if (blockIdx.x == 0) {
       __syncthreads();
       for (;;) {
-        const uint32_t nc = ld_volatile(&cnt[L % 4]);
+        const uint32_t nc = qchunks(qc, L % 4);
         if (nc == 0) {
           finish(L, true);
           code = 1;
@@ -1546,7 +1592,7 @@ __device__ __forceinline__ void cascade_body(const RankDev& r, const CasOpts& a,
     ++e;
     if (code == 1) break;
     for (;;) {  // grid-wide levels while the frontier is large
-      if (ld_volatile(&cnt[L % 4]) <= kSoloChunks) break;
+      if (qchunks(qc, L % 4) <= kSoloChunks) break;
       level(L, false);
       grid.sync();
       ++L;

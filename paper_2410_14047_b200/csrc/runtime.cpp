@@ -147,6 +147,7 @@ void Context::alloc_rank(RankDev& r, uint32_t tau) {
   r.fresh[2] = as<uint32_t>(arena_.get(p + "fresh2", nn * r.W32 * 4));
   r.lstamp = as<uint32_t>(arena_.get(p + "lstamp", nn * 4));
   r.dstamp = as<uint32_t>(arena_.get(p + "dstamp", nn * 4));
+  r.cstamp = as<unsigned long long>(arena_.get(p + "cstamp", nn * 8));
   r.dirty = as<uint32_t>(arena_.get(p + "dirty", nn * 4));
   r.tbits = cfg_.count ? as<uint32_t>(arena_.get(p + "tbits", (nn * r.W32 + 31) / 32 * 4 + 4))
                        : nullptr;
@@ -255,6 +256,7 @@ void Context::reset_rank_state(RankDev& r) {
   DFS_CUDA(cudaMemsetAsync(r.fresh[2], 0, nn * r.W32 * 4, stream_));
   DFS_CUDA(cudaMemsetAsync(r.lstamp, 0, nn * 4, stream_));
   DFS_CUDA(cudaMemsetAsync(r.dstamp, 0, nn * 4, stream_));
+  DFS_CUDA(cudaMemsetAsync(r.cstamp, 0, nn * 8, stream_));
   DFS_CUDA(cudaMemsetAsync(r.regs, 0, nn * r.Jp, stream_));
   DFS_CUDA(cudaMemsetAsync(r.scores, 0, nn * 8, stream_));
   DFS_CUDA(cudaMemsetAsync(r.q.counts, 0, 16 * 4, stream_));
