@@ -304,6 +304,30 @@ def run_ours(args, rank, world, local_rank):
                     "units": {x: alg[x] for x in ("E", "B", "T", "S", "L", "convergences")}}
         upd_per_s = alg["L"] / max(sim_active, 1e-12)
 
+    # North-star workload (BASELINE.json north_star): R-MAT scale 23 (100M
+    # edges), IC p=0.01, R=1024, K=50 — end-to-end seconds with the graph resident.
+    north = None
+    if args.north_star and world == 1:
+        gen3, a3, m3, w3, r3, k3, desc3 = CONFIGS["c3ic"]
+        g3 = D.generate(gen3, a3, m3, SEED)
+        ctx.upload(g3)
+        ts3 = []
+        for i in range(4):
+            flush.add_(1)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ctx.run_json(None, k=k3, r=r3, devices=1, weights=w3, seed=SEED, timings=False,
+                         resident=True)
+            e1.record(stream)
+            e1.synchronize()
+            if i:
+                ts3.append(e0.elapsed_time(e1) / 1e3)
+        north = {"workload": desc3, "n": g3.n, "m": g3.m, "seconds": round(statistics.mean(ts3), 5),
+                 "runs": len(ts3), "n_gpus": 1, "target_seconds_8gpu": 1.0}
+        del g3
+
     cpu = None
     if not args.no_cpu_baseline:
         try:
@@ -332,6 +356,7 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": d2h},
         "clocks": clocks,
         "gpu_launches": int(statistics.mean(s["launches"] for s in stats)),
+        "north_star": north,
     }
     print(json.dumps(line), flush=True)
     if dist:
@@ -346,6 +371,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--north-star", dest="north_star", action="store_true", default=True)
+    ap.add_argument("--no-north-star", dest="north_star", action="store_false")
     args = ap.parse_args()
     rank, world, local_rank = env_rank()
     if args.impl == "reference":
