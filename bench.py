@@ -14,8 +14,10 @@ R-MAT scale-20, 16M edges, IC p=0.01, R=256 simulations, K=50 seeds.
             compiled from /root/reference) on the host cores, same workload.
 
 Multi-GPU (torchrun, N ranks): FASST sample-space partitioning, devices = N,
-one partition per GPU (paper_2410_14047_b200.dist).  Timing is the max over
-ranks of CUDA-event time.
+one partition per GPU; the per-round exchange runs inside each GPU's
+persistent kernel over peer memory (paper_2410_14047_b200.dist.PeerRunner;
+NCCL only swaps the IPC handles).  Timing is the max over ranks of CUDA-event
+time.
 """
 from __future__ import annotations
 
@@ -181,42 +183,65 @@ def run_reference(D, cfgname, steps, warmup, graph=None):
 # ----------------------------------------------------------------- our arm
 def algorithmic_bytes(D, ctx, g, cfgname, devices):
     """Reference-schedule work units of SURVEY.md §8(d), counted by an
-    instrumented Jacobi replay (same schedule as proj/src/engine.cpp:57-96)."""
+    instrumented replay with the reference's Jacobi schedule
+    (proj/src/engine.cpp:57-144): implementation-independent numerators.
+
+      simulate  B_sim = sum over sweeps of 12 E + 32 B + 64 T + 8 (n+1)
+      cascade   B_cas = 12 E_c + (J/8) (F + 2 (F - C))   F frontier rows over
+                all levels, E_c their device-graph out-edges, C cascades
+                (targets touched = frontier rows of the next level)
+      score     K (n J + 8 n)   (the reference rescores every row each round)
+      fills     rebuilds * n J  (the first fill is a separate launch)
+    """
     gen, a, m, wspec, r, k, desc = CONFIGS[cfgname]
-    ctx.run_json(None, k=k, r=r, devices=devices, weights=wspec, seed=SEED, timings=False,
-                 jacobi=1, count=1, resident=True)
+    rep = json.loads(ctx.run_json(None, k=k, r=r, devices=devices, weights=wspec, seed=SEED,
+                                  timings=False, jacobi=1, count=1, resident=True))
     st = ctx.stats()
     E, B, T, S = st["cnt_edges"], st["cnt_batches"], st["cnt_touched"], st["cnt_sweeps"]
     conv = max(st["cnt_convergences"], 1)
     n = st["n"]
+    J = r // devices
     b_sim = 12 * E + 32 * B + 64 * T + 8 * (n + 1) * S
+    F, Ec, C = st["cnt_cas_rows"], st["cnt_cas_edges"], st["cnt_cascades"]
+    b_cas = 12 * Ec + (J / 8) * (F + 2 * (F - C))
+    b_score = k * (n * J + 8 * n)
+    b_fill = rep["rebuilds"] * n * J
     return {"E": E, "B": B, "T": T, "S": S, "L": st["sketch_edge_updates"], "convergences": conv,
-            "bytes": b_sim, "bytes_per_launch": b_sim / conv}
+            "cascade_rows": F, "cascade_edges": Ec, "cascades": C,
+            "bytes": b_sim, "bytes_per_launch": b_sim / conv, "sim_bytes": b_sim,
+            "cascade_bytes": b_cas, "score_bytes": b_score, "fill_bytes": b_fill,
+            "run_bytes": b_sim + b_cas + b_score + b_fill}
 
 
 def run_ours(args, rank, world, local_rank):
     import torch
     import paper_2410_14047_b200 as D
 
+    if args.share_gpu:  # plumbing check only: every rank on cuda:0, gloo (time-sliced, not a number)
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     gen, a, m, wspec, r, k, desc = CONFIGS[args.config]
     devices = world  # FASST partitions: one per GPU
     g = make_graph(D, args.config)
     g.pin()
     ctx = D.Context(local_rank)
-    if world > 1:
+    if world > 1:  # peer mode: exchange inside the persistent kernel over NVLink
         from paper_2410_14047_b200 import dist as pdist
-        runner = pdist.DistRunner(ctx, g, rank, world)
+        runner = pdist.PeerRunner(ctx, g, rank, world)
     stream = torch.cuda.ExternalStream(ctx.stream, device=local_rank)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=f"cuda:{local_rank}")
 
     def one_run(resident):
         if world > 1:
-            return runner.run_json(k=k, r=r, weights=wspec, seed=SEED, resident=resident)
+            return runner.run_json(k=k, r=r, weights=wspec, seed=SEED, resident=resident,
+                                   timings=False)
         if resident:
             return ctx.run_json(None, k=k, r=r, devices=1, weights=wspec, seed=SEED,
                                 timings=False, resident=True)
@@ -251,7 +276,8 @@ def run_ours(args, rank, world, local_rank):
     clocks = clk.stop()
     step_s = statistics.mean(times)
     if dist:
-        t = torch.tensor([step_s], device=f"cuda:{local_rank}", dtype=torch.float64)
+        t = torch.tensor([step_s], device="cpu" if args.share_gpu else f"cuda:{local_rank}",
+                         dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         step_s = float(t.item())
 
@@ -269,7 +295,8 @@ def run_ours(args, rank, world, local_rank):
         e2e_times.append(e0.elapsed_time(e1) / 1e3)
     e2e_s = statistics.mean(e2e_times)
     if dist:
-        t = torch.tensor([e2e_s], device=f"cuda:{local_rank}", dtype=torch.float64)
+        t = torch.tensor([e2e_s], device="cpu" if args.share_gpu else f"cuda:{local_rank}",
+                         dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     assert json.loads(rep_e2e)["seeds"] == json.loads(rep)["seeds"]
@@ -281,27 +308,39 @@ def run_ours(args, rank, world, local_rank):
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (persistent simulate)
+    # ---- roofline of the dominant kernel: k_run, the whole greedy loop as one
+    # persistent launch per step (CUDA events around that launch on the
+    # context stream); the simulate phase inside it is reported alongside
+    # (in-kernel globaltimer spans, the only way to time a phase of one launch).
     alg = algorithmic_bytes(D, ctx, g, args.config, devices) if world == 1 else None
+    krun_s = statistics.mean(s["run_kernel"] for s in stats)
     sim_active = statistics.mean(s["sim_active"] for s in stats)
     sim_launches = statistics.mean(s["sim_launches"] for s in stats)
     peak, peak_kind = measured_peak()
     roofline = None
     upd_per_s = None
     if alg:
-        per_launch_s = sim_active / max(sim_launches, 1)
-        achieved = alg["bytes_per_launch"] / per_launch_s / 1e9
+        achieved = alg["run_bytes"] / krun_s / 1e9
         traffic = None
         tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
         if os.path.exists(tp):
             with open(tp) as f:
                 traffic = json.load(f).get("dram_bytes_per_launch")
-        roofline = {"bound": "hbm", "kernel": "k_simulate (persistent, to convergence)",
+        per_conv_s = sim_active / max(sim_launches, 1)
+        sim_gbs = alg["bytes_per_launch"] / per_conv_s / 1e9
+        roofline = {"bound": "hbm", "kernel": "k_run (whole greedy loop, one launch per step)",
                     "achieved": round(achieved, 1), "peak": peak, "peak_source": peak_kind,
                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                    "alg_bytes_per_launch": alg["bytes_per_launch"],
-                    "launch_ms": round(per_launch_s * 1e3, 4),
-                    "units": {x: alg[x] for x in ("E", "B", "T", "S", "L", "convergences")}}
+                    "alg_bytes_per_launch": alg["run_bytes"],
+                    "launch_ms": round(krun_s * 1e3, 4),
+                    "alg_bytes_split": {x: alg[x] for x in ("sim_bytes", "cascade_bytes",
+                                                           "score_bytes", "fill_bytes")},
+                    "simulate_phase": {"achieved": round(sim_gbs, 1),
+                                       "frac": round(sim_gbs / peak, 4),
+                                       "alg_bytes_per_convergence": alg["bytes_per_launch"],
+                                       "ms_per_convergence": round(per_conv_s * 1e3, 4)},
+                    "units": {x: alg[x] for x in ("E", "B", "T", "S", "L", "convergences",
+                                                  "cascade_rows", "cascade_edges", "cascades")}}
         upd_per_s = alg["L"] / max(sim_active, 1e-12)
 
     # North-star workload (BASELINE.json north_star): R-MAT scale 23 (100M
@@ -329,7 +368,7 @@ def run_ours(args, rank, world, local_rank):
         del g3
 
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
         try:
             cpu = run_reference(D, args.config, steps=1, warmup=0, graph=g)
         except Exception as ex:  # reported, never fatal
@@ -371,6 +410,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="test only: all ranks on cuda:0 over gloo (checks the N>1 path, no timing)")
     ap.add_argument("--north-star", dest="north_star", action="store_true", default=True)
     ap.add_argument("--no-north-star", dest="north_star", action="store_false")
     args = ap.parse_args()

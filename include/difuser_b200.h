@@ -66,6 +66,10 @@ typedef struct dfs_stats {
   uint32_t sim_launches; /* simulate launches that ran */
   uint32_t n;
   uint64_t m;
+  /* cascade work units (count mode): frontier rows over all levels, their
+   * device-graph out-edges, cascades started */
+  uint64_t cnt_cas_rows, cnt_cas_edges, cnt_cascades;
+  double run_kernel; /* seconds of the whole-loop kernel launch (CUDA events) */
 } dfs_stats;
 
 const char *dfs_last_error(void);
@@ -148,6 +152,31 @@ int dfs_get_registers(dfs_ctx *ctx, uint32_t tau, int8_t *out_nJ);
 int dfs_set_registers(dfs_ctx *ctx, uint32_t tau, const int8_t *in_nJ);
 /* {updates, items, edges, batches, touched, sweeps, convergences, visited} */
 int dfs_rank_counters(dfs_ctx *ctx, uint32_t tau, uint64_t out[8]);
+
+/* ---- peer (multi-GPU) mode ----------------------------------------------
+ * One FASST partition per GPU (one process per GPU, or one context per
+ * partition in one process).  Replaces the per-device worker threads and the
+ * in-process CollectiveGroup of proj/src/runtime.cpp:64-172 and
+ * proj/src/collectives.cpp:44-113: the per-round reduce_to_root (binomial
+ * order), root argmax, seed broadcast and visited-count allreduce run inside
+ * the persistent kernel over peer memory (NVLink P2P; CUDA IPC between
+ * processes) — the host does not participate between rounds.
+ * Setup, per rank: dfs_prepare_partition(ctx, g, cfg{devices = world}, rank,
+ * world) -> dfs_peer_export -> exchange the handles out of band (e.g.
+ * torch.distributed all_gather) -> dfs_peer_open.  Same-process contexts on
+ * distinct devices: dfs_peer_link instead.  Then every rank calls dfs_peer_run_json
+ * concurrently; each returns the same report (= reference run with
+ * devices = world).  A rank that never arrives makes the others fail with
+ * DFS_ERUNTIME after 120 s instead of hanging. */
+#define DFS_PEER_HANDLE_BYTES 152
+int dfs_peer_export(dfs_ctx *ctx, void *handle_out /* DFS_PEER_HANDLE_BYTES */);
+int dfs_peer_open(dfs_ctx *ctx, uint32_t rank, uint32_t world,
+                  const void *handles /* world * DFS_PEER_HANDLE_BYTES, rank order */);
+int dfs_peer_link(dfs_ctx *const *ctxs, uint32_t world);
+/* resident != 0: use the graph uploaded by dfs_upload/dfs_prepare_partition
+ * (g may be NULL for const/wc weights); else upload g first. */
+int dfs_peer_run_json(dfs_ctx *ctx, const dfs_graph *g, const dfs_config *cfg, int timings,
+                      int resident, char **json_out);
 
 /* ---- report formatting (report.cpp:9-41) for drivers that assemble the
  * greedy loop themselves (multi-process path): same nlohmann dump(2) output. */

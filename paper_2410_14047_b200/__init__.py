@@ -20,6 +20,7 @@ from ._capi import Config, Stats, check, lib
 __all__ = ["_config", 
     "Graph", "edge_hash", "graph_from_text", "greedy_exact", "influence", "is_sampled",
     "load_graph", "random_value_at", "run", "run_json", "save_cache", "generate", "Context",
+    "peer_link",
 ]
 
 
@@ -270,6 +271,44 @@ class Context:
     def set_registers(self, tau: int, regs) -> None:
         regs = np.ascontiguousarray(regs, np.int8)
         check(lib().dfs_set_registers(self._h, tau, regs.ctypes.data))
+
+    # ---- peer (multi-GPU) mode: one FASST partition per GPU, exchange in-kernel
+    def prepare_partition(self, graph, rank, world, k=1, r=256, mode="fasst",
+                          weights="const:0.1", rebuild_eps=0.01, seed=0, resident=False):
+        """Build only partition `rank` of `world` (= devices) on this context."""
+        cfg = _config(k, r, world, mode, weights, rebuild_eps, seed)
+        check(lib().dfs_prepare_partition(self._h, None if resident else graph._h, C.byref(cfg),
+                                          rank, world))
+        if graph is not None:
+            self._graph = graph
+        self._cfg = dict(k=k, r=r, devices=world)
+        self._J = r // world
+
+    def peer_export(self) -> bytes:
+        buf = C.create_string_buffer(_capi.PEER_HANDLE_BYTES)
+        check(lib().dfs_peer_export(self._h, buf))
+        return buf.raw
+
+    def peer_open(self, rank: int, world: int, handles) -> None:
+        blob = b"".join(handles)
+        assert len(blob) == world * _capi.PEER_HANDLE_BYTES
+        buf = C.create_string_buffer(blob, len(blob))
+        check(lib().dfs_peer_open(self._h, rank, world, buf))
+
+    def run_peer_json(self, graph, k=10, r=256, devices=2, mode="fasst", weights="const:0.1",
+                      rebuild_eps=0.01, seed=0, timings=True, resident=False):
+        """This rank's share of a multi-GPU run; every rank returns the same report."""
+        cfg = _config(k, r, devices, mode, weights, rebuild_eps, seed)
+        out = C.c_void_p()
+        check(lib().dfs_peer_run_json(self._h, graph._h if graph is not None else None,
+                                      C.byref(cfg), int(timings), int(resident), C.byref(out)))
+        return self._take_json(out)
+
+
+def peer_link(ctxs) -> None:
+    """Link same-process contexts (partition i on ctxs[i]) for peer-mode runs."""
+    arr = (C.c_void_p * len(ctxs))(*[c._h.value for c in ctxs])
+    check(lib().dfs_peer_link(arr, len(ctxs)))
 
 
 _ctx_lock = threading.Lock()

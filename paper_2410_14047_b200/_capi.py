@@ -23,8 +23,11 @@ SYMBOLS = [
     "dfs_fill", "dfs_simulate", "dfs_scores", "dfs_commit_cascade", "dfs_visited_count",
     "dfs_get_registers", "dfs_set_registers", "dfs_influence", "dfs_greedy_exact",
     "dfs_ctx_stream", "dfs_graph_pin", "dfs_rank_counters", "dfs_prepare_partition",
-    "dfs_scores_device", "dfs_rebuild", "dfs_format_report",
+    "dfs_scores_device", "dfs_rebuild", "dfs_format_report", "dfs_peer_export", "dfs_peer_open",
+    "dfs_peer_link", "dfs_peer_run_json",
 ]
+
+PEER_HANDLE_BYTES = 152  # DFS_PEER_HANDLE_BYTES
 
 
 class Config(C.Structure):
@@ -42,7 +45,8 @@ class Stats(C.Structure):
                                           "cnt_batches", "cnt_touched", "cnt_sweeps",
                                           "cnt_convergences", "launches")] + \
                [("sim_active", C.c_double), ("sim_launches", C.c_uint32), ("n", C.c_uint32),
-                ("m", C.c_uint64)]
+                ("m", C.c_uint64), ("cnt_cas_rows", C.c_uint64), ("cnt_cas_edges", C.c_uint64),
+                ("cnt_cascades", C.c_uint64), ("run_kernel", C.c_double)]
 
 
 class ReportFields(C.Structure):
@@ -120,6 +124,10 @@ def lib():
         "dfs_scores_device": (i32, [vp, u32, i32, vp]),
         "dfs_rebuild": (i32, [vp, u32]),
         "dfs_format_report": (i32, [C.POINTER(ReportFields), C.POINTER(C.c_void_p)]),
+        "dfs_peer_export": (i32, [vp, vp]),
+        "dfs_peer_open": (i32, [vp, u32, u32, vp]),
+        "dfs_peer_link": (i32, [C.POINTER(C.c_void_p), u32]),
+        "dfs_peer_run_json": (i32, [vp, vp, C.POINTER(Config), i32, i32, C.POINTER(C.c_void_p)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

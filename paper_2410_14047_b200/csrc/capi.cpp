@@ -7,6 +7,7 @@
 #include <memory>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "graph.h"
 #include "hash.cuh"
@@ -272,6 +273,10 @@ int dfs_last_stats(const dfs_ctx* ctx, dfs_stats* out) {
     out->sim_launches = r.sim_launches;
     out->n = uint32_t(r.n);
     out->m = r.m;
+    out->cnt_cas_rows = r.cnt_cas_rows;
+    out->cnt_cas_edges = r.cnt_cas_edges;
+    out->cnt_cascades = r.cnt_cascades;
+    out->run_kernel = r.run_kernel;
   });
 }
 
@@ -291,6 +296,46 @@ int dfs_prepare_partition(dfs_ctx* ctx, const dfs_graph* g, const dfs_config* cf
     dfs::RunConfig rc = to_config(cfg);
     if (g) ctx->c->upload(g->g);  // g == NULL: use the resident graph
     ctx->c->prepare(rc, g ? &g->g : nullptr, rank, world);
+  });
+}
+static_assert(DFS_PEER_HANDLE_BYTES == dfs::kPeerHandleBytes, "peer handle size");
+int dfs_peer_export(dfs_ctx* ctx, void* handle_out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(handle_out, "handle_out");
+    ctx->c->peer_export(handle_out);
+  });
+}
+int dfs_peer_open(dfs_ctx* ctx, uint32_t rank, uint32_t world, const void* handles) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(handles, "handles");
+    ctx->c->peer_open(rank, world, handles);
+  });
+}
+int dfs_peer_link(dfs_ctx* const* ctxs, uint32_t world) {
+  return guard([&] {
+    need(ctxs, "ctxs");
+    std::vector<dfs::Context*> v;
+    for (uint32_t i = 0; i < world; ++i) {
+      need(ctxs[i], "ctx");
+      v.push_back(ctxs[i]->c.get());
+    }
+    dfs::Context::peer_link(v);
+  });
+}
+int dfs_peer_run_json(dfs_ctx* ctx, const dfs_graph* g, const dfs_config* cfg, int timings,
+                      int resident, char** json_out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(json_out, "json_out");
+    dfs::RunConfig rc = to_config(cfg);
+    if (!resident) {
+      need(g, "graph");
+      ctx->c->upload(g->g);
+    }
+    ctx->last = ctx->c->run_peer(rc, g ? &g->g : nullptr);
+    *json_out = dup_string(dfs::report_to_json(ctx->last, timings != 0));
   });
 }
 int dfs_scores_device(dfs_ctx* ctx, uint32_t tau, int full, void* dst) {

@@ -95,6 +95,9 @@ struct RankCtl {
   unsigned long long cnt_edges, cnt_batches, cnt_touched, cnt_sweeps, cnt_convergences;
   // solo-mode hand-back word: (launch tick << 32) | (resume sweep/level << 2) | code
   unsigned long long release;
+  // cascade work units of the reference schedule (count mode): frontier rows
+  // summed over levels, device-graph edges out of them, cascades started
+  unsigned long long cnt_cas_rows, cnt_cas_edges, cnt_cascades;
 };
 
 // Work queues used by the persistent simulate / cascade kernels.  Rotating
@@ -153,6 +156,32 @@ struct RunArrays {
   uint32_t* blk_arg = nullptr;
   uint32_t* blk_min = nullptr;
   uint32_t nblk = 0;
+};
+
+// ---------------------------------------------------------------- peer mode
+// Multi-GPU: one FASST partition per GPU (one process, or one context, per
+// GPU).  The per-round exchange of proj/src/runtime.cpp:88-130 (partial score
+// reduce in binomial order, argmax, seed broadcast, covered-count allreduce)
+// runs INSIDE the persistent k_run kernel over peer memory (NVLink P2P loads
+// of mapped peer buffers, CUDA IPC across processes) with flag barriers; the
+// host is not involved between rounds.
+constexpr uint32_t kMaxPeers = 16;
+
+// Mailbox of one rank in its own HBM; peers read it through a mapping.
+struct alignas(128) PeerBox {
+  unsigned long long arrive;   // last barrier epoch this rank reached (monotonic)
+  unsigned long long visited;  // this rank's VISITED count after the round's cascade
+  double best_s;               // best positive uncommitted reduced score of the slice
+  unsigned int best_v;         // its id (0xFFFFFFFF: none)
+  unsigned int minu;           // smallest uncommitted id of the slice (0xFFFFFFFF: none)
+  unsigned long long timeouts; // barriers abandoned after the deadline (peer died)
+  unsigned long long pad[11];
+};
+
+struct PeerView {
+  uint32_t world = 0, rank = 0;
+  PeerBox* box[kMaxPeers] = {};          // box[t]: rank t's mailbox (own one for t == rank)
+  const double* scores[kMaxPeers] = {};  // rank t's partial score vector (n doubles)
 };
 
 // ---------------------------------------------------------------- launchers
@@ -216,6 +245,7 @@ int coop_grid(int which, int variant = 0);  // 0 simulate, 1 cascade, 2 whole ru
 void launch_run(const RankDev* ranks_dev, uint32_t mu, uint32_t k, uint32_t R, uint32_t n,
                 double eps, int cap, int jacobi, int count, int K, RunArrays& ra,
                 const double* const* parts, RankCtl* const* ctls, double* reduced,
-                unsigned long long* phase_ns, cudaStream_t s);
+                unsigned long long* phase_ns, const PeerView* peer, int grid_share,
+                cudaStream_t s);
 
 }  // namespace dfs

@@ -18,6 +18,7 @@
 #include <cub/cub.cuh>
 #include <cuda/std/functional>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -1250,15 +1251,17 @@ __device__ __forceinline__ Best best_of(Best a, Best b) {
   return r;
 }
 
-// Block partial of the argmax (runtime.cpp:95-119): best positive
-// uncommitted (score, id) and the smallest uncommitted id of this block.
-__device__ __forceinline__ void argmax_partial(const double* __restrict__ scores, uint32_t n,
-                                               const RunArrays& ra, Best* sb) {
+// Block partial of the argmax (runtime.cpp:95-119) over ids [lo, hi): best
+// positive uncommitted (score, id) and the smallest uncommitted id of this
+// block.  val(v) yields the (reduced) score of v.
+template <class V>
+__device__ __forceinline__ void argmax_partial_range(uint32_t lo, uint32_t hi, V&& val,
+                                                     const RunArrays& ra, Best* sb) {
   Best b{0.0, 0xFFFFFFFFu, 0xFFFFFFFFu};
-  for (uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n;
+  for (uint64_t v = lo + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < hi;
        v += uint64_t(gridDim.x) * blockDim.x) {
     if (ra.committed[v]) continue;
-    const double s = scores[v];
+    const double s = val(uint32_t(v));
     if (b.minu == 0xFFFFFFFFu) b.minu = uint32_t(v);
     if (s > b.s) {  // ascending v within a thread: strict > keeps the first
       b.s = s;
@@ -1282,8 +1285,13 @@ __device__ __forceinline__ void argmax_partial(const double* __restrict__ scores
   }
 }
 
-// Combine nblk partials (one block): choice, committed mark, saturation.
-__device__ __forceinline__ void argmax_finish(uint32_t nblk, const RunArrays& ra, Best* sb) {
+__device__ __forceinline__ void argmax_partial(const double* __restrict__ scores, uint32_t n,
+                                               const RunArrays& ra, Best* sb) {
+  argmax_partial_range(0, n, [&](uint32_t v) { return scores[v]; }, ra, sb);
+}
+
+// Combine nblk partials (one block); the result is valid in thread 0.
+__device__ __forceinline__ Best argmax_combine(uint32_t nblk, const RunArrays& ra, Best* sb) {
   Best t{0.0, 0xFFFFFFFFu, 0xFFFFFFFFu};
   for (uint32_t k = threadIdx.x; k < nblk; k += blockDim.x)
     t = best_of(t, Best{__ldcg(ra.blk_score + k), __ldcg(ra.blk_arg + k), __ldcg(ra.blk_min + k)});
@@ -1298,15 +1306,26 @@ __device__ __forceinline__ void argmax_finish(uint32_t nblk, const RunArrays& ra
   if (threadIdx.x == 0) {
     t = sb[0];
     for (int w = 1; w < kWarps; ++w) t = best_of(t, sb[w]);
-    uint32_t choice = t.v;
-    if (choice == 0xFFFFFFFFu) {  // saturated: smallest uncommitted id
-      ra.ctl->saturated = 1;
-      choice = t.minu;
-    }
-    ra.ctl->choice = choice;
-    ra.committed[choice] = 1;
-    ra.ctl->argmax_done = 0;
   }
+  return t;
+}
+
+// Commit the winner (thread 0): choice, committed mark, saturation fallback to
+// the smallest uncommitted id (runtime.cpp:95-121).
+__device__ __forceinline__ void commit_choice(Best t, const RunArrays& ra) {
+  uint32_t choice = t.v;
+  if (choice == 0xFFFFFFFFu) {  // saturated: smallest uncommitted id
+    ra.ctl->saturated = 1;
+    choice = t.minu;
+  }
+  ra.ctl->choice = choice;
+  ra.committed[choice] = 1;
+  ra.ctl->argmax_done = 0;
+}
+
+__device__ __forceinline__ void argmax_finish(uint32_t nblk, const RunArrays& ra, Best* sb) {
+  const Best t = argmax_combine(nblk, ra, sb);
+  if (threadIdx.x == 0) commit_choice(t, ra);
 }
 
 __global__ void __launch_bounds__(kThreads) k_argmax(const double* __restrict__ scores,
@@ -1353,6 +1372,7 @@ struct CasOpts {
   uint32_t seed;
   int dbg;
   int pull_f;
+  int cnt;  // count mode: tally the reference-schedule cascade work units
 };
 
 __device__ __forceinline__ void cascade_body(const RankDev& r, const CasOpts& a,
@@ -1401,6 +1421,7 @@ __device__ __forceinline__ void cascade_body(const RankDev& r, const CasOpts& a,
     __syncwarp();
     if (lane == 0) {
       r.cstamp[s] = (static_cast<unsigned long long>(base) << 32) | (any ? base + 1 : 0u);
+      if (any && a.cnt) r.ctl->cnt_cascades += 1;
       if (any) {
         const uint32_t c0 = r.fwd.row_chunk[s], c1 = r.fwd.row_chunk[s + 1];
         qc[1] = (1ull << 32) | (c1 - c0);
@@ -1425,6 +1446,19 @@ __device__ __forceinline__ void cascade_body(const RankDev& r, const CasOpts& a,
     }
     clear_rows(fprev, r.q.rows[gp], qrows(qc, gp), W32, my_warp, n_warps, lane);
     if ((a.dbg & 4) && blockIdx.x == 0 && threadIdx.x == 0) trace(2 + (solo ? 1 : 0), L, nc);
+    if (a.cnt) {  // frontier rows and their device-graph out-edges
+      const unsigned nr = qrows(qc, g);
+      if (my_warp == 0 && lane == 0) atomicAdd(&r.ctl->cnt_cas_rows, (unsigned long long)nr);
+      unsigned long long ne = 0;
+      for (uint64_t kk = my_warp; kk < nr; kk += n_warps) {
+        const uint32_t u = __ldcg(r.q.rows[g] + kk);
+        const uint64_t b0 = r.fwd.row_off[u], b1 = r.fwd.row_off[u + 1];
+        for (uint64_t i = b0 + lane; i < b1; i += 32)  // items of one edge are consecutive
+          ne += (i == b0 || r.fwd.other[i] != r.fwd.other[i - 1]) ? 1 : 0;
+      }
+      for (int o = 16; o; o >>= 1) ne += __shfl_xor_sync(0xffffffffu, ne, o);
+      if (lane == 0 && ne) atomicAdd(&r.ctl->cnt_cas_edges, ne);
+    }
     const uint32_t stamp = base + L + 1;
     uint32_t* rows_n = r.q.rows[gn];
     uint32_t* chunks_n = r.q.chunks[gn];
@@ -1614,16 +1648,14 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_cascade(CasArgs a) {
   if (threadIdx.x == 0) s_r = a.r;
   __syncthreads();
   cg::grid_group grid = cg::this_grid();
-  const CasOpts o{a.choice, a.seed, a.dbg, a.pull_f};
+  const CasOpts o{a.choice, a.seed, a.dbg, a.pull_f, 0};
   cascade_body(s_r, o, grid, stage, s_release, reinterpret_cast<uint32_t*>(dyn_smem));
 }
 
 // ---------------------------------------------------------------- round end
-__device__ __forceinline__ void round_end_body(const RunArrays& ra, RankCtl* const* ctls,
-                                               uint32_t mu, uint32_t k, uint32_t R, double eps) {
-  if (threadIdx.x || blockIdx.x) return;
-  unsigned long long covered = 0;  // collectives.cpp:96-113 (exact u64 sum)
-  for (uint32_t t = 0; t < mu; ++t) covered += ld_volatile(&ctls[t]->visited);
+__device__ __forceinline__ void round_end_covered(const RunArrays& ra,
+                                                  unsigned long long covered, uint32_t k,
+                                                  uint32_t R, double eps) {
   const double score = __ddiv_rn(double(covered), double(R));  // runtime.cpp:130
   RunCtl* c = ra.ctl;
   const uint32_t step = c->step;
@@ -1638,6 +1670,14 @@ __device__ __forceinline__ void round_end_body(const RunArrays& ra, RankCtl* con
     c->oldscore = score;
   }
   c->step = step + 1;
+}
+
+__device__ __forceinline__ void round_end_body(const RunArrays& ra, RankCtl* const* ctls,
+                                               uint32_t mu, uint32_t k, uint32_t R, double eps) {
+  if (threadIdx.x || blockIdx.x) return;
+  unsigned long long covered = 0;  // collectives.cpp:96-113 (exact u64 sum)
+  for (uint32_t t = 0; t < mu; ++t) covered += ld_volatile(&ctls[t]->visited);
+  round_end_covered(ra, covered, k, R, eps);
 }
 
 __global__ void k_round_end(RunArrays ra, RankCtl* const* ctls, uint32_t mu, uint32_t k,
@@ -1664,12 +1704,67 @@ struct RunArgs {
   RankCtl* const* ctls;
   double* reduced;
   unsigned long long* phase_ns;  // fill, simulate, select, cascade
+  int peer;                      // 1: one partition per GPU, exchange over peer memory
+  PeerView pv;
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+
+// ---- peer exchange primitives (system-scope release/acquire over NVLink)
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+template <class T>
+__device__ __forceinline__ T ld_relaxed_sys(const T* p) {
+  return *reinterpret_cast<const volatile T*>(p);
+}
+constexpr unsigned long long kPeerTimeoutNs = 120ull * 1000 * 1000 * 1000;
+
+// Cross-GPU barrier of epoch `ep`, called by every thread of the grid: after
+// it, every write any rank made before arriving is visible here.  Lane t of
+// block 0's first warp waits for rank t; a peer that never arrives (dead
+// process) releases the wait after kPeerTimeoutNs and is reported by the host.
+__device__ __noinline__ void peer_sync(const PeerView& pv, unsigned long long ep) {
+  cg::grid_group grid = cg::this_grid();
+  __threadfence_system();
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    const unsigned lane = threadIdx.x;
+    if (lane == 0) st_release_sys(&pv.box[pv.rank]->arrive, ep);
+    if (lane < pv.world && lane != pv.rank) {
+      const unsigned long long t0 = global_ns();
+      while (ld_acquire_sys(&pv.box[lane]->arrive) < ep) {
+        if (global_ns() - t0 > kPeerTimeoutNs) {
+          atomicAdd(&pv.box[pv.rank]->timeouts, 1ull);
+          break;
+        }
+        __nanosleep(64);
+      }
+    }
+    __syncwarp();
+    __threadfence_system();
+  }
+  grid.sync();
+}
+
+// Partial scores of every rank summed in the reference's binomial-tree order
+// (collectives.cpp:51-59) straight from peer memory.
+__device__ __forceinline__ double peer_reduced(const PeerView& pv, uint32_t v) {
+  double acc[kMaxPeers];
+#pragma unroll 4
+  for (uint32_t t = 0; t < pv.world; ++t) acc[t] = __ldcg(pv.scores[t] + v);
+  for (uint32_t st = 1; st < pv.world; st <<= 1)
+    for (uint32_t t = 0; t + st < pv.world; t += 2 * st) acc[t] = __dadd_rn(acc[t], acc[t + st]);
+  return acc[0];
 }
 
 // Out-of-line phase bodies keep the register allocation of each phase local.
@@ -1734,6 +1829,11 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
   rebuild();
   bool rebuilt = true;
   const double* argsrc = a.mu > 1 ? a.reduced : a.ranks[0].scores;
+  // peer mode: this rank reduces and searches the id slice [plo, phi)
+  unsigned long long ep = a.peer ? ld_volatile(&a.pv.box[a.pv.rank]->arrive) : 0;
+  const uint32_t pslice = a.peer ? (a.n + a.pv.world - 1) / a.pv.world : 0;
+  const uint32_t plo = a.peer ? min(a.n, a.pv.rank * pslice) : 0;
+  const uint32_t phi = a.peer ? min(a.n, plo + pslice) : 0;
   for (uint32_t step = 0; step < a.k; ++step) {
     if (!rebuilt) {  // rows dirtied by the last cascade
       for (uint32_t t = 0; t < a.mu; ++t) {
@@ -1743,22 +1843,62 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
       grid.sync();
     }
     rebuilt = false;
-    if (a.mu > 1) {
-      treesum_body(a.parts, a.mu, a.n, a.reduced);
+    if (a.peer) {
+      // reduce_to_root + root argmax + broadcast (runtime.cpp:88-121) as: all
+      // partial scores final -> slice sum in binomial order + slice argmax ->
+      // publish (score, id, min-uncommitted) -> every rank picks the winner.
+      peer_sync(a.pv, ++ep);
+      argmax_partial_range(plo, phi, [&](uint32_t v) { return peer_reduced(a.pv, v); }, a.ra, sb);
+      grid.sync();
+      if (blockIdx.x == 0) {
+        const Best t = argmax_combine(gridDim.x, a.ra, sb);
+        if (threadIdx.x == 0) {
+          PeerBox* mine = a.pv.box[a.pv.rank];
+          mine->best_s = t.s;
+          mine->best_v = t.v;
+          mine->minu = t.minu;
+        }
+      }
+      peer_sync(a.pv, ++ep);
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        Best t{0.0, 0xFFFFFFFFu, 0xFFFFFFFFu};
+        for (uint32_t q = 0; q < a.pv.world; ++q) {  // ascending id slices
+          const PeerBox* b = a.pv.box[q];
+          t = best_of(t, Best{ld_relaxed_sys(&b->best_s), ld_relaxed_sys(&b->best_v),
+                              ld_relaxed_sys(&b->minu)});
+        }
+        commit_choice(t, a.ra);
+      }
+      grid.sync();
+    } else {
+      if (a.mu > 1) {
+        treesum_body(a.parts, a.mu, a.n, a.reduced);
+        grid.sync();
+      }
+      argmax_partial(argsrc, a.n, a.ra, sb);
+      grid.sync();
+      if (blockIdx.x == 0) argmax_finish(gridDim.x, a.ra, sb);
       grid.sync();
     }
-    argmax_partial(argsrc, a.n, a.ra, sb);
-    grid.sync();
-    if (blockIdx.x == 0) argmax_finish(gridDim.x, a.ra, sb);
-    grid.sync();
     phase(2);
     for (uint32_t t = 0; t < a.mu; ++t) {
       load_rank(t);
-      const CasOpts co{&a.ra.ctl->choice, 0, a.dbg, a.cas_pull_f};
+      const CasOpts co{&a.ra.ctl->choice, 0, a.dbg, a.cas_pull_f, CNT};
       run_cascade(s_r, co, stage, s_release, reinterpret_cast<uint32_t*>(dyn_smem));
       grid.sync();
     }
-    round_end_body(a.ra, a.ctls, a.mu, a.k, a.R, a.eps);
+    if (a.peer) {  // allreduce(count_visited) (runtime.cpp:129, collectives.cpp:96-113)
+      if (blockIdx.x == 0 && threadIdx.x == 0)
+        a.pv.box[a.pv.rank]->visited = ld_volatile(&a.ranks[0].ctl->visited);
+      peer_sync(a.pv, ++ep);
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long covered = 0;
+        for (uint32_t q = 0; q < a.pv.world; ++q) covered += ld_relaxed_sys(&a.pv.box[q]->visited);
+        round_end_covered(a.ra, covered, a.k, a.R, a.eps);
+      }
+    } else {
+      round_end_body(a.ra, a.ctls, a.mu, a.k, a.R, a.eps);
+    }
     grid.sync();
     phase(3);
     if (step + 1 < a.k && ld_volatile(&a.ra.ctl->rebuild_now)) {
@@ -2054,15 +2194,21 @@ void launch_round_end(RunArrays& ra, RankCtl* const* ctls_dev, uint32_t mu, uint
 void launch_run(const RankDev* ranks_dev, uint32_t mu, uint32_t k, uint32_t R, uint32_t n,
                 double eps, int cap, int jacobi, int count, int K, RunArrays& ra,
                 const double* const* parts, RankCtl* const* ctls, double* reduced,
-                unsigned long long* phase_ns, cudaStream_t s) {
+                unsigned long long* phase_ns, const PeerView* peer, int grid_share,
+                cudaStream_t s) {
   static const int dbg = getenv("DFS_DBG") ? atoi(getenv("DFS_DBG")) : 0;
   static const int spf = getenv("DFS_SIM_PULL") ? atoi(getenv("DFS_SIM_PULL")) : 4;
   static const int cpf = getenv("DFS_CAS_PULL") ? atoi(getenv("DFS_CAS_PULL")) : 8;
-  RunArgs a{ranks_dev, mu, k, R, n, eps, cap, dbg, spf, cpf, K, ra, parts, ctls, reduced, phase_ns};
+  RunArgs a{ranks_dev, mu, k, R, n, eps, cap, dbg, spf, cpf, K, ra, parts, ctls, reduced, phase_ns,
+            peer ? 1 : 0, peer ? *peer : PeerView{}};
   void* args[] = {&a};
   const int variant = jacobi ? (count ? 2 : 1) : 0;
-  DFS_CUDA(cudaLaunchCooperativeKernel(run_kernel(variant), dim3(coop_grid(2, variant)),
-                                       dim3(kThreads), args, kSimSmem, s));
+  // Ranks sharing one device (single-GPU tests of the peer protocol) split
+  // its SMs so that all their persistent grids are co-resident.
+  const int share = grid_share > 1 ? grid_share : 1;
+  const int grid = std::max(1, coop_grid(2, variant) / share);
+  DFS_CUDA(cudaLaunchCooperativeKernel(run_kernel(variant), dim3(grid), dim3(kThreads), args,
+                                       kSimSmem, s));
   ++g_launches;
 }
 

@@ -15,6 +15,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <numeric>
+#include <unistd.h>
 
 #include "hash.cuh"
 
@@ -85,6 +86,7 @@ Context::Context(int device) : device_(device) {
 Context::~Context() {
   cudaSetDevice(device_);
   if (stream_) cudaStreamSynchronize(stream_);
+  peer_close();
   arena_.release();
   if (stream_) cudaStreamDestroy(stream_);
 }
@@ -341,10 +343,28 @@ void Context::prepare(const RunConfig& cfg, const HostGraph* host_w_src, uint32_
 }
 
 Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
+  return run_impl(cfg, host_w_src, false);
+}
+
+Report Context::run_peer(const RunConfig& cfg, const HostGraph* host_w_src) {
+  if (!peer_.world) throw Error(kRuntime, "peer mode: call peer setup (export/open or link) first");
+  if (cfg.mu != peer_.world)
+    throw Error(kInvalid, "peer mode: devices must equal the peer world size");
+  return run_impl(cfg, host_w_src, true);
+}
+
+Report Context::run_impl(const RunConfig& cfg, const HostGraph* host_w_src, bool peer) {
   auto t_total = Clock::now();
   const unsigned long long launches0 = launches();
-  prepare(cfg, host_w_src);
-  const uint32_t n = g_.n, mu = cfg.mu, k = cfg.k;
+  if (peer) {
+    prepare(cfg, host_w_src, peer_.rank, peer_.world);
+    if (ranks_[0].scores != peer_.view.scores[peer_.rank])
+      throw Error(kRuntime, "peer mode: partition buffers moved since the peer setup; redo it");
+  } else {
+    prepare(cfg, host_w_src);
+  }
+  // mu: the reference's device count (report counters); nl: partitions held here
+  const uint32_t n = g_.n, mu = cfg.mu, k = cfg.k, nl = uint32_t(ranks_.size());
   cudaStream_t s = stream_;
 
   // ---- run-level device state
@@ -361,17 +381,17 @@ Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
   DFS_CUDA(cudaMemsetAsync(ra.ctl, 0, sizeof(RunCtl), s));
   DFS_CUDA(cudaMemsetAsync(ra.committed, 0, std::max<uint32_t>(n, 1), s));
   const double* argmax_src = ranks_[0].scores;
-  std::vector<RankCtl*> hctl(mu);
-  std::vector<const double*> hparts(mu);
-  for (uint32_t t = 0; t < mu; ++t) {
+  std::vector<RankCtl*> hctl(nl);
+  std::vector<const double*> hparts(nl);
+  for (uint32_t t = 0; t < nl; ++t) {
     hctl[t] = ranks_[t].ctl;
     hparts[t] = ranks_[t].scores;
   }
-  RankCtl** dctl = as<RankCtl*>(arena_.get("run.ctls", mu * sizeof(void*)));
-  const double** dparts = as<const double*>(arena_.get("run.parts", mu * sizeof(void*)));
-  DFS_CUDA(cudaMemcpyAsync(dctl, hctl.data(), mu * sizeof(void*), cudaMemcpyHostToDevice, s));
-  DFS_CUDA(cudaMemcpyAsync(dparts, hparts.data(), mu * sizeof(void*), cudaMemcpyHostToDevice, s));
-  if (mu > 1) {
+  RankCtl** dctl = as<RankCtl*>(arena_.get("run.ctls", nl * sizeof(void*)));
+  const double** dparts = as<const double*>(arena_.get("run.parts", nl * sizeof(void*)));
+  DFS_CUDA(cudaMemcpyAsync(dctl, hctl.data(), nl * sizeof(void*), cudaMemcpyHostToDevice, s));
+  DFS_CUDA(cudaMemcpyAsync(dparts, hparts.data(), nl * sizeof(void*), cudaMemcpyHostToDevice, s));
+  if (nl > 1) {
     ra.reduced = as<double>(arena_.get("run.reduced", std::max<uint32_t>(n, 1) * 8));
     argmax_src = ra.reduced;
   }
@@ -394,53 +414,58 @@ Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
     int sim_step = -2;  // simulate span: -1 initial, else the round it may rebuild after
   };
   std::vector<Span> spans;
+  size_t krun0 = size_t(-1);
 
   // Default: the whole loop as one persistent kernel (launch_run).
   // DFS_RUN_MODE=launches selects the per-phase launch sequence (same results).
-  static const bool multi = getenv("DFS_RUN_MODE") && std::string(getenv("DFS_RUN_MODE")) == "launches";
+  static const bool multi_env =
+      getenv("DFS_RUN_MODE") && std::string(getenv("DFS_RUN_MODE")) == "launches";
+  const bool multi = multi_env && !peer;  // peer mode exchanges inside k_run only
   unsigned long long* phase_ns = as<unsigned long long>(arena_.get("run.phase", 8 * 8));
   if (!multi) {
     int lj = 0;
     while ((1u << lj) < ranks_[0].J) ++lj;
-    RankDev* dranks = as<RankDev>(arena_.get("run.ranks", mu * sizeof(RankDev)));
-    DFS_CUDA(cudaMemcpyAsync(dranks, ranks_.data(), mu * sizeof(RankDev), cudaMemcpyHostToDevice, s));
+    RankDev* dranks = as<RankDev>(arena_.get("run.ranks", nl * sizeof(RankDev)));
+    DFS_CUDA(cudaMemcpyAsync(dranks, ranks_.data(), nl * sizeof(RankDev), cudaMemcpyHostToDevice, s));
     DFS_CUDA(cudaMemsetAsync(phase_ns, 0, 8 * 8, s));
     const size_t f0 = mark();
-    for (uint32_t t = 0; t < mu; ++t) launch_fill(ranks_[t], nullptr, 0, s, false);
+    for (uint32_t t = 0; t < nl; ++t) launch_fill(ranks_[t], nullptr, 0, s, false);
     const size_t f1 = mark();
     spans.push_back({f0, f1, &pt.fill});
-    launch_run(dranks, mu, k, cfg.r, n, cfg.rebuild_eps, cfg.sim_cap, cfg.jacobi, cfg.count, 53 - lj,
-               ra, dparts, dctl, ra.reduced, phase_ns, s);
+    krun0 = mark();
+    launch_run(dranks, nl, k, cfg.r, n, cfg.rebuild_eps, cfg.sim_cap, cfg.jacobi, cfg.count, 53 - lj,
+               ra, dparts, dctl, ra.reduced, phase_ns, peer ? &peer_.view : nullptr,
+               peer ? peer_.grid_share : 1, s);
   } else {
     size_t e0 = mark();
-    for (uint32_t t = 0; t < mu; ++t) launch_fill(ranks_[t], nullptr, 0, s);
+    for (uint32_t t = 0; t < nl; ++t) launch_fill(ranks_[t], nullptr, 0, s);
     size_t e1 = mark();
-    for (uint32_t t = 0; t < mu; ++t) launch_simulate(ranks_[t], cfg.jacobi, cfg.count, cfg.sim_cap, nullptr, 0, s);
+    for (uint32_t t = 0; t < nl; ++t) launch_simulate(ranks_[t], cfg.jacobi, cfg.count, cfg.sim_cap, nullptr, 0, s);
     size_t e2 = mark();
-    for (uint32_t t = 0; t < mu; ++t) launch_score(ranks_[t], 1, nullptr, 0, s);
+    for (uint32_t t = 0; t < nl; ++t) launch_score(ranks_[t], 1, nullptr, 0, s);
     spans.push_back({e0, e1, &pt.fill});
     spans.push_back({e1, e2, &pt.simulate, -1});
     size_t prev = e2;
     for (uint32_t step = 0; step < k; ++step) {
       // select: rescore dirty rows, binomial-order sum, argmax (runtime.cpp:88-122)
-      for (uint32_t t = 0; t < mu; ++t) launch_score(ranks_[t], 0, rebuild, 0, s);
-      if (mu > 1) launch_treesum(dparts, mu, n, ra.reduced, s);
+      for (uint32_t t = 0; t < nl; ++t) launch_score(ranks_[t], 0, rebuild, 0, s);
+      if (nl > 1) launch_treesum(dparts, nl, n, ra.reduced, s);
       launch_argmax(argmax_src, ra, n, s);
       size_t a = mark();
       spans.push_back({prev, a, &pt.select});
       // commit + cascade (runtime.cpp:124-127) and the covered-count allreduce
-      for (uint32_t t = 0; t < mu; ++t) launch_cascade(ranks_[t], &ra.ctl->choice, 0, s);
-      launch_round_end(ra, dctl, mu, k, cfg.r, cfg.rebuild_eps, s);
+      for (uint32_t t = 0; t < nl; ++t) launch_cascade(ranks_[t], &ra.ctl->choice, 0, s);
+      launch_round_end(ra, dctl, nl, k, cfg.r, cfg.rebuild_eps, s);
       size_t b = mark();
       spans.push_back({a, b, &pt.cascade});
       prev = b;
       if (step + 1 < k) {  // eps-gated rebuild (runtime.cpp:139-153), predicated on device
-        for (uint32_t t = 0; t < mu; ++t) launch_fill(ranks_[t], rebuild, 1, s, true);
+        for (uint32_t t = 0; t < nl; ++t) launch_fill(ranks_[t], rebuild, 1, s, true);
         size_t c = mark();
-        for (uint32_t t = 0; t < mu; ++t)
+        for (uint32_t t = 0; t < nl; ++t)
           launch_simulate(ranks_[t], cfg.jacobi, cfg.count, cfg.sim_cap, rebuild, 1, s);
         size_t d = mark();
-        for (uint32_t t = 0; t < mu; ++t) launch_score(ranks_[t], 1, rebuild, 1, s);
+        for (uint32_t t = 0; t < nl; ++t) launch_score(ranks_[t], 1, rebuild, 1, s);
         spans.push_back({b, c, &pt.fill});
         spans.push_back({c, d, &pt.simulate, int(step)});
         prev = d;
@@ -449,6 +474,15 @@ Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
   }
   size_t eend = mark();
   sync();
+  if (peer) {
+    PeerBox b{};
+    DFS_CUDA(cudaMemcpy(&b, peer_.box, sizeof b, cudaMemcpyDeviceToHost));
+    if (b.timeouts != peer_.timeouts_seen) {
+      peer_.timeouts_seen = b.timeouts;
+      throw Error(kRuntime, "peer mode: a peer did not reach a round barrier in time "
+                            "(peer process failed?); results are invalid");
+    }
+  }
   if (getenv("DFS_DBG") && (atoi(getenv("DFS_DBG")) & 4)) dump_trace();
 
   // ---- results
@@ -469,7 +503,7 @@ Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
     DFS_CUDA(cudaMemcpy(rep.rebuild_rounds.data(), ra.rebuild_rounds, rc.n_rebuilds * 4,
                         cudaMemcpyDeviceToHost));
   rep.saturated = rc.saturated != 0;
-  for (uint32_t t = 0; t < mu; ++t) {
+  for (uint32_t t = 0; t < nl; ++t) {
     RankCtl c{};
     DFS_CUDA(cudaMemcpy(&c, ranks_[t].ctl, sizeof c, cudaMemcpyDeviceToHost));
     if (c.error) {
@@ -487,6 +521,9 @@ Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
     rep.cnt_touched += c.cnt_touched;
     rep.cnt_sweeps += c.cnt_sweeps;
     rep.cnt_convergences += c.cnt_convergences;
+    rep.cnt_cas_rows += c.cnt_cas_rows;
+    rep.cnt_cas_edges += c.cnt_cas_edges;
+    rep.cnt_cascades += c.cnt_cascades;
   }
   for (uint32_t sd : rep.seeds_dense) rep.seeds.push_back(orig_id_[sd]);
   // comms counters of the reference's collective schedule (collectives.cpp:
@@ -502,7 +539,7 @@ Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
     pt.select += hp[2] * 1e-9;
     pt.cascade += hp[3] * 1e-9;
     rep.sim_active = hp[1] * 1e-9;
-    rep.sim_launches = (1 + rep.rebuilds) * mu;
+    rep.sim_launches = (1 + rep.rebuilds) * nl;
   }
   for (const Span& sp : spans) {
     float ms = 0;
@@ -512,10 +549,14 @@ Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
         (sp.sim_step >= 0 && std::find(rep.rebuild_rounds.begin(), rep.rebuild_rounds.end(),
                                        uint32_t(sp.sim_step)) != rep.rebuild_rounds.end())) {
       rep.sim_active += ms * 1e-3;
-      rep.sim_launches += mu;
+      rep.sim_launches += nl;
     }
   }
-  (void)eend;
+  if (krun0 != size_t(-1)) {
+    float ms = 0;
+    DFS_CUDA(cudaEventElapsedTime(&ms, ev[krun0], ev[eend]));
+    rep.run_kernel = ms * 1e-3;
+  }
   for (cudaEvent_t e : ev) cudaEventDestroy(e);
   pt.upload = last_.upload;
   pt.total = since(t_total);
@@ -523,6 +564,144 @@ Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
   rep.timings = pt;
   last_ = pt;
   return rep;
+}
+
+// ---------------------------------------------------------------- peer mode
+// One FASST partition per GPU; the per-round exchange runs inside k_run over
+// peer memory.  Setup only maps buffers: rank t's mailbox and
+// its partial-score vector (the send buffer of the reference's reduce_to_root,
+// collectives.cpp:44-64) become directly addressable by every other rank.
+namespace {
+struct PeerHandle {
+  cudaIpcMemHandle_t box, scores;
+  unsigned char uuid[16];
+  int64_t pid;
+};
+static_assert(sizeof(PeerHandle) <= kPeerHandleBytes, "peer handle layout");
+
+void device_uuid(int dev, unsigned char out[16]) {
+  cudaDeviceProp p{};
+  DFS_CUDA(cudaGetDeviceProperties(&p, dev));
+  std::memcpy(out, &p.uuid, 16);
+}
+}  // namespace
+
+PeerBox* Context::peer_box() {
+  return as<PeerBox>(arena_.get("peer.box", sizeof(PeerBox)));
+}
+
+void Context::peer_close() {
+  for (void* p : peer_.opened) cudaIpcCloseMemHandle(p);
+  peer_ = PeerState{};
+}
+
+static void check_partition(const std::vector<RankDev>& ranks, const RunConfig& cfg,
+                            uint32_t rank, uint32_t world) {
+  if (world < 2 || world > kMaxPeers)
+    throw Error(kInvalid, "peer mode: world size must be in [2, " + std::to_string(kMaxPeers) + "]");
+  if (rank >= world) throw Error(kInvalid, "peer mode: rank out of range");
+  if (ranks.size() != 1 || cfg.mu != world || ranks[0].tau != rank)
+    throw Error(kRuntime, "peer mode: prepare this context as partition rank of world first");
+}
+
+void Context::peer_export(void* out) {
+  DFS_CUDA(cudaSetDevice(device_));
+  if (ranks_.size() != 1) throw Error(kRuntime, "peer mode: prepare a single partition first");
+  peer_close();
+  PeerBox* box = peer_box();
+  DFS_CUDA(cudaMemsetAsync(box, 0, sizeof(PeerBox), stream_));  // barrier epochs restart at 0
+  sync();
+  PeerHandle h{};
+  DFS_CUDA(cudaIpcGetMemHandle(&h.box, box));
+  DFS_CUDA(cudaIpcGetMemHandle(&h.scores, ranks_[0].scores));
+  device_uuid(device_, h.uuid);
+  h.pid = int64_t(getpid());
+  std::memset(out, 0, kPeerHandleBytes);
+  std::memcpy(out, &h, sizeof h);
+}
+
+void Context::peer_open(uint32_t rank, uint32_t world, const void* handles) {
+  DFS_CUDA(cudaSetDevice(device_));
+  check_partition(ranks_, cfg_, rank, world);
+  for (void* p : peer_.opened) cudaIpcCloseMemHandle(p);
+  peer_.opened.clear();
+  PeerState ps;
+  ps.world = world;
+  ps.rank = rank;
+  ps.box = peer_box();
+  ps.view.world = world;
+  ps.view.rank = rank;
+  unsigned char me[16];
+  device_uuid(device_, me);
+  const auto* hs = static_cast<const unsigned char*>(handles);
+  ps.grid_share = 0;
+  for (uint32_t t = 0; t < world; ++t) {
+    PeerHandle h;
+    std::memcpy(&h, hs + size_t(t) * kPeerHandleBytes, sizeof h);
+    if (std::memcmp(h.uuid, me, 16) == 0) ++ps.grid_share;
+    if (t == rank) {
+      ps.view.box[t] = ps.box;
+      ps.view.scores[t] = ranks_[0].scores;
+      continue;
+    }
+    if (h.pid == int64_t(getpid()))
+      throw Error(kInvalid, "peer mode: same-process peers must be linked with peer_link");
+    void* pb = nullptr;
+    void* psc = nullptr;
+    DFS_CUDA(cudaIpcOpenMemHandle(&pb, h.box, cudaIpcMemLazyEnablePeerAccess));
+    ps.opened.push_back(pb);
+    DFS_CUDA(cudaIpcOpenMemHandle(&psc, h.scores, cudaIpcMemLazyEnablePeerAccess));
+    ps.opened.push_back(psc);
+    ps.view.box[t] = static_cast<PeerBox*>(pb);
+    ps.view.scores[t] = static_cast<const double*>(psc);
+  }
+  if (ps.grid_share < 1) ps.grid_share = 1;
+  peer_ = std::move(ps);
+}
+
+void Context::peer_link(const std::vector<Context*>& ctxs) {
+  const uint32_t world = uint32_t(ctxs.size());
+  for (uint32_t i = 0; i < world; ++i) {
+    Context* c = ctxs[i];
+    check_partition(c->ranks_, c->cfg_, i, world);
+    DFS_CUDA(cudaSetDevice(c->device_));
+    c->peer_close();
+    PeerBox* box = c->peer_box();
+    DFS_CUDA(cudaMemset(box, 0, sizeof(PeerBox)));
+  }
+  for (uint32_t i = 0; i < world; ++i) {
+    Context* c = ctxs[i];
+    DFS_CUDA(cudaSetDevice(c->device_));
+    PeerState ps;
+    ps.world = world;
+    ps.rank = i;
+    ps.box = c->peer_box();
+    ps.view.world = world;
+    ps.view.rank = i;
+    ps.grid_share = 0;
+    for (uint32_t t = 0; t < world; ++t) {
+      Context* o = ctxs[t];
+      if (o->device_ == c->device_) {
+        // Two persistent grids of one process on one device cannot be relied
+        // on to run concurrently (device-synchronising runtime calls and
+        // cooperative-launch serialisation): use one process per rank there.
+        if (o != c)
+          throw Error(kInvalid, "peer mode: same-process peers must be on distinct devices "
+                                "(use one process per rank, dfs_peer_export/open)");
+        ++ps.grid_share;
+      } else {
+        int can = 0;
+        DFS_CUDA(cudaDeviceCanAccessPeer(&can, c->device_, o->device_));
+        if (!can) throw Error(kRuntime, "peer mode: no P2P access between the peer devices");
+        const cudaError_t e = cudaDeviceEnablePeerAccess(o->device_, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) DFS_CUDA(e);
+        cudaGetLastError();
+      }
+      ps.view.box[t] = o->peer_box();
+      ps.view.scores[t] = o->ranks_[0].scores;
+    }
+    c->peer_ = std::move(ps);
+  }
 }
 
 // ---------------------------------------------------------------- stage API

@@ -65,12 +65,30 @@ struct Report {  // runtime.hpp:29-41
   uint64_t items_fwd = 0, items_rev = 0, device_edges = 0;
   // reference-schedule units (count mode), summed over ranks and convergences
   uint64_t cnt_edges = 0, cnt_batches = 0, cnt_touched = 0, cnt_sweeps = 0, cnt_convergences = 0;
+  uint64_t cnt_cas_rows = 0, cnt_cas_edges = 0, cnt_cascades = 0;
+  double run_kernel = 0;        // seconds of the k_run launch (CUDA events on the stream)
   uint64_t launches = 0;        // kernels launched by run()
   double sim_active = 0;        // seconds of simulate launches that ran (not gated off)
   uint32_t sim_launches = 0;    // simulate launches that ran
 };
 
 std::string report_to_json(const Report& rep, bool include_timings);
+
+// Peer (multi-GPU) session of one context: which partition it holds, the
+// mapped mailboxes / partial-score vectors of every rank, and the share of
+// the GPU its persistent kernel may occupy (> 1 when several ranks' contexts
+// live on one device, e.g. the single-GPU tests of the peer protocol).
+struct PeerState {
+  uint32_t world = 0, rank = 0;
+  int grid_share = 1;
+  PeerView view{};
+  PeerBox* box = nullptr;
+  std::vector<void*> opened;  // IPC mappings (closed on re-setup / destruction)
+  unsigned long long timeouts_seen = 0;
+};
+// Exported handle: IPC handles of the mailbox and the partial-score vector,
+// the device UUID and the process id.
+constexpr size_t kPeerHandleBytes = 2 * 64 + 16 + 8;
 
 class Context {
  public:
@@ -114,7 +132,20 @@ class Context {
   const PhaseTimings& last_timings() const { return last_; }
   void sync();
 
+  // ---- peer mode (one FASST partition per GPU; exchange inside k_run)
+  // After prepare(cfg, host, rank, world): write this rank's handle.
+  void peer_export(void* out);
+  // Map every rank's exported buffers (handles: world * kPeerHandleBytes).
+  void peer_open(uint32_t rank, uint32_t world, const void* handles);
+  // Same-process peers (one context per partition, distinct devices): direct pointers.
+  static void peer_link(const std::vector<Context*>& ctxs);
+  void peer_close();
+  Report run_peer(const RunConfig& cfg, const HostGraph* host_w_src = nullptr);
+  const PeerState& peer() const { return peer_; }
+
  private:
+  Report run_impl(const RunConfig& cfg, const HostGraph* host_w_src, bool peer);
+  PeerBox* peer_box();
   void build_items(RankDev& r);
   void finish_items(RankDev& r, int dir, const uint64_t* pos);
   void alloc_rank(RankDev& r, uint32_t tau);
@@ -133,6 +164,7 @@ class Context {
   std::vector<RankDev> ranks_;
   PhaseTimings last_{};
   double prep_seconds_ = 0;
+  PeerState peer_{};
 };
 
 }  // namespace dfs

@@ -176,4 +176,40 @@ class DistRunner:
         return self.run(**kw)
 
 
-__all__ = ["binomial_sum", "select_seed", "allreduce_count", "DistRunner", "_capi"]
+class PeerRunner:
+    """One rank (one GPU, one process) of a multi-GPU run in PEER mode: the
+    whole greedy loop is one persistent kernel per GPU and the per-round
+    exchange (binomial-order partial-score reduce, argmax, seed broadcast,
+    visited-count allreduce; runtime.cpp:88-130) happens inside it over
+    NVLink peer memory (CUDA IPC mappings of every rank's mailbox and partial
+    score vector).  torch.distributed is used only to swap the IPC handles.
+    """
+
+    def __init__(self, ctx, graph, rank: int, world: int, group=None):
+        self.ctx, self.g, self.rank, self.world, self.group = ctx, graph, rank, world, group
+        self._key = None
+
+    def setup(self, k=10, r=256, mode="fasst", weights="const:0.1", rebuild_eps=0.01, seed=0,
+              resident=True):
+        if dist.is_initialized():
+            dist.barrier(group=self.group)  # no peer kernel of a previous run is still reading
+        self.ctx.prepare_partition(None if resident else self.g, self.rank, self.world, k=k, r=r,
+                                   mode=mode, weights=weights, rebuild_eps=rebuild_eps, seed=seed,
+                                   resident=resident)
+        mine = self.ctx.peer_export()
+        handles = [None] * self.world
+        dist.all_gather_object(handles, mine, group=self.group)
+        self.ctx.peer_open(self.rank, self.world, handles)
+        self._key = (self.g.n, self.g.m, r, mode)
+
+    def run_json(self, k=10, r=256, mode="fasst", weights="const:0.1", rebuild_eps=0.01, seed=0,
+                 resident=True, timings=False):
+        if self._key != (self.g.n, self.g.m, r, mode):
+            self.setup(k=k, r=r, mode=mode, weights=weights, rebuild_eps=rebuild_eps, seed=seed,
+                       resident=True)
+        return self.ctx.run_peer_json(None if resident else self.g, k=k, r=r, devices=self.world,
+                                      mode=mode, weights=weights, rebuild_eps=rebuild_eps,
+                                      seed=seed, timings=timings, resident=resident)
+
+
+__all__ = ["binomial_sum", "select_seed", "allreduce_count", "DistRunner", "PeerRunner", "_capi"]
