@@ -379,6 +379,10 @@ __global__ void k_small_items(uint32_t nsmall, const uint32_t* __restrict__ smal
 }
 
 // ---------------------------------------------------------------- fill
+// 4 mask bits -> 4 bytes of 0xFF / 0x00.
+__device__ __forceinline__ uint32_t expand4(uint32_t m4) {
+  return ((m4 * 0x00204081u) & 0x01010101u) * 0xFFu;
+}
 // sketch.cpp:55-66: M[u][j] = clz64(fmix64(jkey[j] + u*golden)) unless VISITED.
 // One thread per 4 registers (one u32 store, coalesced across the warp).
 // use_pristine: registers are the cached first fill with VISITED re-applied
@@ -405,24 +409,27 @@ __device__ __forceinline__ void fill_body(uint32_t n, uint32_t J, uint32_t Jp,
     }
     return;
   }
-  // warp per row, lanes over 4-register words (coalesced u32 stores)
+  // warp per row, lanes over 4-register words (coalesced u32 stores).  The
+  // four hashes of a word are independent (keys fetched as two 16-byte
+  // loads, pads have key 0 and are masked after), no per-register branches.
   for (uint64_t u = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; u < n; u += nw) {
     const uint64_t ug = u * kGolden;
     uint32_t* row = reinterpret_cast<uint32_t*>(regs + u * Jp);
     uint32_t* prow = pristine ? reinterpret_cast<uint32_t*>(pristine + u * Jp) : nullptr;
     for (uint32_t w = lane_id(); w < q; w += 32) {
       const uint32_t j0 = w * 4;
-      const uint32_t vb = vis[u * W32 + (j0 >> 5)] >> (j0 & 31);
-      uint32_t word = 0, pw = 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t j = j0 + k;
-        uint32_t h = 0xFFu;
-        if (j < J) h = uint32_t(__clzll(fmix64(__ldg(jkey + j) + ug)));
-        pw |= h << (8 * k);
-        word |= (((vb >> k) & 1u) ? 0xFFu : h) << (8 * k);
+      const ulonglong2 k01 = __ldg(reinterpret_cast<const ulonglong2*>(jkey + j0));
+      const ulonglong2 k23 = __ldg(reinterpret_cast<const ulonglong2*>(jkey + j0 + 2));
+      const uint32_t vb = (vis[u * W32 + (j0 >> 5)] >> (j0 & 31)) & 15u;
+      uint32_t pw = uint32_t(__clzll(fmix64(k01.x + ug))) |
+                    (uint32_t(__clzll(fmix64(k01.y + ug))) << 8) |
+                    (uint32_t(__clzll(fmix64(k23.x + ug))) << 16) |
+                    (uint32_t(__clzll(fmix64(k23.y + ug))) << 24);
+      if (j0 + 4 > J) {  // pad registers are VISITED
+        const uint32_t live = J > j0 ? J - j0 : 0;  // < 4
+        pw |= 0xFFFFFFFFu << (8 * live);
       }
-      row[w] = word;
+      row[w] = pw | expand4(vb);
       if (prow) prow[w] = pw;
     }
   }
@@ -440,9 +447,6 @@ __global__ void k_fill(uint32_t n, uint32_t J, uint32_t Jp, const uint64_t* __re
 // Byte-wise merge of 4 registers: dst takes max(dst, src) on live simulations;
 // VISITED (-1) in dst is absorbing, VISITED in src never wins
 // (engine.cpp:22-53).  bm = 0xFF per live byte.
-__device__ __forceinline__ uint32_t expand4(uint32_t m4) {
-  return ((m4 * 0x00204081u) & 0x01010101u) * 0xFFu;
-}
 __device__ __forceinline__ uint32_t merge4(uint32_t d, uint32_t s, uint32_t bm) {
   const uint32_t sm = (s & bm) | (0x80808080u & ~bm);  // dead sims -> -128, never win
   return __vmaxs4(d, sm) | __vcmpeq4(d, 0xFFFFFFFFu);   // keep VISITED
@@ -1155,6 +1159,22 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) 
 // below 2^53 * 2^-K, so the reference's double sum is exact and equals the
 // integer sum sum 2^(K-M[j]) scaled by 2^-K.  Rows with a
 // larger register fall back to the sequential double sum.
+// 16 registers: live count, running byte max, exact double sum of 2^-r.
+__device__ __forceinline__ void score_acc(uint4 v, uint32_t& live, uint32_t& mx4, double& den) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    live += __popc(~w[i] & 0x80808080u);
+    mx4 = __vmaxs4(mx4, w[i]);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int rv = int(int8_t(w[i] >> (8 * b)));
+      // 2^-rv built from its exponent bits (rv <= 64 keeps it normal)
+      if (rv >= 0) den += __hiloint2double((1023 - rv) << 20, 0);
+    }
+  }
+}
+
 __device__ __forceinline__ void score_body(const int8_t* __restrict__ regs, uint32_t n, uint32_t J,
                                            uint32_t Jp, int K, int full,
                                            const uint32_t* __restrict__ rows, RankCtl* ctl,
@@ -1162,45 +1182,73 @@ __device__ __forceinline__ void score_body(const int8_t* __restrict__ regs, uint
   const uint32_t nrows = full ? n : ld_volatile(&ctl->dirty_count);
   const unsigned lane = lane_id();
   const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t k = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; k < nrows; k += nw) {
-    const uint32_t u = full ? uint32_t(k) : rows[k];
-    const uint32_t* row = reinterpret_cast<const uint32_t*>(regs + uint64_t(u) * Jp);
-    uint32_t live = 0;
-    int mx = 0;
-    unsigned long long isum = 0;
-    for (uint32_t q = lane; q < Jp / 4; q += 32) {
-      const uint32_t wv = __ldcg(row + q);
+  const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  // G lanes per row (power of two <= the row's 16-byte words), R rows per
+  // warp, two row groups per step: every lane keeps up to 8 independent
+  // 16-byte loads in flight before reducing (the score is a streaming pass).
+  const uint32_t q16 = Jp >> 4;
+  uint32_t G = 32;
+  while (G > q16) G >>= 1;
+  const uint32_t R = 32 / G, sub = lane / G, sl = lane % G;
+  const uint4 kDead = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+  for (uint64_t k0 = gw * 2 * R; k0 < nrows; k0 += nw * 2 * R) {
+    uint32_t u[2], live[2] = {0, 0}, mx4[2] = {0, 0};
+    bool ok[2];
+    double den[2] = {0.0, 0.0};
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int rv = int(int8_t(wv >> (8 * b)));
-        if (rv >= 0) {
-          ++live;
-          mx = max(mx, rv);
-          if (rv <= K) isum += 1ull << (K - rv);
+    for (int h = 0; h < 2; ++h) {
+      const uint64_t kk = k0 + h * R + sub;
+      ok[h] = kk < nrows;
+      u[h] = ok[h] ? (full ? uint32_t(kk) : __ldcg(rows + kk)) : 0;
+    }
+    for (uint32_t w0 = sl; w0 < q16; w0 += 4 * G) {
+      uint4 va[2][4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint4* rp = reinterpret_cast<const uint4*>(regs + uint64_t(u[h]) * Jp);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const uint32_t idx = w0 + t * G;
+          va[h][t] = (ok[h] && idx < q16) ? __ldcs(rp + idx) : kDead;
         }
       }
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) score_acc(va[h][t], live[h], mx4[h], den[h]);
     }
-    for (int o = 16; o; o >>= 1) {
-      live += __shfl_xor_sync(0xffffffffu, live, o);
-      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      isum += __shfl_xor_sync(0xffffffffu, isum, o);
-    }
-    if (lane == 0) {
-      double sc = 0.0;
-      if (live) {
-        double denom;
-        if (mx <= K) {
-          denom = ldexp(double(isum), -K);
-        } else {  // exact sequential replay (rare)
-          denom = 0.0;
-          const int8_t* rb = regs + uint64_t(u) * Jp;
-          for (uint32_t j = 0; j < J; ++j)
-            if (rb[j] >= 0) denom = __dadd_rn(denom, ldexp(1.0, -int(rb[j])));
-        }
-        const double lv = double(live);
-        sc = __ddiv_rn(__dmul_rn(lv, lv), __dmul_rn(denom, kPhi));
+    for (uint32_t o = G >> 1; o; o >>= 1) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        live[h] += __shfl_xor_sync(0xffffffffu, live[h], o);
+        mx4[h] = __vmaxs4(mx4[h], __shfl_xor_sync(0xffffffffu, mx4[h], o));
+        den[h] += __shfl_xor_sync(0xffffffffu, den[h], o);
       }
-      scores[u] = sc;
+    }
+    if (sl == 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (!ok[h]) continue;
+        const uint32_t m = mx4[h];
+        const int mx = max(max(int(m & 0xFF), int((m >> 8) & 0xFF)),
+                           max(int((m >> 16) & 0xFF), int(m >> 24)));
+        double sc = 0.0;
+        if (live[h]) {
+          // Every live register <= K with J * 2^K <= 2^53: each partial sum of
+          // 2^-r is an exact multiple of 2^-K, so any summation order equals
+          // the reference's sequential sum (sketch.cpp:122-126) bit for bit.
+          double denom = den[h];
+          if (mx > K) {  // exact sequential replay (rare)
+            denom = 0.0;
+            const int8_t* rb = regs + uint64_t(u[h]) * Jp;
+            for (uint32_t j = 0; j < J; ++j)
+              if (rb[j] >= 0) denom = __dadd_rn(denom, ldexp(1.0, -int(rb[j])));
+          }
+          const double lv = double(live[h]);
+          sc = __ddiv_rn(__dmul_rn(lv, lv), __dmul_rn(denom, kPhi));
+        }
+        scores[u[h]] = sc;
+      }
     }
   }
 }
