@@ -397,14 +397,43 @@ __device__ __forceinline__ void fill_body(uint32_t n, uint32_t J, uint32_t Jp,
   const uint32_t q = Jp >> 2;
   const uint32_t W32 = Jp >> 5;
   const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  if (use_pristine && pristine) {  // pure streaming copy, warp per row
-    for (uint64_t u = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; u < n; u += nw) {
-      const uint32_t* src = reinterpret_cast<const uint32_t*>(pristine + u * Jp);
-      uint32_t* dst = reinterpret_cast<uint32_t*>(regs + u * Jp);
-      for (uint32_t w = lane_id(); w < q; w += 32) {
-        const uint32_t j0 = w * 4;
-        const uint32_t vb = (__ldcg(vis + u * W32 + (j0 >> 5)) >> (j0 & 31)) & 15u;
-        dst[w] = __ldcs(src + w) | (((vb * 0x00204081u) & 0x01010101u) * 0xFFu);
+  if (use_pristine && pristine) {
+    // Streaming copy (16-byte vectors, G lanes per row, 4 loads in flight
+    // per lane) with the VISITED bits re-applied.
+    const uint32_t q16 = Jp >> 4;
+    uint32_t G = 32;
+    while (G > q16) G >>= 1;
+    const uint32_t R = 32 / G, lane = lane_id(), sub = lane / G, sl = lane % G;
+    const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    for (uint64_t u0 = gw * R; u0 < n; u0 += nw * R) {
+      const uint64_t u = u0 + sub;
+      if (u >= n) continue;
+      const uint4* src = reinterpret_cast<const uint4*>(pristine + u * Jp);
+      uint4* dst = reinterpret_cast<uint4*>(regs + u * Jp);
+      const uint32_t* vrow = vis + u * W32;
+      for (uint32_t w0 = sl; w0 < q16; w0 += 4 * G) {
+        uint4 v[4];
+        uint32_t vb[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const uint32_t w = w0 + t * G;
+          if (w < q16) {
+            v[t] = __ldcs(src + w);
+            vb[t] = __ldcg(vrow + (w >> 1)) >> ((w & 1) * 16);
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const uint32_t w = w0 + t * G;
+          if (w < q16) {
+            uint4 o = v[t];
+            o.x |= expand4(vb[t] & 15u);
+            o.y |= expand4((vb[t] >> 4) & 15u);
+            o.z |= expand4((vb[t] >> 8) & 15u);
+            o.w |= expand4((vb[t] >> 12) & 15u);
+            dst[w] = o;
+          }
+        }
       }
     }
     return;
@@ -1159,26 +1188,59 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) 
 // below 2^53 * 2^-K, so the reference's double sum is exact and equals the
 // integer sum sum 2^(K-M[j]) scaled by 2^-K.  Rows with a
 // larger register fall back to the sequential double sum.
-// 16 registers: live count, running byte max, exact double sum of 2^-r.
-__device__ __forceinline__ void score_acc(uint4 v, uint32_t& live, uint32_t& mx4, double& den) {
+// Streaming 16-byte load that the compiler may not sink to its first use
+// (keeps a lane's batch of loads in flight together).
+__device__ __forceinline__ uint4 ld_stream_early(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.cs.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// Empty asm "rewriting" a loaded vector: compute on it cannot be hoisted
+// above this point, so a batch of ld_stream_early loads issues back to back.
+__device__ __forceinline__ void pin_after_loads(uint4& v) {
+  asm volatile("" : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w));
+}
+
+// Score lookup table (shared memory): the high words of 256 doubles (the low
+// words are 0), indexed by a register byte: live r <= K -> 2^-r; live r > K ->
+// 2^60 (flags the exact sequential fallback: without it the sum is <= J <
+// 2^50); negative bytes (VISITED) -> 0.0.  32-bit entries: one bank per
+// value, so a warp's lookups are (nearly) conflict-free.
+constexpr double kScoreFlag = 1152921504606846976.0;  // 2^60
+__device__ __forceinline__ void score_table(uint32_t* tbl, int K) {
+  for (int b = threadIdx.x; b < 256; b += blockDim.x)
+    tbl[b] = b >= 128 ? 0u : uint32_t(__double2hiint(b <= K ? ldexp(1.0, -b) : kScoreFlag));
+  __syncthreads();
+}
+
+__device__ __forceinline__ double score_term(const uint32_t* tbl, uint32_t w, uint32_t sel) {
+  return __hiloint2double(int(tbl[__byte_perm(w, 0, sel)]), 0);
+}
+
+// 16 registers: live count and the sum of table terms (pairwise tree: short
+// dependency chains; the sum is exact in any order, see score_body).
+__device__ __forceinline__ void score_acc(uint4 v, const uint32_t* tbl, uint32_t& live,
+                                          double& den) {
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  double p[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     live += __popc(~w[i] & 0x80808080u);
-    mx4 = __vmaxs4(mx4, w[i]);
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int rv = int(int8_t(w[i] >> (8 * b)));
-      // 2^-rv built from its exponent bits (rv <= 64 keeps it normal)
-      if (rv >= 0) den += __hiloint2double((1023 - rv) << 20, 0);
-    }
+    p[i] = (score_term(tbl, w[i], 0x4440) + score_term(tbl, w[i], 0x4441)) +
+           (score_term(tbl, w[i], 0x4442) + score_term(tbl, w[i], 0x4443));
   }
+  den += (p[0] + p[1]) + (p[2] + p[3]);
 }
 
+// Called by every thread of a block; tbl: 256 words of shared memory.
 __device__ __forceinline__ void score_body(const int8_t* __restrict__ regs, uint32_t n, uint32_t J,
                                            uint32_t Jp, int K, int full,
                                            const uint32_t* __restrict__ rows, RankCtl* ctl,
-                                           double* __restrict__ scores) {
+                                           double* __restrict__ scores, uint32_t* tbl) {
+  score_table(tbl, K);
   const uint32_t nrows = full ? n : ld_volatile(&ctl->dirty_count);
   const unsigned lane = lane_id();
   const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
@@ -1192,7 +1254,7 @@ __device__ __forceinline__ void score_body(const int8_t* __restrict__ regs, uint
   const uint32_t R = 32 / G, sub = lane / G, sl = lane % G;
   const uint4 kDead = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
   for (uint64_t k0 = gw * 2 * R; k0 < nrows; k0 += nw * 2 * R) {
-    uint32_t u[2], live[2] = {0, 0}, mx4[2] = {0, 0};
+    uint32_t u[2], live[2] = {0, 0};
     bool ok[2];
     double den[2] = {0.0, 0.0};
 #pragma unroll
@@ -1207,21 +1269,25 @@ __device__ __forceinline__ void score_body(const int8_t* __restrict__ regs, uint
       for (int h = 0; h < 2; ++h) {
         const uint4* rp = reinterpret_cast<const uint4*>(regs + uint64_t(u[h]) * Jp);
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
+        for (int t = 0; t < 4; ++t) {  // unconditional (clamped) loads: all 8 in flight
           const uint32_t idx = w0 + t * G;
-          va[h][t] = (ok[h] && idx < q16) ? __ldcs(rp + idx) : kDead;
+          va[h][t] = ld_stream_early(rp + (idx < q16 ? idx : q16 - 1));
+          if (!ok[h] || idx >= q16) va[h][t] = kDead;
         }
       }
 #pragma unroll
       for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int t = 0; t < 4; ++t) score_acc(va[h][t], live[h], mx4[h], den[h]);
+        for (int t = 0; t < 4; ++t) pin_after_loads(va[h][t]);
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) score_acc(va[h][t], tbl, live[h], den[h]);
     }
     for (uint32_t o = G >> 1; o; o >>= 1) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         live[h] += __shfl_xor_sync(0xffffffffu, live[h], o);
-        mx4[h] = __vmaxs4(mx4[h], __shfl_xor_sync(0xffffffffu, mx4[h], o));
         den[h] += __shfl_xor_sync(0xffffffffu, den[h], o);
       }
     }
@@ -1229,16 +1295,13 @@ __device__ __forceinline__ void score_body(const int8_t* __restrict__ regs, uint
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         if (!ok[h]) continue;
-        const uint32_t m = mx4[h];
-        const int mx = max(max(int(m & 0xFF), int((m >> 8) & 0xFF)),
-                           max(int((m >> 16) & 0xFF), int(m >> 24)));
         double sc = 0.0;
         if (live[h]) {
           // Every live register <= K with J * 2^K <= 2^53: each partial sum of
           // 2^-r is an exact multiple of 2^-K, so any summation order equals
           // the reference's sequential sum (sketch.cpp:122-126) bit for bit.
           double denom = den[h];
-          if (mx > K) {  // exact sequential replay (rare)
+          if (denom >= 1125899906842624.0) {  // a register > K (2^50): exact sequential replay
             denom = 0.0;
             const int8_t* rb = regs + uint64_t(u[h]) * Jp;
             for (uint32_t j = 0; j < J; ++j)
@@ -1257,7 +1320,8 @@ __global__ void k_score(const int8_t* __restrict__ regs, uint32_t n, uint32_t J,
                         int K, int full, const uint32_t* __restrict__ rows, RankCtl* ctl,
                         double* __restrict__ scores, const unsigned int* gate, unsigned int want) {
   if (gate && ld_volatile(gate) != want) return;
-  score_body(regs, n, J, Jp, K, full, rows, ctl, scores);
+  __shared__ uint32_t tbl[256];
+  score_body(regs, n, J, Jp, K, full, rows, ctl, scores, tbl);
 }
 
 // ---------------------------------------------------------------- reduce/argmax
@@ -1870,7 +1934,8 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
     phase(1);
     for (uint32_t t = 0; t < a.mu; ++t) {
       load_rank(t);
-      score_body(s_r.regs, s_r.n, s_r.J, s_r.Jp, a.K, 1, s_r.dirty, s_r.ctl, s_r.scores);
+      score_body(s_r.regs, s_r.n, s_r.J, s_r.Jp, a.K, 1, s_r.dirty, s_r.ctl, s_r.scores,
+                 reinterpret_cast<uint32_t*>(dyn_smem));
     }
     grid.sync();
   };
@@ -1886,7 +1951,8 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
     if (!rebuilt) {  // rows dirtied by the last cascade
       for (uint32_t t = 0; t < a.mu; ++t) {
         load_rank(t);
-        score_body(s_r.regs, s_r.n, s_r.J, s_r.Jp, a.K, 0, s_r.dirty, s_r.ctl, s_r.scores);
+        score_body(s_r.regs, s_r.n, s_r.J, s_r.Jp, a.K, 0, s_r.dirty, s_r.ctl, s_r.scores,
+                   reinterpret_cast<uint32_t*>(dyn_smem));
       }
       grid.sync();
     }

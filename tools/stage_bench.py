@@ -33,3 +33,4 @@ def timed(f, reps=3):
 print("fill ms", timed(lambda: ctx.fill(0)))
 print("simulate ms", timed(lambda: (ctx.fill(0), ctx.simulate(0)), reps=2))
 print("scores(D2H incl) ms", timed(lambda: ctx.scores(0), reps=2))
+del ctx, g
