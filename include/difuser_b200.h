@@ -153,6 +153,17 @@ int dfs_set_registers(dfs_ctx *ctx, uint32_t tau, const int8_t *in_nJ);
 /* {updates, items, edges, batches, touched, sweeps, convergences, visited} */
 int dfs_rank_counters(dfs_ctx *ctx, uint32_t tau, uint64_t out[8]);
 
+/* ---- FASST analytics (proj/src/fasst.cpp:101-168; CLI partition-stats /
+ * fillrate, tools/difuser.cpp:116-159) on the resident graph (g: for
+ * normal/uniform weights, else nullable).  cfg: r, devices (= mu), mode,
+ * weights, seed.  Outputs (exact integer counts; fractions are count / m):
+ * dup_count[mu+1] edges sampled by exactly k chunks (duplication_stats),
+ * loads[mu] per-chunk sampled edges (device_edge_loads), fill[2] = {live
+ * lanes, counted batches} over 32-lane batches of X (fill_rate; {0, 0} and
+ * return DFS_OK when r % 32 != 0 — the reference throws there). */
+int dfs_fasst_stats(dfs_ctx *ctx, const dfs_graph *g, const dfs_config *cfg,
+                    uint64_t *dup_count, uint64_t *loads, uint64_t fill[2]);
+
 /* ---- peer (multi-GPU) mode ----------------------------------------------
  * One FASST partition per GPU (one process per GPU, or one context per
  * partition in one process).  Replaces the per-device worker threads and the

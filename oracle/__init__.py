@@ -77,6 +77,10 @@ def lib():
         L.dor_commit_cascade.restype = C.c_uint64
         L.dor_commit_cascade.argtypes = [C.c_uint32, _u64p, _u32p, _u64p, C.c_uint32,
                                          _i8p, _u64p, C.c_uint32]
+        L.dor_fasst_stats.restype = None
+        L.dor_fasst_stats.argtypes = [C.c_uint64, _u32p, _u32p, _u32p, _u32p, C.c_uint32,
+                                      C.c_uint32, _u64p, _u64p, C.POINTER(C.c_uint64),
+                                      C.POINTER(C.c_uint64)]
         L.dor_run.restype = C.c_int
         L.dor_run.argtypes = [C.c_uint32, C.c_uint64, _u64p, _u32p, _u32p, C.c_uint32,
                               C.c_uint32, C.c_uint32, C.c_int, C.c_double, C.c_uint64,
@@ -223,6 +227,31 @@ def make_plan(r, mu, mode, seed):
     if lib().dor_make_plan(r, mu, 1 if mode == "fasst" else 0, seed, x, order, C.byref(deg)) != 0:
         raise ValueError("make_plan: mu must divide R")
     return x, order, bool(deg.value)
+
+
+def fasst_stats(g: CSR, r, mu, mode, weights, seed):
+    """duplication_stats / device_edge_loads / fill_rate (fasst.cpp:101-168),
+    returned in the layout of oracle/refprobe.cpp's fasst_stats."""
+    xs, order, _ = make_plan(r, mu, mode, seed)
+    # fill_rate sorts X itself for FASST and keeps generation order otherwise
+    xfill = np.sort(xs, kind="stable") if mode == "fasst" else xs
+    w = np.ascontiguousarray(g.weights(weights, seed), np.uint32)
+    dup = np.zeros(mu + 1, np.uint64)
+    loads = np.zeros(mu, np.uint64)
+    lanes, batches = C.c_uint64(), C.c_uint64()
+    lib().dor_fasst_stats(g.m, np.ascontiguousarray(g.ehash(), np.uint32), w, xs,
+                          np.ascontiguousarray(xfill, np.uint32), r, mu, dup, loads,
+                          C.byref(lanes), C.byref(batches))
+    out = {"dup_count": [int(x) for x in dup], "dup_fraction": [int(x) / g.m if g.m else 0.0
+                                                                 for x in dup],
+           "loads": [int(x) for x in loads]}
+    sampled = sum(out["dup_count"][1:])
+    for lim in (1, 2):
+        out[f"share_within_{lim}"] = (sum(out["dup_count"][1:lim + 1]) / sampled) if sampled else 0.0
+    if r % 32 == 0:
+        out["fill_rate"] = lanes.value / (32.0 * batches.value) if batches.value else 0.0
+        out["fill_batches"] = batches.value
+    return out
 
 
 def device_graph(g: CSR, w, xs):

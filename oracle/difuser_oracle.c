@@ -444,3 +444,46 @@ int dor_run(uint32_t n, uint64_t m, const uint64_t *offsets,
   free(order);
   return rc;
 }
+
+/* ---- FASST analytics (proj/src/fasst.cpp:90-168) -------------------------
+ * xs: the plan's slot values (chunk tau = xs[tau*J, (tau+1)*J)); xfill: the
+ * X values in fill-rate order (sorted for FASST, generation order for naive).
+ * dup_count[mu+1]: edges sampled by exactly k chunks (W = 0 edges count as
+ * k = 0, fasst.cpp:107-109); loads[mu]: per-chunk sampled edges
+ * (fasst.cpp:128-138); fill: live lanes and counted (edge, 32-lane batch)
+ * pairs (fasst.cpp:140-168, R % 32 == 0). */
+static int chunk_hits(const uint32_t *xs, uint32_t J, uint32_t h, uint32_t w) {
+  for (uint32_t j = 0; j < J; ++j) /* fasst.cpp:93-97 */
+    if ((xs[j] ^ h) < w) return 1;
+  return 0;
+}
+
+void dor_fasst_stats(uint64_t m, const uint32_t *ehash, const uint32_t *w,
+                     const uint32_t *xs, const uint32_t *xfill, uint32_t r,
+                     uint32_t mu, uint64_t *dup_count, uint64_t *loads,
+                     uint64_t *live_lanes, uint64_t *batches) {
+  const uint32_t J = r / mu;
+  memset(dup_count, 0, (mu + 1) * sizeof *dup_count);
+  memset(loads, 0, mu * sizeof *loads);
+  *live_lanes = 0;
+  *batches = 0;
+  for (uint64_t e = 0; e < m; ++e) {
+    uint32_t k = 0;
+    if (w[e] != 0)
+      for (uint32_t t = 0; t < mu; ++t) {
+        const int hit = chunk_hits(xs + (uint64_t)t * J, J, ehash[e], w[e]);
+        k += hit;
+        loads[t] += hit;
+      }
+    dup_count[k]++;
+    if (w[e] == 0 || r % 32 != 0) continue;
+    for (uint32_t b = 0; b < r / 32; ++b) { /* fasst.cpp:154-163 */
+      uint32_t c = 0;
+      for (uint32_t t = 0; t < 32; ++t) c += (xfill[b * 32 + t] ^ ehash[e]) < w[e];
+      if (c) {
+        *live_lanes += c;
+        ++*batches;
+      }
+    }
+  }
+}

@@ -63,6 +63,14 @@ uint64_t dor_commit_cascade(uint32_t n, const uint64_t *d_offsets,
                             uint32_t j_local, int8_t *regs, uint64_t *vis,
                             uint32_t seed);
 
+/* ---- FASST analytics (proj/src/fasst.cpp:90-168): duplication histogram
+ * dup_count[mu+1], per-chunk edge loads[mu], fill-rate live lanes / batches
+ * over xfill (X sorted for FASST, generation order for naive). */
+void dor_fasst_stats(uint64_t m, const uint32_t *ehash, const uint32_t *w,
+                     const uint32_t *xs, const uint32_t *xfill, uint32_t r,
+                     uint32_t mu, uint64_t *dup_count, uint64_t *loads,
+                     uint64_t *live_lanes, uint64_t *batches);
+
 /* ---- full greedy run (proj/src/runtime.cpp:37-179), mu simulated devices
  * executed one after another.  `w` is the fixed-point weight array already
  * assigned (apply_weights).  Outputs: seeds_dense[k], traj[k],

@@ -151,6 +151,26 @@ def main():
             })
     with open(os.path.join(OUT, "traces.json"), "w") as f:
         json.dump(traces, f)
+
+    # ---- FASST analytics (fasst.cpp:101-168) ----------------------------------
+    fs_graphs = {"er200": gs["er200"], "er300": gs["er300"],
+                 "er3000": O.build_csr(*O.er_edges(3000, 24000, 21))}
+    fstats = []
+    for name, r, mu, mode, wspec, seed in [
+        ("er200", 256, 4, "fasst", "const:0.1", 2), ("er200", 256, 4, "naive", "const:0.1", 2),
+        ("er300", 1024, 8, "fasst", "const:0.01", 7), ("er300", 1024, 8, "naive", "const:0.01", 7),
+        ("er300", 96, 3, "fasst", "wc", 5), ("er3000", 512, 8, "fasst", "const:0.05", 3),
+        ("er3000", 512, 8, "naive", "const:0.05", 3), ("er3000", 256, 2, "fasst", "wc", 1),
+        ("er3000", 4096, 8, "fasst", "const:0.005", 9), ("er3000", 128, 1, "naive", "const:1", 4),
+    ]:
+        g = fs_graphs[name]
+        w = probe.weights(g.offsets.tolist(), g.adj.tolist(), wspec, seed)
+        d = probe.fasst_stats(g.offsets.tolist(), g.adj.tolist(), w, r, mu, mode, seed)
+        fstats.append({"graph": name, "r": r, "mu": mu, "mode": mode, "weights": wspec,
+                       "seed": seed, **{k: (list(v) if isinstance(v, (list, tuple)) else v)
+                                        for k, v in d.items()}})
+    with open(os.path.join(OUT, "fasst_stats.json"), "w") as f:
+        json.dump({"graphs": {k: graph_dict(v) for k, v in fs_graphs.items()}, "cases": fstats}, f)
     print("golden fixtures written to", OUT)
 
 

@@ -133,6 +133,34 @@ PYBIND11_MODULE(_refprobe, mod) {
       py::arg("mu"), py::arg("mode"), py::arg("seed"), py::arg("tau"),
       py::arg("seeds") = std::vector<uint32_t>{});
 
+  // FASST analytics (proj/src/fasst.cpp:101-168): duplication histogram,
+  // per-device edge loads and the 32-lane batch fill rate, on the weighted
+  // graph as apply_weights leaves it.
+  mod.def(
+      "fasst_stats",
+      [](const std::vector<uint64_t>& offsets, const std::vector<uint32_t>& adj,
+         const std::vector<uint32_t>& weights, uint32_t r, uint32_t mu,
+         const std::string& mode, uint64_t seed) {
+        WeightedGraph g = make_graph(offsets, adj, weights);
+        RandomVector x = gen_random_vector(r, derive_seed(seed, kSeedTagSamples));
+        PartitionPlan plan = make_plan(x, mu, parse_partition_mode(mode));
+        DuplicationHistogram h = duplication_stats(g, plan);
+        py::dict d;
+        d["dup_count"] = h.count;
+        d["dup_fraction"] = h.fraction;
+        d["share_within_1"] = h.sampled_share_within(1);
+        d["share_within_2"] = h.sampled_share_within(2);
+        d["loads"] = device_edge_loads(g, plan);
+        if (r % 32 == 0) {
+          FillRateReport fr = fill_rate(g, x, parse_partition_mode(mode));
+          d["fill_rate"] = fr.fill_rate;
+          d["fill_batches"] = fr.batches;
+        }
+        return d;
+      },
+      py::arg("offsets"), py::arg("adj"), py::arg("weights"), py::arg("r"), py::arg("mu"),
+      py::arg("mode"), py::arg("seed"));
+
   mod.def("fmix64", [](uint64_t k) { return fmix64(k); });
   mod.def("splitmix64_at", [](uint64_t s, uint64_t i) { return splitmix64_at(s, i); });
   mod.def("murmur3_pair", [](uint64_t a, uint64_t b) {

@@ -20,7 +20,7 @@ from ._capi import Config, Stats, check, lib
 __all__ = ["_config", 
     "Graph", "edge_hash", "graph_from_text", "greedy_exact", "influence", "is_sampled",
     "load_graph", "random_value_at", "run", "run_json", "save_cache", "generate", "Context",
-    "peer_link",
+    "peer_link", "fasst_stats",
 ]
 
 
@@ -272,6 +272,34 @@ class Context:
         regs = np.ascontiguousarray(regs, np.int8)
         check(lib().dfs_set_registers(self._h, tau, regs.ctypes.data))
 
+    # ---- FASST analytics (proj/src/fasst.cpp:101-168)
+    def fasst_stats(self, graph, r=256, devices=1, mode="fasst", weights="const:0.1", seed=0,
+                    resident=False) -> dict:
+        """duplication_stats + device_edge_loads + fill_rate of the plan of
+        (r, devices, mode, seed) under `weights`, on the GPU.  Same fields as
+        the reference's DuplicationHistogram / loads / FillRateReport."""
+        if not resident:
+            self.upload(graph)
+        cfg = _config(1, r, devices, mode, weights, 0.01, seed)
+        dup = np.zeros(devices + 1, np.uint64)
+        loads = np.zeros(devices, np.uint64)
+        fill = np.zeros(2, np.uint64)
+        check(lib().dfs_fasst_stats(self._h, graph._h if graph is not None else None,
+                                    C.byref(cfg), dup.ctypes.data, loads.ctypes.data,
+                                    fill.ctypes.data))
+        m = int(self._graph.m) if self._graph is not None else graph.m
+        counts = [int(x) for x in dup]
+        sampled = sum(counts[1:])
+        out = {"dup_count": counts, "dup_fraction": [c / m if m else 0.0 for c in counts],
+               "loads": [int(x) for x in loads]}
+        for lim in (1, 2):  # DuplicationHistogram::sampled_share_within (fasst.cpp:119-126)
+            out[f"share_within_{lim}"] = (sum(counts[1:lim + 1]) / sampled) if sampled else 0.0
+        if r % 32 == 0:  # FillRateReport (fasst.cpp:140-168)
+            lanes, batches = int(fill[0]), int(fill[1])
+            out["fill_rate"] = lanes / (32.0 * batches) if batches else 0.0
+            out["fill_batches"] = batches
+        return out
+
     # ---- peer (multi-GPU) mode: one FASST partition per GPU, exchange in-kernel
     def prepare_partition(self, graph, rank, world, k=1, r=256, mode="fasst",
                           weights="const:0.1", rebuild_eps=0.01, seed=0, resident=False):
@@ -303,6 +331,12 @@ class Context:
         check(lib().dfs_peer_run_json(self._h, graph._h if graph is not None else None,
                                       C.byref(cfg), int(timings), int(resident), C.byref(out)))
         return self._take_json(out)
+
+
+def fasst_stats(graph, r=256, devices=1, mode="fasst", weights="const:0.1", seed=0) -> dict:
+    """FASST analytics (duplication histogram, device edge loads, fill rate)."""
+    return default_context().fasst_stats(graph, r=r, devices=devices, mode=mode, weights=weights,
+                                         seed=seed)
 
 
 def peer_link(ctxs) -> None:

@@ -298,6 +298,23 @@ int dfs_prepare_partition(dfs_ctx* ctx, const dfs_graph* g, const dfs_config* cf
     ctx->c->prepare(rc, g ? &g->g : nullptr, rank, world);
   });
 }
+int dfs_fasst_stats(dfs_ctx* ctx, const dfs_graph* g, const dfs_config* cfg,
+                    uint64_t* dup_count, uint64_t* loads, uint64_t fill[2]) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(dup_count, "dup_count");
+    need(loads, "loads");
+    need(fill, "fill");
+    dfs::RunConfig rc = to_config(cfg);
+    const std::vector<uint64_t> h = ctx->c->fasst_stats(rc, g ? &g->g : nullptr);
+    const uint32_t mu = rc.mu;
+    std::memcpy(dup_count, h.data(), (size_t(mu) + 1) * 8);
+    std::memcpy(loads, h.data() + mu + 1, size_t(mu) * 8);
+    fill[0] = h[2 * size_t(mu) + 1];
+    fill[1] = h[2 * size_t(mu) + 2];
+  });
+}
+
 static_assert(DFS_PEER_HANDLE_BYTES == dfs::kPeerHandleBytes, "peer handle size");
 int dfs_peer_export(dfs_ctx* ctx, void* handle_out) {
   return guard([&] {

@@ -206,6 +206,12 @@ void launch_tweights(const DevGraph& g, int kind, uint32_t W, const uint32_t* w,
                      cudaStream_t s);
 // Reverse items from forward items (no sampling recomputation).
 void launch_xlut(const RankDev& r, cudaStream_t s);
+void launch_xlut_of(const uint32_t* x, uint32_t J, uint32_t* lut, cudaStream_t s);
+// FASST analytics (fasst.cpp:101-168): out = [dup counts 0..mu | loads | live
+// lanes | batches] (2 mu + 3 u64).
+void launch_fasst_stats(const DevGraph& g, const uint32_t* w, const uint32_t* x,
+                        const uint32_t* xlut, uint32_t R, uint32_t mu, int sorted, int fill,
+                        unsigned long long* out, cudaStream_t s);
 void launch_rev_counts(const DevGraph& g, const uint32_t* cnt_f, uint32_t* cnt_r, cudaStream_t s);
 void launch_rev_copy(const DevGraph& g, const uint32_t* cnt_f, const uint32_t* cnt_r,
                      const uint64_t* pos_f, const uint64_t* pos_r, const Items& f, Items& rv,

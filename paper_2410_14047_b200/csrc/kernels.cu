@@ -378,6 +378,72 @@ __global__ void k_small_items(uint32_t nsmall, const uint32_t* __restrict__ smal
   }
 }
 
+// ---------------------------------------------------------------- FASST analytics
+// duplication_stats / device_edge_loads / fill_rate of proj/src/fasst.cpp:
+// 101-168 in one pass over the edges.  x: the plan's slot values (sorted for
+// FASST, generation order for naive; chunk tau = slots [tau*J, (tau+1)*J)),
+// which is also the order fill_rate batches X in.  Sorted slots use the live
+// window of each edge; naive plans test every slot.  Counters are exact
+// integers (block-shared, one global atomic per counter per block).
+// out: [0, mu] duplication counts, [mu+1, 2mu] loads, [2mu+1] live lanes,
+// [2mu+2] counted batches.
+__global__ void k_fasst_stats(uint64_t m, const uint32_t* __restrict__ ehash,
+                              const uint32_t* __restrict__ w, const uint32_t* __restrict__ x,
+                              const uint32_t* __restrict__ glut, uint32_t R, uint32_t mu,
+                              int sorted, int fill, unsigned long long* out) {
+  extern __shared__ uint32_t sx[];
+  uint32_t* lut = sx + R;
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(lut + (1u << kLutBits) + 2);
+  const uint32_t ncnt = 2 * mu + 3;
+  for (uint32_t i = threadIdx.x; i < R; i += blockDim.x) sx[i] = x[i];
+  if (sorted)
+    for (uint32_t k = threadIdx.x; k <= (1u << kLutBits); k += blockDim.x) lut[k] = glut[k];
+  for (uint32_t i = threadIdx.x; i < ncnt; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  const uint32_t J = R / mu;
+  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < m;
+       e += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t W = w[e];
+    if (W == 0) {  // fasst.cpp:107-109: never sampled, k = 0
+      atomicAdd(&cnt[0], 1ull);
+      continue;
+    }
+    const uint32_t h = ehash[e];
+    uint32_t lo = 0, hi = R;
+    if (sorted) edge_window(sx, lut, R, h, W, 1, lo, hi);
+    unsigned long long hits = 0;  // chunks sampling e (mu <= 64)
+    uint32_t bc = 0, cur_b = lo >> 5;
+    unsigned long long lanes = 0, batches = 0;
+    for (uint32_t i = lo; i < hi; ++i) {
+      if ((i >> 5) != cur_b) {
+        if (bc) {
+          lanes += bc;
+          ++batches;
+        }
+        bc = 0;
+        cur_b = i >> 5;
+      }
+      if ((sx[i] ^ h) < W) {  // sampling.hpp:37-39
+        hits |= 1ull << (i / J);
+        ++bc;
+      }
+    }
+    if (bc) {
+      lanes += bc;
+      ++batches;
+    }
+    atomicAdd(&cnt[__popcll(hits)], 1ull);
+    for (unsigned long long t = hits; t; t &= t - 1) atomicAdd(&cnt[mu + 1 + __ffsll(t) - 1], 1ull);
+    if (fill && batches) {
+      atomicAdd(&cnt[2 * mu + 1], lanes);
+      atomicAdd(&cnt[2 * mu + 2], batches);
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < ncnt; i += blockDim.x)
+    if (cnt[i]) atomicAdd(&out[i], cnt[i]);
+}
+
 // ---------------------------------------------------------------- fill
 // 4 mask bits -> 4 bytes of 0xFF / 0x00.
 __device__ __forceinline__ uint32_t expand4(uint32_t m4) {
@@ -2140,6 +2206,26 @@ void launch_items_pass(const DevGraph& g, const uint32_t* w, const uint32_t* tw,
   else
     k_items<0><<<grid, kThreads, smem, s>>>(g.m, ph, pw, po, pr, r.x, r.J, r.Jp, fasst, cnt, pos_off,
                                             nullptr, nullptr, nullptr, nullptr, r.xlut);
+  DFS_CUDA(cudaGetLastError());
+  ++g_launches;
+}
+
+void launch_fasst_stats(const DevGraph& g, const uint32_t* w, const uint32_t* x,
+                        const uint32_t* xlut, uint32_t R, uint32_t mu, int sorted, int fill,
+                        unsigned long long* out, cudaStream_t s) {
+  DFS_CUDA(cudaMemsetAsync(out, 0, (2 * size_t(mu) + 3) * 8, s));
+  if (!g.m) return;
+  const size_t smem = (size_t(R) + (1u << kLutBits) + 2) * 4 + (2 * size_t(mu) + 3) * 8 + 16;
+  DFS_CUDA(cudaFuncSetAttribute(k_fasst_stats, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(std::max<size_t>(smem, 48 << 10))));
+  k_fasst_stats<<<grid_for(g.m, kThreads * 4), kThreads, smem, s>>>(g.m, g.ehash, w, x, xlut, R, mu,
+                                                                     sorted, fill, out);
+  DFS_CUDA(cudaGetLastError());
+  ++g_launches;
+}
+
+void launch_xlut_of(const uint32_t* x, uint32_t J, uint32_t* lut, cudaStream_t s) {
+  k_xlut<<<(((1u << kLutBits) + 1) + kThreads - 1) / kThreads, kThreads, 0, s>>>(x, J, lut);
   DFS_CUDA(cudaGetLastError());
   ++g_launches;
 }

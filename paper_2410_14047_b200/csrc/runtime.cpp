@@ -270,6 +270,33 @@ void Context::reset_rank_state(RankDev& r) {
 
 void Context::prepare(const RunConfig& cfg, const HostGraph* host_w_src, uint32_t part_rank,
                       uint32_t part_world) {
+  auto t0 = Clock::now();
+  plan_weights(cfg, host_w_src);
+  // ---- per-rank state and sampled items (fasst.cpp:50-88, build phase)
+  if (part_world && (part_world != cfg.mu || part_rank >= part_world))
+    throw Error(kInvalid, "partition rank/world must match devices");
+  const uint32_t first = part_world ? part_rank : 0;
+  const uint32_t count = part_world ? 1 : cfg.mu;
+  ranks_.assign(count, RankDev{});
+  for (uint32_t t = 0; t < count; ++t) {
+    RankDev& r = ranks_[t];
+    alloc_rank(r, first + t);
+    build_items(r);
+    const std::string p = "r" + std::to_string(first + t) + ".q.";
+    const uint64_t cap = std::max<uint64_t>(std::max(r.fwd.chunks, r.rev.chunks), 1);
+    for (int gi = 0; gi < kGens; ++gi) {
+      r.q.chunks[gi] = as<uint32_t>(arena_.get(p + "c" + std::to_string(gi), cap * 4));
+      r.q.rows[gi] = as<uint32_t>(arena_.get(p + "r" + std::to_string(gi),
+                                             std::max<uint32_t>(g_.n, 1) * 4));
+    }
+    reset_rank_state(r);
+  }
+  prep_seconds_ = since(t0);
+}
+
+// Validation, FASST plan and weights of a run (runtime.cpp:38-47,
+// fasst.cpp:21-48, apply_weights runtime.cpp:15-17).
+void Context::plan_weights(const RunConfig& cfg, const HostGraph* host_w_src) {
   if (!has_graph()) throw Error(kRuntime, "no graph uploaded");
   DFS_CUDA(cudaSetDevice(device_));
   // runtime.cpp:38-42, then gen_random_vector (sampling.cpp:8), make_plan
@@ -283,7 +310,6 @@ void Context::prepare(const RunConfig& cfg, const HostGraph* host_w_src, uint32_
                               std::to_string(cfg.r) + ")");
   if (cfg.mu > 64) throw Error(kInvalid, "run: at most 64 sample-space partitions per context");
   if (cfg.r / cfg.mu > 8192) throw Error(kInvalid, "run: at most 8192 simulations per partition");
-  auto t0 = Clock::now();
   cfg_ = cfg;
   // ---- plan (fasst.cpp:21-48): X_r, stable sort for FASST
   const uint64_t xs = derive_seed(cfg.seed, kSeedTagSamples);
@@ -320,30 +346,28 @@ void Context::prepare(const RunConfig& cfg, const HostGraph* host_w_src, uint32_
       sync();
     }
   }
-  // ---- per-rank state and sampled items (fasst.cpp:50-88, build phase)
-  if (part_world && (part_world != cfg.mu || part_rank >= part_world))
-    throw Error(kInvalid, "partition rank/world must match devices");
-  const uint32_t first = part_world ? part_rank : 0;
-  const uint32_t count = part_world ? 1 : cfg.mu;
-  ranks_.assign(count, RankDev{});
-  for (uint32_t t = 0; t < count; ++t) {
-    RankDev& r = ranks_[t];
-    alloc_rank(r, first + t);
-    build_items(r);
-    const std::string p = "r" + std::to_string(first + t) + ".q.";
-    const uint64_t cap = std::max<uint64_t>(std::max(r.fwd.chunks, r.rev.chunks), 1);
-    for (int gi = 0; gi < kGens; ++gi) {
-      r.q.chunks[gi] = as<uint32_t>(arena_.get(p + "c" + std::to_string(gi), cap * 4));
-      r.q.rows[gi] = as<uint32_t>(arena_.get(p + "r" + std::to_string(gi),
-                                             std::max<uint32_t>(g_.n, 1) * 4));
-    }
-    reset_rank_state(r);
-  }
-  prep_seconds_ = since(t0);
 }
 
 Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
   return run_impl(cfg, host_w_src, false);
+}
+
+std::vector<uint64_t> Context::fasst_stats(const RunConfig& cfg, const HostGraph* host_w_src) {
+  RunConfig c = cfg;
+  c.k = 1;  // k is not an input of the analytics
+  if (c.r > 32768) throw Error(kInvalid, "fasst_stats: at most 32768 simulations");
+  plan_weights(c, host_w_src);
+  const uint32_t R = c.r, mu = c.mu;
+  uint32_t* x = as<uint32_t>(arena_.get("fs.x", size_t(R) * 4));
+  uint32_t* lut = as<uint32_t>(arena_.get("fs.lut", 4100 * 4));
+  unsigned long long* out = as<unsigned long long>(arena_.get("fs.out", (2 * size_t(mu) + 3) * 8));
+  DFS_CUDA(cudaMemcpyAsync(x, x_.data(), size_t(R) * 4, cudaMemcpyHostToDevice, stream_));
+  if (c.fasst) launch_xlut_of(x, R, lut, stream_);
+  launch_fasst_stats(g_, w_, x, lut, R, mu, c.fasst ? 1 : 0, R % 32 == 0 ? 1 : 0, out, stream_);
+  std::vector<uint64_t> h(2 * size_t(mu) + 3);
+  DFS_CUDA(cudaMemcpyAsync(h.data(), out, h.size() * 8, cudaMemcpyDeviceToHost, stream_));
+  sync();
+  return h;
 }
 
 Report Context::run_peer(const RunConfig& cfg, const HostGraph* host_w_src) {

@@ -132,6 +132,10 @@ class Context {
   const PhaseTimings& last_timings() const { return last_; }
   void sync();
 
+  // FASST analytics (fasst.cpp:101-168) of a plan on the resident graph:
+  // out = [dup counts 0..mu | per-chunk loads | fill live lanes | batches].
+  std::vector<uint64_t> fasst_stats(const RunConfig& cfg, const HostGraph* host_w_src);
+
   // ---- peer mode (one FASST partition per GPU; exchange inside k_run)
   // After prepare(cfg, host, rank, world): write this rank's handle.
   void peer_export(void* out);
@@ -145,6 +149,7 @@ class Context {
 
  private:
   Report run_impl(const RunConfig& cfg, const HostGraph* host_w_src, bool peer);
+  void plan_weights(const RunConfig& cfg, const HostGraph* host_w_src);
   PeerBox* peer_box();
   void build_items(RankDev& r);
   void finish_items(RankDev& r, int dir, const uint64_t* pos);

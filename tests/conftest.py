@@ -28,3 +28,10 @@ def golden():
 def ctx():
     import paper_2410_14047_b200 as D
     return D.Context(0)
+
+
+@pytest.fixture(scope="session")
+def golden_fasst():
+    import json
+    with open(os.path.join(ROOT, "tests", "golden", "fasst_stats.json")) as f:
+        return json.load(f)

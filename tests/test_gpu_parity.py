@@ -277,3 +277,25 @@ def test_dist_runner_single_rank_report(D, ctx, golden):
         g = _graph(D, runs["graphs"][case["graph"]])
         got = DistRunner(ctx, g, 0, 1).run(**cfg)
         assert got == case["json"], case["config"]
+
+
+def test_fasst_stats_match_reference(D, ctx, golden_fasst):
+    """FASST analytics on the GPU (duplication histogram, per-device edge loads,
+    fill rate; proj/src/fasst.cpp:101-168) vs the compiled reference."""
+    gs = golden_fasst["graphs"]
+    for c in golden_fasst["cases"]:
+        g = _graph(D, gs[c["graph"]])
+        got = ctx.fasst_stats(g, r=c["r"], devices=c["mu"], mode=c["mode"], weights=c["weights"],
+                              seed=c["seed"])
+        for key in ("dup_count", "dup_fraction", "loads", "share_within_1", "share_within_2",
+                    "fill_rate", "fill_batches"):
+            if key in c:
+                assert got[key] == c[key], (key, c["graph"], c["r"], c["mu"], c["mode"])
+
+
+@pytest.mark.parametrize("mode", ["fasst", "naive"])
+def test_fasst_stats_match_oracle_rmat(D, ctx, mode):
+    g = D.generate("rmat", 14, 200000, 3)
+    got = ctx.fasst_stats(g, r=1024, devices=8, mode=mode, weights="wc", seed=5)
+    want = O.fasst_stats(_oracle_csr(g), 1024, 8, mode, "wc", 5)
+    assert got == want

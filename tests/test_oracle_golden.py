@@ -142,3 +142,17 @@ def test_oracle_vs_live_reference(seed):
 
 def test_golden_fixture_generator_present():
     assert os.path.exists(os.path.join(os.path.dirname(O.HERE), "oracle", "make_golden.py"))
+
+
+def test_fasst_stats_match_reference(golden_fasst):
+    """duplication_stats / device_edge_loads / fill_rate (fasst.cpp:101-168)
+    of the restatement vs the compiled reference's own values."""
+    gs = golden_fasst["graphs"]
+    for c in golden_fasst["cases"]:
+        gd = gs[c["graph"]]
+        g = O.CSR(gd["offsets"], gd["adj"], gd["orig_ids"])
+        got = O.fasst_stats(g, c["r"], c["mu"], c["mode"], c["weights"], c["seed"])
+        for key in ("dup_count", "dup_fraction", "loads", "share_within_1", "share_within_2",
+                    "fill_rate", "fill_batches"):
+            if key in c:
+                assert got[key] == c[key], (key, c["graph"], c["r"], c["mu"], c["mode"])
