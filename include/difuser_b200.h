@@ -153,6 +153,15 @@ int dfs_set_registers(dfs_ctx *ctx, uint32_t tau, const int8_t *in_nJ);
 /* {updates, items, edges, batches, touched, sweeps, convergences, visited} */
 int dfs_rank_counters(dfs_ctx *ctx, uint32_t tau, uint64_t out[8]);
 
+/* ---- Monte-Carlo influence on the GPU (oracle.cpp:30-79, the binding's
+ * influence(), pymodule.cpp:92-107): (mean, std_error) bit-identical to the
+ * reference; reached (nullable) receives the trials*runs per-trial reached
+ * counts in the reference's trial order.  resident != 0 uses the graph
+ * uploaded by dfs_upload (g still needed for normal/uniform weights). */
+int dfs_mc_influence(dfs_ctx *ctx, const dfs_graph *g, int resident, const uint32_t *seeds,
+                     uint32_t nseeds, uint32_t trials, uint64_t seed, uint32_t runs,
+                     const char *weights, double *mean, double *std_error, uint32_t *reached);
+
 /* ---- FASST analytics (proj/src/fasst.cpp:101-168; CLI partition-stats /
  * fillrate, tools/difuser.cpp:116-159) on the resident graph (g: for
  * normal/uniform weights, else nullable).  cfg: r, devices (= mu), mode,

@@ -171,6 +171,22 @@ def main():
                                         for k, v in d.items()}})
     with open(os.path.join(OUT, "fasst_stats.json"), "w") as f:
         json.dump({"graphs": {k: graph_dict(v) for k, v in fs_graphs.items()}, "cases": fstats}, f)
+    # ---- Monte-Carlo influence (oracle.cpp:30-79, the binding's influence()) ---
+    infl = []
+    for name, seeds, trials, seed, runs, wspec in [
+        ("er200", [0, 5, 17], 300, 4, 1, "const:0.1"), ("er300", [1, 2], 257, 7, 2, "const:0.2"),
+        ("er3000", [10, 200, 3000 - 1], 100, 3, 1, "const:0.05"), ("er3000", [5], 64, 1, 3, "wc"),
+        ("er120", [], 40, 0, 1, "const:0.5"), ("cycle16", [3], 33, 9, 1, "const:0.5"),
+        ("er3000", [7, 8], 96, 11, 1, "uniform:0,0.2"),
+    ]:
+        g = fs_graphs.get(name) or gs[name]
+        rg = ref.graph_from_text(g.edges_text())
+        mean, se = ref.influence(rg, seeds, trials=trials, seed=seed, runs=runs, weights=wspec)
+        infl.append({"graph": name, "seeds": seeds, "trials": trials, "seed": seed, "runs": runs,
+                     "weights": wspec, "mean": float(mean).hex(), "std_error": float(se).hex()})
+    with open(os.path.join(OUT, "influence.json"), "w") as f:
+        json.dump({"graphs": {k: graph_dict(v) for k, v in list(fs_graphs.items()) +
+                              [(k, gs[k]) for k in ("er120", "cycle16")]}, "cases": infl}, f)
     print("golden fixtures written to", OUT)
 
 

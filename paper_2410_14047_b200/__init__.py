@@ -272,6 +272,25 @@ class Context:
         regs = np.ascontiguousarray(regs, np.int8)
         check(lib().dfs_set_registers(self._h, tau, regs.ctypes.data))
 
+    # ---- Monte-Carlo influence on the GPU (proj/src/oracle.cpp:30-79)
+    def influence(self, graph, seeds, trials=10000, seed=0, runs=1, weights="const:0.1",
+                  resident=False, per_trial=False):
+        """(mean, std_error) of the reached set of a dense-id seed set, equal
+        bit for bit to the reference's influence(); per_trial=True also
+        returns the per-trial reached counts (run-major)."""
+        s = np.ascontiguousarray(list(seeds), np.uint32)
+        mean, se = C.c_double(), C.c_double()
+        reached = np.zeros(max(trials * runs, 1), np.uint32)
+        check(lib().dfs_mc_influence(self._h, graph._h if graph is not None else None,
+                                     int(resident), s.ctypes.data if len(s) else None, len(s),
+                                     trials, seed, runs, weights.encode(), C.byref(mean),
+                                     C.byref(se), reached.ctypes.data))
+        if not resident and graph is not None:
+            self._graph = graph
+        if per_trial:
+            return mean.value, se.value, reached[: trials * runs]
+        return mean.value, se.value
+
     # ---- FASST analytics (proj/src/fasst.cpp:101-168)
     def fasst_stats(self, graph, r=256, devices=1, mode="fasst", weights="const:0.1", seed=0,
                     resident=False) -> dict:

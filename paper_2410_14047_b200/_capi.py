@@ -24,7 +24,7 @@ SYMBOLS = [
     "dfs_get_registers", "dfs_set_registers", "dfs_influence", "dfs_greedy_exact",
     "dfs_ctx_stream", "dfs_graph_pin", "dfs_rank_counters", "dfs_prepare_partition",
     "dfs_scores_device", "dfs_rebuild", "dfs_format_report", "dfs_peer_export", "dfs_peer_open",
-    "dfs_peer_link", "dfs_peer_run_json", "dfs_fasst_stats",
+    "dfs_peer_link", "dfs_peer_run_json", "dfs_fasst_stats", "dfs_mc_influence",
 ]
 
 PEER_HANDLE_BYTES = 152  # DFS_PEER_HANDLE_BYTES
@@ -125,6 +125,8 @@ def lib():
         "dfs_rebuild": (i32, [vp, u32]),
         "dfs_format_report": (i32, [C.POINTER(ReportFields), C.POINTER(C.c_void_p)]),
         "dfs_fasst_stats": (i32, [vp, vp, C.POINTER(Config), vp, vp, vp]),
+        "dfs_mc_influence": (i32, [vp, vp, i32, vp, u32, u32, u64, u32, C.c_char_p,
+                                   C.POINTER(C.c_double), C.POINTER(C.c_double), vp]),
         "dfs_peer_export": (i32, [vp, vp]),
         "dfs_peer_open": (i32, [vp, u32, u32, vp]),
         "dfs_peer_link": (i32, [C.POINTER(C.c_void_p), u32]),

@@ -298,6 +298,26 @@ int dfs_prepare_partition(dfs_ctx* ctx, const dfs_graph* g, const dfs_config* cf
     ctx->c->prepare(rc, g ? &g->g : nullptr, rank, world);
   });
 }
+int dfs_mc_influence(dfs_ctx* ctx, const dfs_graph* g, int resident, const uint32_t* seeds,
+                     uint32_t nseeds, uint32_t trials, uint64_t seed, uint32_t runs,
+                     const char* weights, double* mean, double* std_error, uint32_t* reached) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(mean, "mean");
+    need(std_error, "std_error");
+    if (nseeds) need(seeds, "seeds");
+    if (!resident) {
+      need(g, "graph");
+      ctx->c->upload(g->g);
+    }
+    const std::vector<uint32_t> s(seeds, seeds + nseeds);
+    const std::vector<uint32_t> r = ctx->c->mc_influence(
+        s, trials, seed, runs, dfs::WeightSetting::parse(weights ? weights : "const:0.1"),
+        g ? &g->g : nullptr, mean, std_error);
+    if (reached) std::memcpy(reached, r.data(), r.size() * 4);
+  });
+}
+
 int dfs_fasst_stats(dfs_ctx* ctx, const dfs_graph* g, const dfs_config* cfg,
                     uint64_t* dup_count, uint64_t* loads, uint64_t fill[2]) {
   return guard([&] {

@@ -207,6 +207,13 @@ void launch_tweights(const DevGraph& g, int kind, uint32_t W, const uint32_t* w,
 // Reverse items from forward items (no sampling recomputation).
 void launch_xlut(const RankDev& r, cudaStream_t s);
 void launch_xlut_of(const uint32_t* x, uint32_t J, uint32_t* lut, cudaStream_t s);
+// Monte-Carlo influence (oracle.cpp:30-79) of batches [batch0, batch0+nbatch)
+// of 32 trials: live masks (nbatch*m), BFS scratch (vis nbatch*n, fresh and
+// queue nbatch*2n), reached counts (nbatch*32).
+void launch_mc_influence(const DevGraph& g, const uint32_t* w, uint64_t base, uint32_t trials,
+                         uint64_t total, uint64_t batch0, uint32_t nbatch, const uint32_t* seeds,
+                         uint32_t nseeds, uint32_t* live, uint32_t* vis, uint32_t* fresh,
+                         uint32_t* queue, uint32_t* reached, cudaStream_t s);
 // FASST analytics (fasst.cpp:101-168): out = [dup counts 0..mu | loads | live
 // lanes | batches] (2 mu + 3 u64).
 void launch_fasst_stats(const DevGraph& g, const uint32_t* w, const uint32_t* x,

@@ -100,13 +100,6 @@ __global__ void k_ehash_indeg(uint64_t m, const uint32_t* __restrict__ src,
   }
 }
 
-__global__ void k_u32_to_u64(const uint32_t* __restrict__ in, uint64_t* __restrict__ out,
-                             uint64_t n) {
-  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += uint64_t(gridDim.x) * blockDim.x)
-    out[i] = in[i];
-}
-
 // ---------------------------------------------------------------- weights
 // graph.cpp:30-35 + :250-258: W = llround(w * 2^31), wc w = 1/indeg(v).
 __global__ void k_weights(uint64_t m, int kind, uint32_t W, const uint32_t* __restrict__ adj,
@@ -284,12 +277,6 @@ __global__ void k_tweights(uint64_t m, const uint32_t* __restrict__ tedge,
   }
 }
 
-__global__ void k_inverse(uint64_t m, const uint32_t* __restrict__ perm, uint32_t* __restrict__ inv) {
-  for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < m;
-       p += uint64_t(gridDim.x) * blockDim.x)
-    inv[perm[p]] = uint32_t(p);
-}
-
 __global__ void k_row_offsets(uint32_t n, const uint64_t* __restrict__ graph_off,
                               const uint64_t* __restrict__ pos_off, uint64_t* __restrict__ row_off,
                               uint32_t* __restrict__ row_cnt) {
@@ -442,6 +429,206 @@ __global__ void k_fasst_stats(uint64_t m, const uint32_t* __restrict__ ehash,
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < ncnt; i += blockDim.x)
     if (cnt[i]) atomicAdd(&out[i], cnt[i]);
+}
+
+// ---------------------------------------------------------------- MC influence
+// Monte-Carlo oracle of proj/src/oracle.cpp:30-79 on the GPU, bit-identical:
+// trial i = (run, t) draws the liveness of every edge in edge order from its
+// own std::mt19937_64(trial_seed) — (rng() >> 33) < W[e] — then counts the
+// vertices reachable from the seeds over live edges.  32 trials form a batch:
+// phase 1 (k_mc_live) runs 32 generators side by side in one block (one warp
+// per trial, the 312-word twist split over the warp's lanes) and writes one
+// 32-trial live mask per edge (a ballot transpose of the per-trial bits);
+// phase 2 (k_mc_bfs) is a bitset BFS of the 32 trials together, one block per
+// batch.  The per-trial reached counts go to the host, which accumulates the
+// mean / standard error in the reference's trial order (the double sums there
+// are not all exact, so the order matters).
+constexpr int kMtN = 312, kMtM = 156;
+constexpr uint64_t kMtA = 0xB5026F5AA96619E9ull, kMtUpper = 0xFFFFFFFF80000000ull,
+                   kMtLower = 0x7FFFFFFFull;
+
+__device__ __forceinline__ uint64_t mt_mix(uint64_t hi_src, uint64_t lo_src) {
+  const uint64_t y = (hi_src & kMtUpper) | (lo_src & kMtLower);
+  return (y >> 1) ^ ((y & 1) ? kMtA : 0ull);
+}
+__device__ __forceinline__ uint64_t mt_temper(uint64_t z) {
+  z ^= (z >> 29) & 0x5555555555555555ull;
+  z ^= (z << 17) & 0x71D67FFFEDA60000ull;
+  z ^= (z << 37) & 0xFFF7EEE000000000ull;
+  z ^= z >> 43;
+  return z;
+}
+// libstdc++ _M_gen_rand: the three segments in order; each lane reads its
+// inputs before the warp writes (in-place update).
+__device__ __forceinline__ void mt_twist(uint64_t* mt, unsigned lane) {
+  for (int k0 = 0; k0 < kMtN - kMtM; k0 += 32) {
+    const int k = k0 + lane;
+    uint64_t v = 0;
+    if (k < kMtN - kMtM) v = mt[k + kMtM] ^ mt_mix(mt[k], mt[k + 1]);
+    __syncwarp();
+    if (k < kMtN - kMtM) mt[k] = v;
+    __syncwarp();
+  }
+  for (int k0 = kMtN - kMtM; k0 < kMtN - 1; k0 += 32) {
+    const int k = k0 + lane;
+    uint64_t v = 0;
+    if (k < kMtN - 1) v = mt[k + kMtM - kMtN] ^ mt_mix(mt[k], mt[k + 1]);
+    __syncwarp();
+    if (k < kMtN - 1) mt[k] = v;
+    __syncwarp();
+  }
+  if (lane == 0) mt[kMtN - 1] = mt[kMtM - 1] ^ mt_mix(mt[kMtN - 1], mt[0]);
+  __syncwarp();
+}
+
+struct McArgs {
+  uint64_t m;
+  const uint32_t* w;
+  uint64_t base;       // derive_seed(seed, kSeedTagOracle)
+  uint32_t trials;     // per run
+  uint64_t total;      // trials * runs
+  uint64_t batch0;     // first batch of this launch
+  uint32_t nbatch;     // batches in this launch
+  uint32_t* live;      // nbatch * m masks
+};
+
+// One block (32 warps) per batch; warp t runs trial 32*batch + t.
+constexpr size_t kMcLiveSmem = 32 * kMtN * 8 + 32 * (kMtN / 32 + 1) * 4;
+__global__ void __launch_bounds__(1024, 1) k_mc_live(McArgs a) {
+  extern __shared__ uint64_t mc_smem[];
+  uint64_t (*mt)[kMtN] = reinterpret_cast<uint64_t (*)[kMtN]>(mc_smem);
+  uint32_t (*bits)[kMtN / 32 + 1] =
+      reinterpret_cast<uint32_t (*)[kMtN / 32 + 1]>(mc_smem + 32 * kMtN);
+  const unsigned lane = threadIdx.x & 31, wt = threadIdx.x >> 5;
+  for (uint32_t bb = blockIdx.x; bb < a.nbatch; bb += gridDim.x) {
+    const uint64_t trial = (a.batch0 + bb) * 32 + wt;
+    const bool real = trial < a.total;
+    uint64_t* st = mt[wt];
+    if (lane == 0) {  // std::mt19937_64(seed): sequential initialisation
+      const uint64_t run = real ? trial / a.trials : 0, t = real ? trial % a.trials : 0;
+      uint64_t x = splitmix64_at(splitmix64_at(a.base, run), t);  // oracle.cpp:23-25
+      st[0] = x;
+      for (int i = 1; i < kMtN; ++i) {
+        x = 6364136223846793005ull * (x ^ (x >> 62)) + uint64_t(i);
+        st[i] = x;
+      }
+    }
+    __syncwarp();
+    uint32_t* out = a.live + uint64_t(bb) * a.m;
+    for (uint64_t e0 = 0; e0 < a.m; e0 += kMtN) {
+      mt_twist(st, lane);  // every block of 312 draws starts with a twist
+      const uint64_t rem = a.m - e0;
+      const uint32_t cnt = rem < uint64_t(kMtN) ? uint32_t(rem) : uint32_t(kMtN);
+      for (uint32_t c = 0; c * 32 < cnt; ++c) {
+        const uint32_t i = c * 32 + lane;
+        bool lv = false;
+        if (i < cnt && real) lv = uint32_t(mt_temper(st[i]) >> 33) < __ldg(a.w + e0 + i);
+        const unsigned word = __ballot_sync(0xffffffffu, lv);
+        if (lane == 0) bits[wt][c] = word;
+      }
+      __syncthreads();
+      // transpose: warp c turns the 32 trials' words of edges [32c, 32c+32)
+      // into one 32-trial mask per edge
+      if (wt * 32 < cnt) {
+        const unsigned word = bits[lane][wt];
+        unsigned mine = 0;
+#pragma unroll 8
+        for (int j = 0; j < 32; ++j) {
+          const unsigned msk = __ballot_sync(0xffffffffu, (word >> j) & 1u);
+          if (lane == j) mine = msk;
+        }
+        if (wt * 32 + lane < cnt) out[e0 + wt * 32 + lane] = mine;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+struct McBfs {
+  uint32_t n;
+  const uint64_t* off;
+  const uint32_t* adj;
+  uint64_t m;
+  const uint32_t* live;    // nbatch * m
+  const uint32_t* seeds;
+  uint32_t nseeds;
+  uint32_t nbatch;
+  uint32_t* vis;           // nbatch * n
+  uint32_t* fresh;         // nbatch * 2n
+  uint32_t* queue;         // nbatch * 2n
+  uint32_t* reached;       // nbatch * 32
+};
+
+// One block per batch: level-synchronous BFS of 32 trials as bitsets.
+__global__ void __launch_bounds__(1024, 1) k_mc_bfs(McBfs a) {
+  __shared__ unsigned int qn[2];
+  __shared__ unsigned int cnt[32];
+  for (uint32_t bb = blockIdx.x; bb < a.nbatch; bb += gridDim.x) {
+    const uint32_t* live = a.live + uint64_t(bb) * a.m;
+    uint32_t* vis = a.vis + uint64_t(bb) * a.n;
+    uint32_t* fr[2] = {a.fresh + uint64_t(bb) * 2 * a.n, a.fresh + uint64_t(bb) * 2 * a.n + a.n};
+    uint32_t* q[2] = {a.queue + uint64_t(bb) * 2 * a.n, a.queue + uint64_t(bb) * 2 * a.n + a.n};
+    for (uint32_t v = threadIdx.x; v < a.n; v += blockDim.x) {
+      vis[v] = 0;
+      fr[0][v] = 0;
+      fr[1][v] = 0;
+    }
+    if (threadIdx.x < 32) cnt[threadIdx.x] = 0;
+    if (threadIdx.x == 0) {
+      qn[0] = 0;
+      qn[1] = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (uint32_t i = 0; i < a.nseeds; ++i) {
+        const uint32_t s = a.seeds[i];
+        if (!vis[s]) {
+          vis[s] = 0xFFFFFFFFu;
+          fr[0][s] = 0xFFFFFFFFu;
+          q[0][qn[0]++] = s;
+        }
+      }
+    __syncthreads();
+    int cur = 0;
+    while (qn[cur]) {
+      const int nx = cur ^ 1;
+      const unsigned len = qn[cur];
+      // warp per frontier vertex, lanes over its out-edges
+      for (unsigned k = threadIdx.x >> 5; k < len; k += blockDim.x >> 5) {
+        const uint32_t u = q[cur][k];
+        const uint32_t fu = fr[cur][u];
+        for (uint64_t e = a.off[u] + (threadIdx.x & 31); e < a.off[u + 1]; e += 32) {
+          const uint32_t c = fu & live[e];
+          if (!c) continue;
+          const uint32_t v = a.adj[e];
+          if (!(c & ~ld_volatile(vis + v))) continue;
+          const uint32_t nb = c & ~atomicOr(vis + v, c);
+          if (!nb) continue;
+          if (atomicOr(fr[nx] + v, nb) == 0) q[nx][atomicAdd(&qn[nx], 1u)] = v;
+        }
+      }
+      __syncthreads();
+      for (unsigned k = threadIdx.x; k < len; k += blockDim.x) fr[cur][q[cur][k]] = 0;
+      if (threadIdx.x == 0) qn[cur] = 0;
+      __syncthreads();
+      cur = nx;
+    }
+    // reached count per trial: ballot transpose of the visited words
+    unsigned mine = 0;
+    for (uint32_t v0 = (threadIdx.x >> 5) * 32; v0 < a.n; v0 += blockDim.x) {
+      const uint32_t v = v0 + (threadIdx.x & 31);
+      const uint32_t word = v < a.n ? vis[v] : 0;
+#pragma unroll 8
+      for (int t = 0; t < 32; ++t) {
+        const unsigned c = __popc(__ballot_sync(0xffffffffu, (word >> t) & 1u));
+        if ((threadIdx.x & 31) == unsigned(t)) mine += c;
+      }
+    }
+    atomicAdd(&cnt[threadIdx.x & 31], mine);
+    __syncthreads();
+    if (threadIdx.x < 32) a.reached[uint64_t(bb) * 32 + threadIdx.x] = cnt[threadIdx.x];
+    __syncthreads();
+  }
 }
 
 // ---------------------------------------------------------------- fill
@@ -597,13 +784,6 @@ __device__ __forceinline__ void push_row(uint32_t u, uint32_t stamp, uint32_t* l
   for (uint32_t c = c0; c < c1; ++c) chunks[ci + (c - c0)] = c;
 }
 
-__device__ __forceinline__ void push_dirty(uint32_t v, uint32_t base, uint32_t* dstamp,
-                                           uint32_t* dirty, unsigned int* dirty_count) {
-  if (ld_volatile(&dstamp[v]) == base) return;
-  if (atomicExch(&dstamp[v], base) == base) return;
-  dirty[agg_reserve(dirty_count, 1u)] = v;
-}
-
 // Cascade bookkeeping of a row that just received new VISITED bits: one
 // 64-bit stamp (round base << 32 | level stamp) deduplicates both the dirty
 // list (rows to rescore after this cascade) and the next-level frontier.
@@ -734,52 +914,15 @@ __device__ __forceinline__ unsigned long long merge8_full(unsigned long long d,
   return (static_cast<unsigned long long>(hi) << 32) | lo;
 }
 
-// One reverse item staged for the merge: fields + src/dst words (issued
-// before any is consumed so a thread keeps several loads in flight).
+// Fields of one reverse item (push sweeps).
 struct SimItem {
   uint32_t u, mk, b;
-  unsigned long long* dp;
-  unsigned long long sv[4], dv[4];
 };
 
 __device__ __forceinline__ void sim_fields(SimItem& it, const Items& rev, uint64_t i) {
   it.u = __ldg(rev.other + i);
   it.mk = __ldg(rev.mask + i);
   it.b = __ldg(rev.batch + i);
-}
-
-__device__ __forceinline__ void sim_data(SimItem& it, const int8_t* srow, int8_t* regs,
-                                         uint32_t Jp) {
-  const unsigned long long* sp = reinterpret_cast<const unsigned long long*>(srow + it.b * 32);
-  it.dp = reinterpret_cast<unsigned long long*>(regs + uint64_t(it.u) * Jp + it.b * 32);
-#pragma unroll
-  for (int wv = 0; wv < 4; ++wv)
-    if ((it.mk >> (8 * wv)) & 0xFFu) {
-      it.sv[wv] = __ldcg(sp + wv);
-      it.dv[wv] = __ldcg(it.dp + wv);
-    }
-}
-
-// Lock-free byte max (engine.cpp:22-53 semantics) of the staged words.
-__device__ __forceinline__ bool sim_merge(SimItem& it) {
-  bool changed = false;
-#pragma unroll
-  for (int wv = 0; wv < 4; ++wv) {
-    const uint32_t m8 = (it.mk >> (8 * wv)) & 0xFFu;
-    if (!m8) continue;
-    unsigned long long d = it.dv[wv];
-    unsigned long long nv = merge8(d, it.sv[wv], m8);
-    while (nv != d) {
-      const unsigned long long old = atomicCAS(it.dp + wv, d, nv);
-      if (old == d) {
-        changed = true;
-        break;
-      }
-      d = old;
-      nv = merge8(d, it.sv[wv], m8);
-    }
-  }
-  return changed;
 }
 
 // Byte-max CAS loop on one destination word (engine.cpp:22-53 semantics).
@@ -2220,6 +2363,25 @@ void launch_fasst_stats(const DevGraph& g, const uint32_t* w, const uint32_t* x,
                                 int(std::max<size_t>(smem, 48 << 10))));
   k_fasst_stats<<<grid_for(g.m, kThreads * 4), kThreads, smem, s>>>(g.m, g.ehash, w, x, xlut, R, mu,
                                                                      sorted, fill, out);
+  DFS_CUDA(cudaGetLastError());
+  ++g_launches;
+}
+
+void launch_mc_influence(const DevGraph& g, const uint32_t* w, uint64_t base, uint32_t trials,
+                         uint64_t total, uint64_t batch0, uint32_t nbatch, const uint32_t* seeds,
+                         uint32_t nseeds, uint32_t* live, uint32_t* vis, uint32_t* fresh,
+                         uint32_t* queue, uint32_t* reached, cudaStream_t s) {
+  const int blocks = std::max(1, std::min<int>(int(nbatch), num_sms()));
+  if (g.m) {
+    McArgs a{g.m, w, base, trials, total, batch0, nbatch, live};
+    DFS_CUDA(cudaFuncSetAttribute(k_mc_live, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(kMcLiveSmem)));
+    k_mc_live<<<blocks, 1024, kMcLiveSmem, s>>>(a);
+    DFS_CUDA(cudaGetLastError());
+    ++g_launches;
+  }
+  McBfs b{g.n, g.off, g.adj, g.m, live, seeds, nseeds, nbatch, vis, fresh, queue, reached};
+  k_mc_bfs<<<blocks, 1024, 0, s>>>(b);
   DFS_CUDA(cudaGetLastError());
   ++g_launches;
 }

@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstring>
 #include <cstdlib>
 #include <numeric>
@@ -350,6 +351,73 @@ void Context::plan_weights(const RunConfig& cfg, const HostGraph* host_w_src) {
 
 Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
   return run_impl(cfg, host_w_src, false);
+}
+
+std::vector<uint32_t> Context::mc_influence(const std::vector<uint32_t>& seeds, uint32_t trials,
+                                           uint64_t seed, uint32_t runs, const WeightSetting& ws,
+                                           const HostGraph* host_w_src, double* mean,
+                                           double* std_error) {
+  if (!has_graph()) throw Error(kRuntime, "no graph uploaded");
+  DFS_CUDA(cudaSetDevice(device_));
+  // oracle.cpp:33-37: same checks, same exception class
+  if (trials == 0 || runs == 0) throw Error(kInvalid, "oracle: trials and runs must be >= 1");
+  for (uint32_t sd : seeds)
+    if (sd >= g_.n) throw Error(kInvalid, "oracle: seed id out of range");
+  const uint64_t m = g_.m, n = g_.n;
+  // weights as the binding assigns them (pymodule.cpp:96-98)
+  uint32_t* w = as<uint32_t>(arena_.get("mc.w", std::max<uint64_t>(m, 1) * 4));
+  switch (ws.kind) {
+    case WeightKind::Constant: launch_weights(g_, 0, to_fixed_point(ws.a), w, stream_); break;
+    case WeightKind::WeightedCascade: launch_weights(g_, 1, 0, w, stream_); break;
+    default: {
+      if (!host_w_src) throw Error(kRuntime, "randomized weights need the host graph");
+      std::vector<uint32_t> hw;
+      assign_weights(*host_w_src, ws, derive_seed(seed, kSeedTagWeights), hw);
+      DFS_CUDA(cudaMemcpyAsync(w, hw.data(), m * 4, cudaMemcpyHostToDevice, stream_));
+      sync();
+    }
+  }
+  const uint64_t total = uint64_t(trials) * runs;
+  const uint64_t nb_total = (total + 31) / 32;
+  const uint64_t per_batch = m * 4 + 5 * n * 4 + 128;
+  size_t fr = 0, tot = 0;
+  DFS_CUDA(cudaMemGetInfo(&fr, &tot));
+  const uint64_t budget = std::min<uint64_t>(uint64_t(8) << 30, fr / 2);
+  const uint64_t nb = std::max<uint64_t>(1, std::min<uint64_t>(nb_total, budget / per_batch));
+  uint32_t* live = as<uint32_t>(arena_.get("mc.live", std::max<uint64_t>(nb * m, 1) * 4));
+  uint32_t* vis = as<uint32_t>(arena_.get("mc.vis", nb * n * 4));
+  uint32_t* fresh = as<uint32_t>(arena_.get("mc.fresh", nb * 2 * n * 4));
+  uint32_t* queue = as<uint32_t>(arena_.get("mc.queue", nb * 2 * n * 4));
+  uint32_t* reached = as<uint32_t>(arena_.get("mc.reached", nb_total * 32 * 4));
+  uint32_t* dseeds = as<uint32_t>(arena_.get("mc.seeds", std::max<size_t>(seeds.size(), 1) * 4));
+  if (!seeds.empty())
+    DFS_CUDA(cudaMemcpyAsync(dseeds, seeds.data(), seeds.size() * 4, cudaMemcpyHostToDevice,
+                             stream_));
+  const uint64_t base = derive_seed(seed, kSeedTagOracle);
+  for (uint64_t b0 = 0; b0 < nb_total; b0 += nb) {
+    const uint32_t cnt = uint32_t(std::min<uint64_t>(nb, nb_total - b0));
+    launch_mc_influence(g_, w, base, trials, total, b0, cnt, dseeds, uint32_t(seeds.size()), live,
+                        vis, fresh, queue, reached + b0 * 32, stream_);
+  }
+  std::vector<uint32_t> h(nb_total * 32);
+  DFS_CUDA(cudaMemcpyAsync(h.data(), reached, h.size() * 4, cudaMemcpyDeviceToHost, stream_));
+  sync();
+  h.resize(total);
+  // oracle.cpp:65-77, in the reference's trial order
+  double sum = 0, sumsq = 0;
+  for (uint64_t i = 0; i < total; ++i) {
+    const double reached_i = double(h[i]);
+    sum += reached_i;
+    sumsq += reached_i * reached_i;
+  }
+  const double T = double(trials) * runs;
+  *mean = sum / T;
+  *std_error = 0.0;
+  if (T > 1) {
+    const double var = (sumsq - sum * sum / T) / (T - 1);
+    *std_error = std::sqrt(std::max(0.0, var) / T);
+  }
+  return h;
 }
 
 std::vector<uint64_t> Context::fasst_stats(const RunConfig& cfg, const HostGraph* host_w_src) {

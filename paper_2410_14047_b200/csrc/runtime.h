@@ -136,6 +136,14 @@ class Context {
   // out = [dup counts 0..mu | per-chunk loads | fill live lanes | batches].
   std::vector<uint64_t> fasst_stats(const RunConfig& cfg, const HostGraph* host_w_src);
 
+  // Monte-Carlo influence (oracle.cpp:30-79) on the resident graph: per-trial
+  // reached counts (run-major), mean and standard error bit-identical to the
+  // reference's influence_stats.
+  std::vector<uint32_t> mc_influence(const std::vector<uint32_t>& seeds, uint32_t trials,
+                                     uint64_t seed, uint32_t runs, const WeightSetting& ws,
+                                     const HostGraph* host_w_src, double* mean,
+                                     double* std_error);
+
   // ---- peer mode (one FASST partition per GPU; exchange inside k_run)
   // After prepare(cfg, host, rank, world): write this rank's handle.
   void peer_export(void* out);

@@ -35,3 +35,10 @@ def golden_fasst():
     import json
     with open(os.path.join(ROOT, "tests", "golden", "fasst_stats.json")) as f:
         return json.load(f)
+
+
+@pytest.fixture(scope="session")
+def golden_influence():
+    import json
+    with open(os.path.join(ROOT, "tests", "golden", "influence.json")) as f:
+        return json.load(f)

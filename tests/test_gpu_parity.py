@@ -299,3 +299,26 @@ def test_fasst_stats_match_oracle_rmat(D, ctx, mode):
     got = ctx.fasst_stats(g, r=1024, devices=8, mode=mode, weights="wc", seed=5)
     want = O.fasst_stats(_oracle_csr(g), 1024, 8, mode, "wc", 5)
     assert got == want
+
+
+def test_mc_influence_matches_reference(D, ctx, golden_influence):
+    """Monte-Carlo influence on the GPU (32 mt19937_64 streams per block, bitset
+    BFS) == the reference's influence() bit for bit (oracle.cpp:30-79)."""
+    gs = golden_influence["graphs"]
+    for c in golden_influence["cases"]:
+        g = _graph(D, gs[c["graph"]])
+        mean, se = ctx.influence(g, c["seeds"], trials=c["trials"], seed=c["seed"], runs=c["runs"],
+                                 weights=c["weights"])
+        assert (mean.hex(), se.hex()) == (c["mean"], c["std_error"]), c
+
+
+def test_mc_influence_gpu_equals_host_rmat(D, ctx):
+    g = D.generate("rmat", 12, 40000, 5)
+    seeds = [0, 3, 77, 1000]
+    for w in ("const:0.05", "wc"):
+        got = ctx.influence(g, seeds, trials=200, seed=2, runs=2, weights=w)
+        assert got == D.influence(g, seeds, trials=200, seed=2, runs=2, weights=w)
+    with pytest.raises(ValueError):
+        ctx.influence(g, [g.n], trials=10)
+    with pytest.raises(ValueError):
+        ctx.influence(g, [0], trials=0)
