@@ -1114,16 +1114,28 @@ __device__ __forceinline__ void simulate_body(const RankDev& r, const SimOpts& a
         const bool owner = r.fwd.row_chunk[u + 1] - r.fwd.row_chunk[u] == 1;
         unsigned long long* drow = reinterpret_cast<unsigned long long*>(r.regs + uint64_t(u) * Jp);
         bool changed = false;
-        for (uint32_t b = lane; b < W32; b += 32) {
-          if (!((touched[b >> 5] >> (b & 31)) & 1u)) continue;
+        // Write-back spread over the lanes by 8-byte word (word w = batch
+        // w/4): every lane issues its (up to 4) destination loads together,
+        // so a chunk costs one memory round trip instead of one per word.
+        const uint32_t nwords = W32 * 4;
+        for (uint32_t w0 = 0; w0 < nwords; w0 += 128) {
+          unsigned long long av[4], dv[4];
 #pragma unroll
-          for (int wv = 0; wv < 4; ++wv) {
-            const unsigned long long av = acc[b * 4 + wv];
-            if (av == kNeg8) continue;
-            acc[b * 4 + wv] = kNeg8;
-            unsigned long long* dp = drow + b * 4 + wv;
-            unsigned long long d = __ldcg(dp);
-            unsigned long long nv = merge8_full(d, av);
+          for (int t = 0; t < 4; ++t) {
+            const uint32_t w = w0 + 32 * t + lane;
+            av[t] = kNeg8;
+            if (w < nwords && ((touched[w >> 7] >> ((w >> 2) & 31)) & 1u)) {
+              av[t] = acc[w];
+              if (av[t] != kNeg8) acc[w] = kNeg8;
+            }
+            dv[t] = av[t] != kNeg8 ? __ldcg(drow + w) : 0;
+          }
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            if (av[t] == kNeg8) continue;
+            unsigned long long* dp = drow + w0 + 32 * t + lane;
+            unsigned long long d = dv[t];
+            unsigned long long nv = merge8_full(d, av[t]);
             if (nv == d) continue;
             if (owner) {
               *dp = nv;
@@ -1136,7 +1148,7 @@ __device__ __forceinline__ void simulate_body(const RankDev& r, const SimOpts& a
                   break;
                 }
                 d = old;
-                nv = merge8_full(d, av);
+                nv = merge8_full(d, av[t]);
               }
             }
           }
