@@ -1078,23 +1078,23 @@ __device__ __forceinline__ void simulate_body(const RankDev& r, const SimOpts& a
           mq[q] = act ? __ldg(r.fwd.mask + i) : 0;
           bq[q] = act ? __ldg(r.fwd.batch + i) : 0;
         }
-        if (s > 1) {
-          uint32_t st[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) st[q] = mq[q] ? __ldcg(r.lstamp + vq[q]) : 0;
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (st[q] < need) mq[q] = 0;
-        }
+        // Source stamps and first live source words are loaded together
+        // (speculatively: pull sweeps run when most sources changed), then
+        // items whose source did not change since the previous sweep drop out.
+        uint32_t st[4];
         unsigned long long s0[4];
         int w0[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           w0[q] = mq[q] ? (__ffs(mq[q]) - 1) >> 3 : 0;
+          st[q] = (s > 1 && mq[q]) ? __ldcg(r.lstamp + vq[q]) : 0xFFFFFFFFu;
           s0[q] = mq[q] ? __ldcg(reinterpret_cast<const unsigned long long*>(
                               srcm + uint64_t(vq[q]) * Jp + bq[q] * 32) + w0[q])
                         : 0;
         }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (st[q] < need) mq[q] = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           if (!mq[q]) continue;
@@ -1186,19 +1186,14 @@ __device__ __forceinline__ void simulate_body(const RankDev& r, const SimOpts& a
             bq[q] = mq[q] ? __ldg(r.fwd.batch + iq[q]) : 0;
             mq[q] = mq[q] ? __ldg(r.fwd.mask + iq[q]) : 0;
           }
-          if (s > 1) {
-            uint32_t st[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) st[q] = mq[q] ? __ldcg(r.lstamp + vq[q]) : 0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if (st[q] < need) mq[q] = 0;
-          }
+          // stamps, first source and destination words in one round trip
+          uint32_t st[4];
           unsigned long long s0[4], d0[4];
           int w0[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             w0[q] = mq[q] ? (__ffs(mq[q]) - 1) >> 3 : 0;
+            st[q] = (s > 1 && mq[q]) ? __ldcg(r.lstamp + vq[q]) : 0xFFFFFFFFu;
             s0[q] = mq[q] ? __ldcg(reinterpret_cast<const unsigned long long*>(
                                 srcm + uint64_t(vq[q]) * Jp + bq[q] * 32) + w0[q])
                           : 0;
@@ -1206,6 +1201,9 @@ __device__ __forceinline__ void simulate_body(const RankDev& r, const SimOpts& a
                                 r.regs + uint64_t(uq[q]) * Jp + bq[q] * 32) + w0[q])
                           : 0;
           }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (st[q] < need) mq[q] = 0;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             if (!mq[q]) continue;
