@@ -1838,11 +1838,21 @@ __device__ __forceinline__ void cascade_body(const RankDev& r, const CasOpts& a,
           mq[q] = act ? __ldg(r.rev.mask + i) : 0;
           bq[q] = act ? __ldg(r.rev.batch + i) : 0;
         }
-        // bottom-up: only simulations still unvisited at v look for a parent
+        // bottom-up: only simulations still unvisited at v look for a parent.
+        // v's visited row is one coalesced load (lane b holds batch b) issued
+        // with the item fields; items pick their batch word by shuffle, and
+        // only items with unvisited live simulations load their parent's
+        // fresh word.
         const uint32_t* vrow = r.vis + uint64_t(v) * W32;
+        const bool narrow = W32 <= 32;
+        const uint32_t vw = (narrow && lane < W32) ? __ldcg(vrow + lane) : 0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (mq[q]) mq[q] &= ~__ldcg(vrow + bq[q]);
+        for (int q = 0; q < 4; ++q) {
+          uint32_t x;
+          if (narrow) x = __shfl_sync(0xffffffffu, vw, bq[q] & 31);
+          else x = mq[q] ? __ldcg(vrow + bq[q]) : 0;
+          mq[q] &= ~x;
+        }
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           fq[q] = mq[q] ? __ldcg(fcur + uint64_t(uq[q]) * W32 + bq[q]) & mq[q] : 0;
