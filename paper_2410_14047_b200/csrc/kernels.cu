@@ -166,7 +166,7 @@ __global__ void k_items(uint64_t npos, const uint32_t* __restrict__ p_hash,
                         const uint64_t* __restrict__ pos_off, uint32_t* __restrict__ it_other,
                         uint32_t* __restrict__ it_mask, uint8_t* __restrict__ it_batch,
                         uint32_t* __restrict__ it_row, const uint32_t* __restrict__ glut) {
-  extern __shared__ uint32_t sx[];
+  extern __shared__ __align__(16) uint32_t sx[];
   uint32_t* lut = sx + Jp;  // lut[k] = lower_bound(x, k << kLutShift), k in [0, 2^kLutBits]
   for (uint32_t i = threadIdx.x; i < Jp; i += blockDim.x) sx[i] = x[i];
   __syncthreads();
@@ -186,11 +186,17 @@ __global__ void k_items(uint64_t npos, const uint32_t* __restrict__ p_hash,
         const uint32_t other = WRITE ? p_other[p] : 0;
         const uint32_t rowv = WRITE ? p_row[p] : 0;
         for (uint32_t b = lo >> 5; b <= (hi - 1) >> 5; ++b) {
-          // only slots inside the window can pass the test
+          // Only slots inside the window can pass the test (DESIGN.md
+          // §window), and any slot outside it fails on its own, so the
+          // window is covered by aligned 4-slot vector loads without masking.
           uint32_t mk = 0;
           const uint32_t i0 = max(lo, b * 32), i1 = min(hi, b * 32 + 32);
-          for (uint32_t i = i0; i < i1; ++i)
-            mk |= uint32_t((sx[i] ^ h) < W) << (i - b * 32);  // sampling.hpp:37-39
+          for (uint32_t g = i0 & ~3u; g < i1; g += 4) {
+            const uint4 xv = *reinterpret_cast<const uint4*>(sx + g);  // sampling.hpp:37-39
+            const uint32_t m4 = uint32_t((xv.x ^ h) < W) | (uint32_t((xv.y ^ h) < W) << 1) |
+                                (uint32_t((xv.z ^ h) < W) << 2) | (uint32_t((xv.w ^ h) < W) << 3);
+            mk |= m4 << (g - b * 32);
+          }
           if (mk) {
             if (WRITE) {
               it_other[o] = other;
@@ -246,17 +252,18 @@ __global__ void k_rev_copy(uint64_t m, const uint32_t* __restrict__ tedge,
   }
 }
 
+// Transposed position p holds edge tedge[p]; its target is the sort key
+// (tdst, written by the sort), its source one gather, and its hash is
+// recomputed (hash.hpp:91-93) instead of gathered.
 __global__ void k_transpose_fields(uint64_t m, const uint32_t* __restrict__ tedge,
                                    const uint32_t* __restrict__ src,
-                                   const uint32_t* __restrict__ adj,
-                                   const uint32_t* __restrict__ ehash, uint32_t* __restrict__ tsrc,
-                                   uint32_t* __restrict__ thash, uint32_t* __restrict__ tdst) {
+                                   const uint32_t* __restrict__ tdst, uint32_t* __restrict__ tsrc,
+                                   uint32_t* __restrict__ thash) {
   for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < m;
        p += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t e = tedge[p];
-    tsrc[p] = src[e];
-    thash[p] = ehash[e];
-    tdst[p] = adj[e];
+    const uint32_t u = src[tedge[p]];
+    tsrc[p] = u;
+    thash[p] = edge_hash(u, tdst[p]);
   }
 }
 
@@ -2317,8 +2324,10 @@ void launch_graph_prepare(DevGraph& g, void* tmp, size_t tmp_bytes, cudaStream_t
     int end_bit = 1;
     while (end_bit < 32 && (uint64_t(1) << end_bit) < g.n) ++end_bit;
     size_t bytes = cub_bytes;
-    DFS_CUDA(cub::DeviceRadixSort::SortPairs(cubtmp, bytes, g.adj, keys_out, iota, g.tedge, m, 0,
+    // keys out = the targets in transposed order (tdst), values out = edge ids
+    DFS_CUDA(cub::DeviceRadixSort::SortPairs(cubtmp, bytes, g.adj, g.tdst, iota, g.tedge, m, 0,
                                              end_bit, s));
+    (void)keys_out;
 
   }
   // toff = exclusive scan of in-degrees (indeg[n] == 0 by the memset above)
@@ -2326,8 +2335,8 @@ void launch_graph_prepare(DevGraph& g, void* tmp, size_t tmp_bytes, cudaStream_t
   DFS_CUDA(cub::DeviceScan::ExclusiveScan(cubtmp, bytes, g.indeg, g.toff,
                                           cuda::std::plus<uint64_t>{}, uint64_t(0), g.n + 1, s));
   if (m)
-    k_transpose_fields<<<grid_for(m), kThreads, 0, s>>>(m, g.tedge, g.src, g.adj, g.ehash, g.tsrc,
-                                                       g.thash, g.tdst);
+    k_transpose_fields<<<grid_for(m), kThreads, 0, s>>>(m, g.tedge, g.src, g.tdst, g.tsrc,
+                                                       g.thash);
   DFS_CUDA(cudaGetLastError());
   ++g_launches;
 }
