@@ -156,7 +156,16 @@ struct RunArrays {
   uint32_t* blk_arg = nullptr;
   uint32_t* blk_min = nullptr;
   uint32_t nblk = 0;
+  // Argmax cache (one local partition): best positive uncommitted (score,
+  // id) and smallest uncommitted id of every kSeg-row segment; only segments
+  // holding rescored rows are recomputed each round.
+  double* seg_score = nullptr;
+  uint32_t* seg_arg = nullptr;
+  uint32_t* seg_min = nullptr;
+  uint32_t* seg_stamp = nullptr;
+  uint32_t nseg = 0;
 };
+constexpr uint32_t kSeg = 1024;
 
 // ---------------------------------------------------------------- peer mode
 // Multi-GPU: one FASST partition per GPU (one process, or one context, per

@@ -893,6 +893,7 @@ __device__ __forceinline__ void for_frontier_items(const Items& it, const uint32
 
 constexpr unsigned long long kNeg8 = 0x8080808080808080ull;  // "no contribution"
 constexpr uint32_t kSoloChunks = 16;  // frontier (chunks) a single block iterates alone
+constexpr uint32_t kSoloDirty = 512;  // dirty rows block 0 rescores alone
 constexpr uint32_t kPullMaxJp = 4096;  // pull accumulators live in shared memory
 
 // Shared-memory running max of the live bytes of one source word.
@@ -1465,12 +1466,14 @@ __device__ __forceinline__ void score_acc(uint4 v, const uint32_t* tbl, uint32_t
 __device__ __forceinline__ void score_body(const int8_t* __restrict__ regs, uint32_t n, uint32_t J,
                                            uint32_t Jp, int K, int full,
                                            const uint32_t* __restrict__ rows, RankCtl* ctl,
-                                           double* __restrict__ scores, uint32_t* tbl) {
+                                           double* __restrict__ scores, uint32_t* tbl,
+                                           bool block_only = false) {
   score_table(tbl, K);
   const uint32_t nrows = full ? n : ld_volatile(&ctl->dirty_count);
   const unsigned lane = lane_id();
-  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = block_only ? kWarps : (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t gw = block_only ? threadIdx.x >> 5
+                                 : (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   // G lanes per row (power of two <= the row's 16-byte words), R rows per
   // warp, two row groups per step: every lane keeps up to 8 independent
   // 16-byte loads in flight before reducing (the score is a streaming pass).
@@ -1664,6 +1667,66 @@ __device__ __forceinline__ void commit_choice(Best t, const RunArrays& ra) {
 __device__ __forceinline__ void argmax_finish(uint32_t nblk, const RunArrays& ra, Best* sb) {
   const Best t = argmax_combine(nblk, ra, sb);
   if (threadIdx.x == 0) commit_choice(t, ra);
+}
+
+// Argmax cache: best of segment `seg` (one warp; ascending ids per lane, then
+// best_of = strict > from 0.0 with ties to the smaller id, runtime.cpp:95-119).
+__device__ __forceinline__ void seg_recompute(const double* __restrict__ scores, uint32_t n,
+                                              uint32_t seg, const RunArrays& ra) {
+  const unsigned lane = lane_id();
+  Best b{0.0, 0xFFFFFFFFu, 0xFFFFFFFFu};
+  const uint32_t lo = seg * kSeg, hi = min(n, lo + kSeg);
+  for (uint32_t v0 = lo + lane; v0 < hi; v0 += 256) {
+    double sc[8];
+    uint32_t cm[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {  // 8 independent loads in flight per lane
+      const uint32_t v = v0 + 32 * k;
+      const bool ok = v < hi;
+      sc[k] = ok ? __ldcg(scores + v) : 0.0;
+      cm[k] = ok ? ld_volatile(ra.committed + v) : 1u;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (cm[k]) continue;
+      const uint32_t v = v0 + 32 * k;
+      if (b.minu == 0xFFFFFFFFu) b.minu = v;
+      if (sc[k] > b.s) {
+        b.s = sc[k];
+        b.v = v;
+      }
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    Best x{__shfl_xor_sync(0xffffffffu, b.s, o), __shfl_xor_sync(0xffffffffu, b.v, o),
+           __shfl_xor_sync(0xffffffffu, b.minu, o)};
+    b = best_of(b, x);
+  }
+  if (lane == 0) {
+    ra.seg_score[seg] = b.s;
+    ra.seg_arg[seg] = b.v;
+    ra.seg_min[seg] = b.minu;
+  }
+}
+
+// Block-wide best over the segment cache; valid in thread 0.
+__device__ __forceinline__ Best seg_combine(const RunArrays& ra, Best* sb) {
+  Best t{0.0, 0xFFFFFFFFu, 0xFFFFFFFFu};
+  for (uint32_t k = threadIdx.x; k < ra.nseg; k += blockDim.x)
+    t = best_of(t, Best{__ldcg(ra.seg_score + k), __ldcg(ra.seg_arg + k), __ldcg(ra.seg_min + k)});
+  for (int o = 16; o; o >>= 1) {
+    Best x{__shfl_xor_sync(0xffffffffu, t.s, o), __shfl_xor_sync(0xffffffffu, t.v, o),
+           __shfl_xor_sync(0xffffffffu, t.minu, o)};
+    t = best_of(t, x);
+  }
+  __syncthreads();
+  if (lane_id() == 0) sb[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    t = sb[0];
+    for (int w = 1; w < kWarps; ++w) t = best_of(t, sb[w]);
+  }
+  return t;
 }
 
 __global__ void __launch_bounds__(kThreads) k_argmax(const double* __restrict__ scores,
@@ -2152,6 +2215,9 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
     __syncthreads();
   };
   const SimOpts so{a.cap, a.dbg, a.sim_pull_f};
+  // one local partition, no peers: argmax through the segment cache, and
+  // rounds with few dirty rows run their select step in block 0 alone
+  const bool segs = a.mu == 1 && !a.peer;
   bool first_fill = true;  // the first fill ran as a separate full-occupancy launch
   auto rebuild = [&]() {  // fill -> simulate -> full rescore, every partition
     if (!first_fill)
@@ -2174,6 +2240,13 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
                  reinterpret_cast<uint32_t*>(dyn_smem));
     }
     grid.sync();
+    if (segs) {  // full rescore: rebuild the whole argmax cache
+      const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+      const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+      for (uint64_t sg = gw; sg < a.ra.nseg; sg += nw)
+        seg_recompute(a.ranks[0].scores, a.n, uint32_t(sg), a.ra);
+      grid.sync();
+    }
   };
   rebuild();
   bool rebuilt = true;
@@ -2183,17 +2256,69 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
   const uint32_t pslice = a.peer ? (a.n + a.pv.world - 1) / a.pv.world : 0;
   const uint32_t plo = a.peer ? min(a.n, a.pv.rank * pslice) : 0;
   const uint32_t phi = a.peer ? min(a.n, plo + pslice) : 0;
+  const bool tr = (a.dbg & 4) && blockIdx.x == 0 && threadIdx.x == 0;  // DFS_DBG bit 2
   for (uint32_t step = 0; step < a.k; ++step) {
-    if (!rebuilt) {  // rows dirtied by the last cascade
+    if (tr) trace(4, step, 0);
+    if (segs) {
+      // select (runtime.cpp:88-121) through the argmax cache.  Small dirty
+      // sets: block 0 rescores them, refreshes their segments and picks the
+      // winner with block barriers only; the other blocks go straight to the
+      // cascade, whose first (solo) levels block 0 runs as well.
+      const RankDev& r0 = a.ranks[0];
+      const uint32_t nd = rebuilt ? 0u : ld_volatile(&r0.ctl->dirty_count);
+      if (nd <= kSoloDirty) {
+        if (blockIdx.x == 0) {
+          if (!rebuilt) {
+            load_rank(0);
+            score_body(s_r.regs, s_r.n, s_r.J, s_r.Jp, a.K, 0, s_r.dirty, s_r.ctl, s_r.scores,
+                       reinterpret_cast<uint32_t*>(dyn_smem), true);
+            __syncthreads();
+            // duplicates of one segment compute identical values (benign)
+            for (uint32_t i = threadIdx.x >> 5; i < nd; i += kWarps)
+              seg_recompute(r0.scores, a.n, __ldcg(r0.dirty + i) / kSeg, a.ra);
+            __syncthreads();
+          }
+          const Best t = seg_combine(a.ra, sb);
+          if (threadIdx.x == 0) commit_choice(t, a.ra);
+          __syncthreads();
+          if (tr) trace(7, step, ld_volatile(&a.ra.ctl->choice));
+        }
+      } else {
+        score_body(r0.regs, r0.n, r0.J, r0.Jp, a.K, 0, r0.dirty, r0.ctl, r0.scores,
+                   reinterpret_cast<uint32_t*>(dyn_smem));
+        grid.sync();
+        const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+        const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+        const uint32_t stampv = step + 1;
+        for (uint64_t i = gw; i < nd; i += nw) {
+          const uint32_t sg = __ldcg(r0.dirty + i) / kSeg;
+          unsigned prev = 0;
+          if (lane_id() == 0) prev = atomicExch(&a.ra.seg_stamp[sg], stampv);
+          prev = __shfl_sync(0xffffffffu, prev, 0);
+          if (prev != stampv) seg_recompute(r0.scores, a.n, sg, a.ra);
+        }
+        grid.sync();
+        if (blockIdx.x == 0) {
+          const Best t = seg_combine(a.ra, sb);
+          if (threadIdx.x == 0) commit_choice(t, a.ra);
+          __syncthreads();
+        }
+      }
+      rebuilt = false;
+      // the cascade's commit (block 0, warp 0) reads the choice; the other
+      // blocks wait on its release word, so no grid barrier is needed here
+    } else if (!rebuilt) {  // rows dirtied by the last cascade
       for (uint32_t t = 0; t < a.mu; ++t) {
         load_rank(t);
         score_body(s_r.regs, s_r.n, s_r.J, s_r.Jp, a.K, 0, s_r.dirty, s_r.ctl, s_r.scores,
                    reinterpret_cast<uint32_t*>(dyn_smem));
       }
       grid.sync();
+      if (tr) trace(5, step, ld_volatile(&a.ranks[0].ctl->dirty_count));
     }
-    rebuilt = false;
-    if (a.peer) {
+    if (!segs) rebuilt = false;
+    if (segs) {
+    } else if (a.peer) {
       // reduce_to_root + root argmax + broadcast (runtime.cpp:88-121) as: all
       // partial scores final -> slice sum in binomial order + slice argmax ->
       // publish (score, id, min-uncommitted) -> every rank picks the winner.
@@ -2227,8 +2352,10 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
       }
       argmax_partial(argsrc, a.n, a.ra, sb);
       grid.sync();
+      if (tr) trace(6, step, 0);
       if (blockIdx.x == 0) argmax_finish(gridDim.x, a.ra, sb);
       grid.sync();
+      if (tr) trace(7, step, ld_volatile(&a.ra.ctl->choice));
     }
     phase(2);
     for (uint32_t t = 0; t < a.mu; ++t) {
@@ -2270,9 +2397,10 @@ void dump_trace() {
   DFS_CUDA(cudaMemcpyFromSymbol(&n, g_trace_n, sizeof n));
   n = n > 8192 ? 8192 : n;
   DFS_CUDA(cudaMemcpyFromSymbol(h, g_trace, sizeof(unsigned long long) * 4 * n));
-  static const char* names[] = {"sim", "sim-solo", "cas", "cas-solo"};
+  static const char* names[] = {"sim",   "sim-solo", "cas",    "cas-solo",
+                                "round", "rescored", "argmax", "chosen"};
   for (unsigned i = 0; i < n; ++i)
-    fprintf(stderr, "trace %-8s idx=%-4llu nc=%-8llu dt=%.1f us\n", names[h[i][0] & 3], h[i][1],
+    fprintf(stderr, "trace %-8s idx=%-4llu nc=%-8llu dt=%.1f us\n", names[h[i][0] & 7], h[i][1],
             h[i][2], i ? (h[i][3] - h[i - 1][3]) / 1965.0 : 0.0);
   unsigned int z = 0;
   DFS_CUDA(cudaMemcpyToSymbol(g_trace_n, &z, sizeof z));

@@ -470,6 +470,12 @@ Report Context::run_impl(const RunConfig& cfg, const HostGraph* host_w_src, bool
   ra.blk_score = as<double>(arena_.get("run.bs", ra.nblk * 8));
   ra.blk_arg = as<uint32_t>(arena_.get("run.ba", ra.nblk * 4));
   ra.blk_min = as<uint32_t>(arena_.get("run.bm", ra.nblk * 4));
+  ra.nseg = (n + kSeg - 1) / kSeg;
+  ra.seg_score = as<double>(arena_.get("run.ss", std::max<uint32_t>(ra.nseg, 1) * 8));
+  ra.seg_arg = as<uint32_t>(arena_.get("run.sa", std::max<uint32_t>(ra.nseg, 1) * 4));
+  ra.seg_min = as<uint32_t>(arena_.get("run.sm", std::max<uint32_t>(ra.nseg, 1) * 4));
+  ra.seg_stamp = as<uint32_t>(arena_.get("run.st", std::max<uint32_t>(ra.nseg, 1) * 4));
+  DFS_CUDA(cudaMemsetAsync(ra.seg_stamp, 0, std::max<uint32_t>(ra.nseg, 1) * 4, s));
   DFS_CUDA(cudaMemsetAsync(ra.ctl, 0, sizeof(RunCtl), s));
   DFS_CUDA(cudaMemsetAsync(ra.committed, 0, std::max<uint32_t>(n, 1), s));
   const double* argmax_src = ranks_[0].scores;
