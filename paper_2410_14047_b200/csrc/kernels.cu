@@ -1436,10 +1436,10 @@ __device__ __forceinline__ void pin_after_loads(uint4& v) {
 // 2^60 (flags the exact sequential fallback: without it the sum is <= J <
 // 2^50); negative bytes (VISITED) -> 0.0.  32-bit entries: one bank per
 // value, so a warp's lookups are (nearly) conflict-free.
-constexpr double kScoreFlag = 1152921504606846976.0;  // 2^60
 __device__ __forceinline__ void score_table(uint32_t* tbl, int K) {
+  // high word of 2^-b is (1023 - b) << 20 (b <= 64 keeps it normal); 2^60 flags
   for (int b = threadIdx.x; b < 256; b += blockDim.x)
-    tbl[b] = b >= 128 ? 0u : uint32_t(__double2hiint(b <= K ? ldexp(1.0, -b) : kScoreFlag));
+    tbl[b] = b >= 128 ? 0u : (b <= K ? uint32_t(1023 - b) << 20 : uint32_t(1023 + 60) << 20);
   __syncthreads();
 }
 
