@@ -137,13 +137,7 @@ void Context::alloc_rank(RankDev& r, uint32_t tau) {
   r.jkey = as<uint64_t>(arena_.get(p + "jkey", r.Jp * 8));
   r.regs = as<int8_t>(arena_.get(p + "regs", nn * r.Jp));
   r.snap = cfg_.jacobi ? as<int8_t>(arena_.get(p + "snap", nn * r.Jp)) : nullptr;
-  {  // cached first fill, when HBM allows (rebuild fills become a copy)
-    size_t fr = 0, tot = 0;
-    DFS_CUDA(cudaMemGetInfo(&fr, &tot));
-    r.pristine = fr > 3 * nn * r.Jp + (size_t(2) << 30)
-                     ? as<int8_t>(arena_.get(p + "pristine", nn * r.Jp))
-                     : nullptr;
-  }
+  r.pristine = nullptr;  // decided once every partition is built (prepare)
   r.vis = as<uint32_t>(arena_.get(p + "vis", nn * r.W32 * 4));
   r.fresh[0] = as<uint32_t>(arena_.get(p + "fresh0", nn * r.W32 * 4));
   r.fresh[1] = as<uint32_t>(arena_.get(p + "fresh1", nn * r.W32 * 4));
@@ -291,6 +285,16 @@ void Context::prepare(const RunConfig& cfg, const HostGraph* host_w_src, uint32_
                                              std::max<uint32_t>(g_.n, 1) * 4));
     }
     reset_rank_state(r);
+  }
+  // Cached first fill per partition (rebuild fills become a copy), only while
+  // HBM allows once every partition's working set is allocated.
+  for (RankDev& r : ranks_) {
+    const size_t bytes = std::max<size_t>(r.n, 1) * r.Jp;
+    const std::string name = "r" + std::to_string(r.tau) + ".pristine";
+    size_t fr = 0, tot = 0;
+    DFS_CUDA(cudaMemGetInfo(&fr, &tot));
+    if (arena_.has(name, bytes) || fr > bytes + (size_t(4) << 30))
+      r.pristine = as<int8_t>(arena_.get(name, bytes));
   }
   prep_seconds_ = since(t0);
 }

@@ -21,6 +21,11 @@ class Arena {
  public:
   ~Arena();
   void* get(const std::string& name, size_t bytes);
+  // Already holds a buffer of at least `bytes` under `name`?
+  bool has(const std::string& name, size_t bytes) const {
+    auto it = bufs_.find(name);
+    return it != bufs_.end() && it->second.bytes >= bytes;
+  }
   size_t bytes() const { return total_; }
   void release();
 
