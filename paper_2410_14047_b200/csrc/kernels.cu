@@ -2215,9 +2215,19 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
     __syncthreads();
   };
   const SimOpts so{a.cap, a.dbg, a.sim_pull_f};
-  // one local partition, no peers: argmax through the segment cache, and
-  // rounds with few dirty rows run their select step in block 0 alone
-  const bool segs = a.mu == 1 && !a.peer;
+  // no peers: argmax through the segment cache (over the binomial-order sum
+  // of the partitions' scores when mu > 1), and rounds with few dirty rows
+  // run their select step in block 0 alone
+  const bool segs = !a.peer;
+  const double* segsrc = a.mu > 1 ? a.reduced : a.ranks[0].scores;
+  // reduced score of v from the mu partial vectors (collectives.cpp:51-59)
+  auto reduce_row = [&](uint32_t v) {
+    double acc[64];
+    for (uint32_t t = 0; t < a.mu; ++t) acc[t] = __ldcg(a.parts[t] + v);
+    for (uint32_t st = 1; st < a.mu; st <<= 1)
+      for (uint32_t t = 0; t + st < a.mu; t += 2 * st) acc[t] = __dadd_rn(acc[t], acc[t + st]);
+    a.reduced[v] = acc[0];
+  };
   bool first_fill = true;  // the first fill ran as a separate full-occupancy launch
   auto rebuild = [&]() {  // fill -> simulate -> full rescore, every partition
     if (!first_fill)
@@ -2241,10 +2251,14 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
     }
     grid.sync();
     if (segs) {  // full rescore: rebuild the whole argmax cache
+      if (a.mu > 1) {
+        treesum_body(a.parts, a.mu, a.n, a.reduced);
+        grid.sync();
+      }
       const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
       const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
       for (uint64_t sg = gw; sg < a.ra.nseg; sg += nw)
-        seg_recompute(a.ranks[0].scores, a.n, uint32_t(sg), a.ra);
+        seg_recompute(segsrc, a.n, uint32_t(sg), a.ra);
       grid.sync();
     }
   };
@@ -2264,18 +2278,33 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
       // sets: block 0 rescores them, refreshes their segments and picks the
       // winner with block barriers only; the other blocks go straight to the
       // cascade, whose first (solo) levels block 0 runs as well.
-      const RankDev& r0 = a.ranks[0];
-      const uint32_t nd = rebuilt ? 0u : ld_volatile(&r0.ctl->dirty_count);
+      uint32_t nd = 0;  // dirty rows over all partitions
+      if (!rebuilt)
+        for (uint32_t t = 0; t < a.mu; ++t) nd += ld_volatile(&a.ranks[t].ctl->dirty_count);
       if (nd <= kSoloDirty) {
         if (blockIdx.x == 0) {
           if (!rebuilt) {
-            load_rank(0);
-            score_body(s_r.regs, s_r.n, s_r.J, s_r.Jp, a.K, 0, s_r.dirty, s_r.ctl, s_r.scores,
-                       reinterpret_cast<uint32_t*>(dyn_smem), true);
+            for (uint32_t t = 0; t < a.mu; ++t) {
+              load_rank(t);
+              score_body(s_r.regs, s_r.n, s_r.J, s_r.Jp, a.K, 0, s_r.dirty, s_r.ctl, s_r.scores,
+                         reinterpret_cast<uint32_t*>(dyn_smem), true);
+            }
             __syncthreads();
+            if (a.mu > 1) {  // rows dirty in any partition: new binomial sums
+              for (uint32_t t = 0; t < a.mu; ++t) {
+                const RankDev& rt = a.ranks[t];
+                const uint32_t c = ld_volatile(&rt.ctl->dirty_count);
+                for (uint32_t i = threadIdx.x; i < c; i += blockDim.x) reduce_row(__ldcg(rt.dirty + i));
+              }
+              __syncthreads();
+            }
             // duplicates of one segment compute identical values (benign)
-            for (uint32_t i = threadIdx.x >> 5; i < nd; i += kWarps)
-              seg_recompute(r0.scores, a.n, __ldcg(r0.dirty + i) / kSeg, a.ra);
+            for (uint32_t t = 0; t < a.mu; ++t) {
+              const RankDev& rt = a.ranks[t];
+              const uint32_t c = ld_volatile(&rt.ctl->dirty_count);
+              for (uint32_t i = threadIdx.x >> 5; i < c; i += kWarps)
+                seg_recompute(segsrc, a.n, __ldcg(rt.dirty + i) / kSeg, a.ra);
+            }
             __syncthreads();
           }
           const Best t = seg_combine(a.ra, sb);
@@ -2284,18 +2313,34 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
           if (tr) trace(7, step, ld_volatile(&a.ra.ctl->choice));
         }
       } else {
-        score_body(r0.regs, r0.n, r0.J, r0.Jp, a.K, 0, r0.dirty, r0.ctl, r0.scores,
-                   reinterpret_cast<uint32_t*>(dyn_smem));
+        for (uint32_t t = 0; t < a.mu; ++t) {
+          load_rank(t);
+          score_body(s_r.regs, s_r.n, s_r.J, s_r.Jp, a.K, 0, s_r.dirty, s_r.ctl, s_r.scores,
+                     reinterpret_cast<uint32_t*>(dyn_smem));
+        }
         grid.sync();
-        const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-        const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+        const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+        const uint64_t gthreads = uint64_t(gridDim.x) * blockDim.x;
+        if (a.mu > 1) {
+          for (uint32_t t = 0; t < a.mu; ++t) {
+            const RankDev& rt = a.ranks[t];
+            const uint32_t c = ld_volatile(&rt.ctl->dirty_count);
+            for (uint64_t i = gtid; i < c; i += gthreads) reduce_row(__ldcg(rt.dirty + i));
+          }
+          grid.sync();
+        }
+        const uint64_t gw = gtid >> 5, nw = gthreads >> 5;
         const uint32_t stampv = step + 1;
-        for (uint64_t i = gw; i < nd; i += nw) {
-          const uint32_t sg = __ldcg(r0.dirty + i) / kSeg;
-          unsigned prev = 0;
-          if (lane_id() == 0) prev = atomicExch(&a.ra.seg_stamp[sg], stampv);
-          prev = __shfl_sync(0xffffffffu, prev, 0);
-          if (prev != stampv) seg_recompute(r0.scores, a.n, sg, a.ra);
+        for (uint32_t t = 0; t < a.mu; ++t) {
+          const RankDev& rt = a.ranks[t];
+          const uint32_t c = ld_volatile(&rt.ctl->dirty_count);
+          for (uint64_t i = gw; i < c; i += nw) {
+            const uint32_t sg = __ldcg(rt.dirty + i) / kSeg;
+            unsigned prev = 0;
+            if (lane_id() == 0) prev = atomicExch(&a.ra.seg_stamp[sg], stampv);
+            prev = __shfl_sync(0xffffffffu, prev, 0);
+            if (prev != stampv) seg_recompute(segsrc, a.n, sg, a.ra);
+          }
         }
         grid.sync();
         if (blockIdx.x == 0) {
