@@ -1,0 +1,7 @@
+#!/bin/bash
+# Pull-threshold sweep: tools/knob_sweep.sh cfg
+cfg=$1
+for sp in 2 4 8 16; do for cp in 4 8 16; do
+  echo -n "SIM_PULL=$sp CAS_PULL=$cp $cfg: "
+  DFS_SIM_PULL=$sp DFS_CAS_PULL=$cp timeout 300 python tools/profile_run.py $cfg 2 2>&1 | tail -1 | python -c "import sys,ast; d=ast.literal_eval(sys.stdin.read()); print({k: round(d[k]*1e3,3) for k in ('simulate','cascade','select','total')})"
+done; done
