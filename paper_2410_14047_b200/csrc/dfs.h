@@ -141,7 +141,8 @@ struct RunCtl {
   unsigned int rebuild_now;
   unsigned int n_rebuilds;
   unsigned int argmax_done;       // last-block counter of the argmax
-  unsigned int pad[2];
+  unsigned int snap_dirty;        // dirty rows left by the last cascade (all partitions)
+  unsigned int pad;
   double oldscore;
 };
 

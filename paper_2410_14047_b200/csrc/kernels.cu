@@ -1006,13 +1006,16 @@ struct SimOpts {
 };
 
 template <int JAC, int CNT>
-__device__ __forceinline__ void simulate_body(const RankDev& r, const SimOpts& a,
+// `base`: this partition's stamp base, identical in every block (callers pass
+// a value no block can have advanced yet); returns the next base.  Reading
+// r.ctl->tick here instead would race with block 0 finishing a solo-only
+// phase (and advancing the tick) before a late block starts it.
+__device__ __forceinline__ uint32_t simulate_body(const RankDev& r, const SimOpts& a,
                                               cg::grid_group& grid, WarpStage* stage,
                                               unsigned long long& s_release,
-                                              unsigned long long* dyn_smem) {
+                                              unsigned long long* dyn_smem, uint32_t base) {
   unsigned int* cnt = r.q.counts;
   unsigned long long* qc = reinterpret_cast<unsigned long long*>(r.q.counts);
-  const uint32_t base = ld_volatile(&r.ctl->tick);
   const unsigned lane = lane_id();
   const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const uint64_t gthreads = uint64_t(gridDim.x) * blockDim.x;
@@ -1392,6 +1395,7 @@ __device__ __forceinline__ void simulate_body(const RankDev& r, const SimOpts& a
     r.ctl->tick = base + s + 2;
     if (err) r.ctl->error = 1;
   }
+  return base + s + 2;
 }
 
 template <int JAC, int CNT>
@@ -1405,7 +1409,9 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) 
   __syncthreads();
   cg::grid_group grid = cg::this_grid();
   const SimOpts o{a.cap, a.dbg, a.pull_f};
-  simulate_body<JAC, CNT>(s_r, o, grid, stage, s_release, dyn_smem);
+  // read before simulate_body's first grid barrier: no block can advance it yet
+  const uint32_t base = ld_volatile(&a.r.ctl->tick);
+  simulate_body<JAC, CNT>(s_r, o, grid, stage, s_release, dyn_smem, base);
 }
 
 // ---------------------------------------------------------------- score
@@ -1776,12 +1782,13 @@ struct CasOpts {
   int cnt;  // count mode: tally the reference-schedule cascade work units
 };
 
-__device__ __forceinline__ void cascade_body(const RankDev& r, const CasOpts& a,
+// `base` as in simulate_body; returns the next stamp base.
+__device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts& a,
                                              cg::grid_group& grid, WarpStage* stage,
-                                             unsigned long long& s_release, uint32_t* cas_smem) {
+                                             unsigned long long& s_release, uint32_t* cas_smem,
+                                                 uint32_t base) {
   unsigned int* cnt = r.q.counts;
   unsigned long long* qc = reinterpret_cast<unsigned long long*>(r.q.counts);
-  const uint32_t base = ld_volatile(&r.ctl->tick);
   const unsigned lane = lane_id();
   const uint64_t gwarp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
@@ -2049,6 +2056,7 @@ __device__ __forceinline__ void cascade_body(const RankDev& r, const CasOpts& a,
     r.ctl->levels = L;
     r.ctl->tick = base + L + 2;
   }
+  return base + L + 2;
 }
 
 __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_cascade(CasArgs a) {
@@ -2060,7 +2068,9 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_cascade(CasArgs a) {
   __syncthreads();
   cg::grid_group grid = cg::this_grid();
   const CasOpts o{a.choice, a.seed, a.dbg, a.pull_f, 0};
-  cascade_body(s_r, o, grid, stage, s_release, reinterpret_cast<uint32_t*>(dyn_smem));
+  const uint32_t base = ld_volatile(&a.r.ctl->tick);
+  grid.sync();  // every block holds `base` before block 0 can finish a solo cascade
+  cascade_body(s_r, o, grid, stage, s_release, reinterpret_cast<uint32_t*>(dyn_smem), base);
 }
 
 // ---------------------------------------------------------------- round end
@@ -2180,16 +2190,17 @@ __device__ __forceinline__ double peer_reduced(const PeerView& pv, uint32_t v) {
 
 // Out-of-line phase bodies keep the register allocation of each phase local.
 template <int JAC, int CNT>
-__device__ __noinline__ void run_simulate(const RankDev& r, const SimOpts& o, WarpStage* stage,
-                                          unsigned long long& s_release,
-                                          unsigned long long* dyn) {
+__device__ __noinline__ uint32_t run_simulate(const RankDev& r, const SimOpts& o, WarpStage* stage,
+                                              unsigned long long& s_release,
+                                              unsigned long long* dyn, uint32_t base) {
   cg::grid_group grid = cg::this_grid();
-  simulate_body<JAC, CNT>(r, o, grid, stage, s_release, dyn);
+  return simulate_body<JAC, CNT>(r, o, grid, stage, s_release, dyn, base);
 }
-__device__ __noinline__ void run_cascade(const RankDev& r, const CasOpts& o, WarpStage* stage,
-                                         unsigned long long& s_release, uint32_t* dyn) {
+__device__ __noinline__ uint32_t run_cascade(const RankDev& r, const CasOpts& o, WarpStage* stage,
+                                             unsigned long long& s_release, uint32_t* dyn,
+                                             uint32_t base) {
   cg::grid_group grid = cg::this_grid();
-  cascade_body(r, o, grid, stage, s_release, dyn);
+  return cascade_body(r, o, grid, stage, s_release, dyn, base);
 }
 
 template <int JAC, int CNT>
@@ -2198,8 +2209,14 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
   __shared__ unsigned long long s_release;
   __shared__ RankDev s_r;
   __shared__ Best sb[kWarps];
+  // Per-partition stamp bases, tracked identically by every block (each phase
+  // returns the next one) so that no block reads a tick another block may
+  // already have advanced.  Read once here, before the first grid barrier.
+  __shared__ uint32_t s_tick[64];
   extern __shared__ unsigned long long dyn_smem[];
   cg::grid_group grid = cg::this_grid();
+  for (uint32_t t = threadIdx.x; t < a.mu; t += blockDim.x) s_tick[t] = ld_volatile(&a.ranks[t].ctl->tick);
+  __syncthreads();
   const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
   unsigned long long t0 = timer ? global_ns() : 0;
   auto phase = [&](int which) {
@@ -2240,8 +2257,9 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
     phase(0);
     for (uint32_t t = 0; t < a.mu; ++t) {
       load_rank(t);
-      run_simulate<JAC, CNT>(s_r, so, stage, s_release, dyn_smem);
+      const uint32_t nt = run_simulate<JAC, CNT>(s_r, so, stage, s_release, dyn_smem, s_tick[t]);
       grid.sync();
+      if (threadIdx.x == 0) s_tick[t] = nt;
     }
     phase(1);
     for (uint32_t t = 0; t < a.mu; ++t) {
@@ -2278,9 +2296,8 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
       // sets: block 0 rescores them, refreshes their segments and picks the
       // winner with block barriers only; the other blocks go straight to the
       // cascade, whose first (solo) levels block 0 runs as well.
-      uint32_t nd = 0;  // dirty rows over all partitions
-      if (!rebuilt)
-        for (uint32_t t = 0; t < a.mu; ++t) nd += ld_volatile(&a.ranks[t].ctl->dirty_count);
+      // dirty rows over all partitions (snapshot of the previous round end)
+      const uint32_t nd = rebuilt ? 0u : ld_volatile(&a.ra.ctl->snap_dirty);
       if (nd <= kSoloDirty) {
         if (blockIdx.x == 0) {
           if (!rebuilt) {
@@ -2406,8 +2423,17 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
     for (uint32_t t = 0; t < a.mu; ++t) {
       load_rank(t);
       const CasOpts co{&a.ra.ctl->choice, 0, a.dbg, a.cas_pull_f, CNT};
-      run_cascade(s_r, co, stage, s_release, reinterpret_cast<uint32_t*>(dyn_smem));
+      const uint32_t nt =
+          run_cascade(s_r, co, stage, s_release, reinterpret_cast<uint32_t*>(dyn_smem), s_tick[t]);
       grid.sync();
+      if (threadIdx.x == 0) s_tick[t] = nt;
+    }
+    // dirty rows for the next select, snapshotted before the barrier below: the
+    // next cascade (block 0 may start it early) overwrites the counts
+    if (segs && blockIdx.x == 0 && threadIdx.x == 0) {
+      uint32_t nd = 0;
+      for (uint32_t t = 0; t < a.mu; ++t) nd += ld_volatile(&a.ranks[t].ctl->dirty_count);
+      a.ra.ctl->snap_dirty = nd;
     }
     if (a.peer) {  // allreduce(count_visited) (runtime.cpp:129, collectives.cpp:96-113)
       if (blockIdx.x == 0 && threadIdx.x == 0)
