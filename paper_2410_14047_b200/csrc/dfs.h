@@ -237,10 +237,14 @@ void launch_rev_copy(const DevGraph& g, const uint32_t* cnt_f, const uint32_t* c
 void launch_row_offsets(const DevGraph& g, int dir, const uint64_t* pos_off, Items& it,
                         uint32_t* row_cnt, cudaStream_t s);
 void launch_chunk_write(uint32_t n, Items& it, const uint64_t* row_chunk64, cudaStream_t s);
-// Split chunk ids into it.small / it.big (counts written to cnt2[0..1]).
-void launch_split_chunks(Items& it, unsigned int* cnt2, cudaStream_t s);
-// it.small_items <- item indices of the chunks in it.small (count in *cnt).
-void launch_small_items(Items& it, unsigned long long* cnt, cudaStream_t s);
+// Split chunk ids into it.small / it.big (counts written to cnt2[0..1]); the
+// chunk count is read on the device (*chunks_dev), chunks_cap bounds it.
+void launch_split_chunks(Items& it, const uint64_t* chunks_dev, uint64_t chunks_cap,
+                         unsigned int* cnt2, cudaStream_t s);
+// it.small_items <- item indices of the chunks in it.small (count *nsmall_dev
+// on the device; total items written to *cnt).
+void launch_small_items(Items& it, const unsigned int* nsmall_dev, uint64_t chunks_cap,
+                        unsigned long long* cnt, cudaStream_t s);
 // Fill registers (VISITED kept, pads VISITED).  gate: run only if *gate == want.
 void launch_fill(const RankDev& r, const unsigned int* gate, unsigned int want, cudaStream_t s,
                  bool use_pristine = false);

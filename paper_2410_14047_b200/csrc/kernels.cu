@@ -317,9 +317,12 @@ __global__ void k_chunk_write(uint32_t n, const uint64_t* __restrict__ row_chunk
   }
 }
 
-__global__ void k_split_chunks(uint64_t chunks, const uint32_t* __restrict__ chunk_row,
+// Chunk count read on the device (no host round trip during the build).
+__global__ void k_split_chunks(const uint64_t* __restrict__ chunks_dev,
+                               const uint32_t* __restrict__ chunk_row,
                                const uint64_t* __restrict__ row_off, uint32_t* __restrict__ small,
                                uint32_t* __restrict__ big, unsigned int* cnt2) {
+  const uint64_t chunks = *chunks_dev;
   for (uint64_t c0 = uint64_t(blockIdx.x) * blockDim.x; c0 < chunks;
        c0 += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t c = c0 + threadIdx.x;
@@ -345,9 +348,11 @@ __global__ void k_split_chunks(uint64_t chunks, const uint32_t* __restrict__ chu
 
 // Item indices of small chunks (each small row is one chunk of <= kSmallRow
 // items): warp per 32 chunks, warp-aggregated append keeps rows contiguous.
-__global__ void k_small_items(uint32_t nsmall, const uint32_t* __restrict__ small,
+__global__ void k_small_items(const unsigned int* __restrict__ nsmall_dev,
+                              const uint32_t* __restrict__ small,
                               const uint64_t* __restrict__ chunk_beg, uint32_t* __restrict__ out,
                               unsigned long long* cnt) {
+  const uint32_t nsmall = *nsmall_dev;
   const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   for (uint64_t k0 = ((uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 32; k0 < nsmall;
        k0 += nw * 32) {
@@ -2660,18 +2665,20 @@ void launch_chunk_write(uint32_t n, Items& it, const uint64_t* row_chunk64, cuda
   ++g_launches;
 }
 
-void launch_split_chunks(Items& it, unsigned int* cnt2, cudaStream_t s) {
-  if (!it.chunks) return;
-  k_split_chunks<<<grid_for(it.chunks), kThreads, 0, s>>>(it.chunks, it.chunk_row, it.row_off,
+void launch_split_chunks(Items& it, const uint64_t* chunks_dev, uint64_t chunks_cap,
+                         unsigned int* cnt2, cudaStream_t s) {
+  if (!chunks_cap) return;
+  k_split_chunks<<<grid_for(chunks_cap), kThreads, 0, s>>>(chunks_dev, it.chunk_row, it.row_off,
                                                            it.small, it.big, cnt2);
   DFS_CUDA(cudaGetLastError());
   ++g_launches;
 }
 
-void launch_small_items(Items& it, unsigned long long* cnt, cudaStream_t s) {
-  if (!it.nsmall) return;
-  k_small_items<<<grid_for(uint64_t(it.nsmall)), kThreads, 0, s>>>(it.nsmall, it.small,
-                                                                   it.chunk_beg, it.small_items, cnt);
+void launch_small_items(Items& it, const unsigned int* nsmall_dev, uint64_t chunks_cap,
+                        unsigned long long* cnt, cudaStream_t s) {
+  if (!chunks_cap) return;
+  k_small_items<<<grid_for(chunks_cap), kThreads, 0, s>>>(nsmall_dev, it.small, it.chunk_beg,
+                                                          it.small_items, cnt);
   DFS_CUDA(cudaGetLastError());
   ++g_launches;
 }

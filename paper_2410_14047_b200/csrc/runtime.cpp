@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <cstdlib>
 #include <numeric>
@@ -161,13 +162,16 @@ void Context::alloc_rank(RankDev& r, uint32_t tau) {
   }
   DFS_CUDA(cudaMemcpyAsync(r.x, xs.data(), r.Jp * 4, cudaMemcpyHostToDevice, stream_));
   DFS_CUDA(cudaMemcpyAsync(r.jkey, jk.data(), r.Jp * 8, cudaMemcpyHostToDevice, stream_));
+  // (cudaMemcpyAsync stages pageable host data before returning: no sync needed)
   launch_xlut(r, stream_);
-  sync();  // host staging vectors go out of scope
 }
 
-// Chunk headers, small/big split and small-item list of one direction
-// (row offsets come from the per-position item offsets `pos`).
-void Context::finish_items(RankDev& r, int dir, const uint64_t* pos) {
+// Chunk headers, small/big split and small-item list of one direction (row
+// offsets come from the per-position item offsets `pos`).  Sized by upper
+// bounds (chunks <= items/kChunk + n) so the host never waits here; the
+// exact counts land in meta[0..2] (chunks, small|big chunk counts, small
+// items) and are read back once per partition by build_items.
+void Context::finish_items(RankDev& r, int dir, const uint64_t* pos, uint64_t* meta) {
   const std::string p = "r" + std::to_string(r.tau) + (dir ? ".rev." : ".fwd.");
   Items& it = dir ? r.rev : r.fwd;
   const uint32_t n = g_.n;
@@ -179,30 +183,20 @@ void Context::finish_items(RankDev& r, int dir, const uint64_t* pos) {
   launch_row_offsets(g_, dir, pos, it, row_cnt, stream_);
   uint64_t* row_chunk64 = as<uint64_t>(arena_.get("tmp.rowchunk", (size_t(n) + 2) * 8));
   scan_u32_u64(row_cnt, row_chunk64, n, stmp, sb, stream_);
-  DFS_CUDA(cudaMemcpyAsync(&it.chunks, row_chunk64 + n, 8, cudaMemcpyDeviceToHost, stream_));
-  sync();
-  if (it.chunks >= (uint64_t(1) << 32)) throw Error(kRuntime, "too many work chunks");
-  it.chunk_row = as<uint32_t>(arena_.get(p + "chunk_row", std::max<uint64_t>(it.chunks, 1) * 4));
-  it.chunk_beg = as<uint64_t>(arena_.get(p + "chunk_beg", (it.chunks + 1) * 8));
+  const uint64_t cap = it.count / kChunk + n + 1;  // >= chunks
+  if (cap >= (uint64_t(1) << 32)) throw Error(kRuntime, "too many work chunks");
+  DFS_CUDA(cudaMemcpyAsync(meta, row_chunk64 + n, 8, cudaMemcpyDeviceToDevice, stream_));
+  it.chunk_row = as<uint32_t>(arena_.get(p + "chunk_row", cap * 4));
+  it.chunk_beg = as<uint64_t>(arena_.get(p + "chunk_beg", (cap + 1) * 8));
   it.row_chunk = as<uint32_t>(arena_.get(p + "row_chunk", (size_t(n) + 1) * 4));
   launch_chunk_write(n, it, row_chunk64, stream_);
-  it.small = as<uint32_t>(arena_.get(p + "small", std::max<uint64_t>(it.chunks, 1) * 4));
-  it.big = as<uint32_t>(arena_.get(p + "big", std::max<uint64_t>(it.chunks, 1) * 4));
+  it.small = as<uint32_t>(arena_.get(p + "small", cap * 4));
+  it.big = as<uint32_t>(arena_.get(p + "big", cap * 4));
   it.small_items = as<uint32_t>(arena_.get(p + "small_items", std::max<uint64_t>(it.count, 1) * 4));
-  unsigned int* c2 = as<unsigned int>(arena_.get("tmp.split", 32));
-  DFS_CUDA(cudaMemsetAsync(c2, 0, 32, stream_));
-  launch_split_chunks(it, c2, stream_);
-  unsigned int hc[2];
-  DFS_CUDA(cudaMemcpyAsync(hc, c2, 8, cudaMemcpyDeviceToHost, stream_));
-  sync();
-  it.nsmall = hc[0];
-  it.nbig = hc[1];
-  unsigned long long* c3 = reinterpret_cast<unsigned long long*>(c2 + 4);
-  launch_small_items(it, c3, stream_);
-  unsigned long long hn = 0;
-  DFS_CUDA(cudaMemcpyAsync(&hn, c3, 8, cudaMemcpyDeviceToHost, stream_));
-  sync();
-  it.nsmall_items = hn;
+  unsigned int* c2 = reinterpret_cast<unsigned int*>(meta + 1);
+  launch_split_chunks(it, meta, cap, c2, stream_);
+  launch_small_items(it, c2, cap, reinterpret_cast<unsigned long long*>(meta + 2), stream_);
+  it.chunks = cap;  // provisional (exact after build_items' readback)
 }
 
 // Sampled items of one partition: forward items by evaluating the sampling
@@ -241,8 +235,20 @@ void Context::build_items(RankDev& r) {
   }
   launch_items_pass(g_, w_, tw_, r, 0, fa, 1, cnt_f, pos_f, f, stream_);
   launch_items_pass(g_, w_, tw_, r, 1, fa, 1, cnt_r, pos_r, rv, stream_);
-  finish_items(r, 0, pos_f);
-  finish_items(r, 1, pos_r);
+  uint64_t* meta = as<uint64_t>(arena_.get("tmp.meta", 8 * 8));
+  DFS_CUDA(cudaMemsetAsync(meta, 0, 8 * 8, stream_));
+  finish_items(r, 0, pos_f, meta);
+  finish_items(r, 1, pos_r, meta + 4);
+  uint64_t hm[8];  // the partition's one metadata readback
+  DFS_CUDA(cudaMemcpyAsync(hm, meta, sizeof hm, cudaMemcpyDeviceToHost, stream_));
+  sync();
+  for (int d = 0; d < 2; ++d) {
+    Items& it = d ? rv : f;
+    it.chunks = hm[4 * d];
+    it.nsmall = uint32_t(hm[4 * d + 1]);
+    it.nbig = uint32_t(hm[4 * d + 1] >> 32);
+    it.nsmall_items = hm[4 * d + 2];
+  }
 }
 
 void Context::reset_rank_state(RankDev& r) {
@@ -260,13 +266,17 @@ void Context::reset_rank_state(RankDev& r) {
   RankCtl c{};
   c.tick = 1;
   DFS_CUDA(cudaMemcpyAsync(r.ctl, &c, sizeof c, cudaMemcpyHostToDevice, stream_));
-  sync();
 }
 
 void Context::prepare(const RunConfig& cfg, const HostGraph* host_w_src, uint32_t part_rank,
                       uint32_t part_world) {
   auto t0 = Clock::now();
+  static const bool ptrace = getenv("DFS_PREP_TRACE") != nullptr;  // diagnostics
+  auto mark = [&](const char* what) {
+    if (ptrace) fprintf(stderr, "prep %-12s %8.3f ms\n", what, since(t0) * 1e3);
+  };
   plan_weights(cfg, host_w_src);
+  mark("plan_weights");
   // ---- per-rank state and sampled items (fasst.cpp:50-88, build phase)
   if (part_world && (part_world != cfg.mu || part_rank >= part_world))
     throw Error(kInvalid, "partition rank/world must match devices");
@@ -276,7 +286,9 @@ void Context::prepare(const RunConfig& cfg, const HostGraph* host_w_src, uint32_
   for (uint32_t t = 0; t < count; ++t) {
     RankDev& r = ranks_[t];
     alloc_rank(r, first + t);
+    mark("alloc_rank");
     build_items(r);
+    mark("build_items");
     const std::string p = "r" + std::to_string(first + t) + ".q.";
     const uint64_t cap = std::max<uint64_t>(std::max(r.fwd.chunks, r.rev.chunks), 1);
     for (int gi = 0; gi < kGens; ++gi) {
@@ -285,17 +297,22 @@ void Context::prepare(const RunConfig& cfg, const HostGraph* host_w_src, uint32_
                                              std::max<uint32_t>(g_.n, 1) * 4));
     }
     reset_rank_state(r);
+    mark("reset");
   }
   // Cached first fill per partition (rebuild fills become a copy), only while
   // HBM allows once every partition's working set is allocated.
   for (RankDev& r : ranks_) {
     const size_t bytes = std::max<size_t>(r.n, 1) * r.Jp;
     const std::string name = "r" + std::to_string(r.tau) + ".pristine";
-    size_t fr = 0, tot = 0;
-    DFS_CUDA(cudaMemGetInfo(&fr, &tot));
-    if (arena_.has(name, bytes) || fr > bytes + (size_t(4) << 30))
-      r.pristine = as<int8_t>(arena_.get(name, bytes));
+    bool take = arena_.has(name, bytes);
+    if (!take) {  // cudaMemGetInfo waits behind queued work: only on first use
+      size_t fr = 0, tot = 0;
+      DFS_CUDA(cudaMemGetInfo(&fr, &tot));
+      take = fr > bytes + (size_t(4) << 30);
+    }
+    if (take) r.pristine = as<int8_t>(arena_.get(name, bytes));
   }
+  mark("pristine");
   prep_seconds_ = since(t0);
 }
 
