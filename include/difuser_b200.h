@@ -188,7 +188,7 @@ int dfs_fasst_stats(dfs_ctx *ctx, const dfs_graph *g, const dfs_config *cfg,
  * concurrently; each returns the same report (= reference run with
  * devices = world).  A rank that never arrives makes the others fail with
  * DFS_ERUNTIME after 120 s instead of hanging. */
-#define DFS_PEER_HANDLE_BYTES 152
+#define DFS_PEER_HANDLE_BYTES 216
 int dfs_peer_export(dfs_ctx *ctx, void *handle_out /* DFS_PEER_HANDLE_BYTES */);
 int dfs_peer_open(dfs_ctx *ctx, uint32_t rank, uint32_t world,
                   const void *handles /* world * DFS_PEER_HANDLE_BYTES, rank order */);

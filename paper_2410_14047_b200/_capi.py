@@ -27,7 +27,7 @@ SYMBOLS = [
     "dfs_peer_link", "dfs_peer_run_json", "dfs_fasst_stats", "dfs_mc_influence",
 ]
 
-PEER_HANDLE_BYTES = 152  # DFS_PEER_HANDLE_BYTES
+PEER_HANDLE_BYTES = 216  # DFS_PEER_HANDLE_BYTES
 
 
 class Config(C.Structure):

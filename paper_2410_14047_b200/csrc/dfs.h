@@ -185,13 +185,17 @@ struct alignas(128) PeerBox {
   unsigned int best_v;         // its id (0xFFFFFFFF: none)
   unsigned int minu;           // smallest uncommitted id of the slice (0xFFFFFFFF: none)
   unsigned long long timeouts; // barriers abandoned after the deadline (peer died)
-  unsigned long long pad[11];
+  unsigned int ndirty;         // rows this rank rescored this round (kAllDirty: all)
+  unsigned int pad0;
+  unsigned long long pad[10];
 };
+constexpr unsigned int kAllDirty = 0xFFFFFFFFu;
 
 struct PeerView {
   uint32_t world = 0, rank = 0;
   PeerBox* box[kMaxPeers] = {};          // box[t]: rank t's mailbox (own one for t == rank)
   const double* scores[kMaxPeers] = {};  // rank t's partial score vector (n doubles)
+  const uint32_t* dirty[kMaxPeers] = {}; // rank t's rescored rows of the round
 };
 
 // ---------------------------------------------------------------- launchers

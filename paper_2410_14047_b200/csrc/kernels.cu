@@ -1682,11 +1682,13 @@ __device__ __forceinline__ void argmax_finish(uint32_t nblk, const RunArrays& ra
 
 // Argmax cache: best of segment `seg` (one warp; ascending ids per lane, then
 // best_of = strict > from 0.0 with ties to the smaller id, runtime.cpp:95-119).
+// Rows [base + seg*kSeg, min(n, ...)) (base: the peer slice start, else 0).
 __device__ __forceinline__ void seg_recompute(const double* __restrict__ scores, uint32_t n,
-                                              uint32_t seg, const RunArrays& ra) {
+                                              uint32_t seg, const RunArrays& ra,
+                                              uint32_t base = 0) {
   const unsigned lane = lane_id();
   Best b{0.0, 0xFFFFFFFFu, 0xFFFFFFFFu};
-  const uint32_t lo = seg * kSeg, hi = min(n, lo + kSeg);
+  const uint32_t lo = base + seg * kSeg, hi = min(n, lo + kSeg);
   for (uint32_t v0 = lo + lane; v0 < hi; v0 += 256) {
     double sc[8];
     uint32_t cm[8];
@@ -1721,9 +1723,9 @@ __device__ __forceinline__ void seg_recompute(const double* __restrict__ scores,
 }
 
 // Block-wide best over the segment cache; valid in thread 0.
-__device__ __forceinline__ Best seg_combine(const RunArrays& ra, Best* sb) {
+__device__ __forceinline__ Best seg_combine(const RunArrays& ra, Best* sb, uint32_t nseg) {
   Best t{0.0, 0xFFFFFFFFu, 0xFFFFFFFFu};
-  for (uint32_t k = threadIdx.x; k < ra.nseg; k += blockDim.x)
+  for (uint32_t k = threadIdx.x; k < nseg; k += blockDim.x)
     t = best_of(t, Best{__ldcg(ra.seg_score + k), __ldcg(ra.seg_arg + k), __ldcg(ra.seg_min + k)});
   for (int o = 16; o; o >>= 1) {
     Best x{__shfl_xor_sync(0xffffffffu, t.s, o), __shfl_xor_sync(0xffffffffu, t.v, o),
@@ -2293,6 +2295,7 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
   const uint32_t pslice = a.peer ? (a.n + a.pv.world - 1) / a.pv.world : 0;
   const uint32_t plo = a.peer ? min(a.n, a.pv.rank * pslice) : 0;
   const uint32_t phi = a.peer ? min(a.n, plo + pslice) : 0;
+  const uint32_t pnseg = (phi - plo + kSeg - 1) / kSeg;  // slice segments (peer mode)
   const bool tr = (a.dbg & 4) && blockIdx.x == 0 && threadIdx.x == 0;  // DFS_DBG bit 2
   for (uint32_t step = 0; step < a.k; ++step) {
     if (tr) trace(4, step, 0);
@@ -2329,7 +2332,7 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
             }
             __syncthreads();
           }
-          const Best t = seg_combine(a.ra, sb);
+          const Best t = seg_combine(a.ra, sb, a.ra.nseg);
           if (threadIdx.x == 0) commit_choice(t, a.ra);
           __syncthreads();
           if (tr) trace(7, step, ld_volatile(&a.ra.ctl->choice));
@@ -2366,7 +2369,7 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
         }
         grid.sync();
         if (blockIdx.x == 0) {
-          const Best t = seg_combine(a.ra, sb);
+          const Best t = seg_combine(a.ra, sb, a.ra.nseg);
           if (threadIdx.x == 0) commit_choice(t, a.ra);
           __syncthreads();
         }
@@ -2383,17 +2386,54 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
       grid.sync();
       if (tr) trace(5, step, ld_volatile(&a.ranks[0].ctl->dirty_count));
     }
-    if (!segs) rebuilt = false;
+    if (!segs && !a.peer) rebuilt = false;
     if (segs) {
     } else if (a.peer) {
-      // reduce_to_root + root argmax + broadcast (runtime.cpp:88-121) as: all
-      // partial scores final -> slice sum in binomial order + slice argmax ->
-      // publish (score, id, min-uncommitted) -> every rank picks the winner.
+      // reduce_to_root + root argmax + broadcast (runtime.cpp:88-121) as: every
+      // rank publishes which rows it rescored -> barrier -> each rank re-sums
+      // (binomial order, straight from the peers' partial vectors) only the
+      // rows of ITS id slice that some rank rescored, refreshes the slice's
+      // segment cache and publishes its best -> barrier -> every rank picks
+      // the same winner.  After a rebuild every row counts as rescored.
+      if (blockIdx.x == 0 && threadIdx.x == 0)
+        a.pv.box[a.pv.rank]->ndirty =
+            rebuilt ? kAllDirty : ld_volatile(&a.ranks[0].ctl->dirty_count);
       peer_sync(a.pv, ++ep);
-      argmax_partial_range(plo, phi, [&](uint32_t v) { return peer_reduced(a.pv, v); }, a.ra, sb);
+      const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+      const uint64_t gthreads = uint64_t(gridDim.x) * blockDim.x;
+      const uint64_t gw = gtid >> 5, nw = gthreads >> 5;
+      if (rebuilt) {  // rebuilds are decided identically on every rank
+        for (uint64_t v = plo + gtid; v < phi; v += gthreads) a.reduced[v] = peer_reduced(a.pv, uint32_t(v));
+        grid.sync();
+        for (uint64_t sg = gw; sg < pnseg; sg += nw) seg_recompute(a.reduced, phi, uint32_t(sg), a.ra, plo);
+      } else {
+        for (uint32_t q = 0; q < a.pv.world; ++q) {
+          const uint32_t c = ld_relaxed_sys(&a.pv.box[q]->ndirty);
+          const uint32_t* dq = a.pv.dirty[q];
+          for (uint64_t i = gtid; i < c; i += gthreads) {
+            const uint32_t v = __ldcg(dq + i);
+            if (v >= plo && v < phi) a.reduced[v] = peer_reduced(a.pv, v);
+          }
+        }
+        grid.sync();
+        const uint32_t stampv = step + 1;
+        for (uint32_t q = 0; q < a.pv.world; ++q) {
+          const uint32_t c = ld_relaxed_sys(&a.pv.box[q]->ndirty);
+          const uint32_t* dq = a.pv.dirty[q];
+          for (uint64_t i = gw; i < c; i += nw) {
+            const uint32_t v = __ldcg(dq + i);
+            if (v < plo || v >= phi) continue;  // warp-uniform
+            const uint32_t sg = (v - plo) / kSeg;
+            unsigned prev = 0;
+            if (lane_id() == 0) prev = atomicExch(&a.ra.seg_stamp[sg], stampv);
+            prev = __shfl_sync(0xffffffffu, prev, 0);
+            if (prev != stampv) seg_recompute(a.reduced, phi, sg, a.ra, plo);
+          }
+        }
+      }
       grid.sync();
       if (blockIdx.x == 0) {
-        const Best t = argmax_combine(gridDim.x, a.ra, sb);
+        const Best t = seg_combine(a.ra, sb, pnseg);
         if (threadIdx.x == 0) {
           PeerBox* mine = a.pv.box[a.pv.rank];
           mine->best_s = t.s;
@@ -2412,6 +2452,7 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
         commit_choice(t, a.ra);
       }
       grid.sync();
+      rebuilt = false;
     } else {
       if (a.mu > 1) {
         treesum_body(a.parts, a.mu, a.n, a.reduced);

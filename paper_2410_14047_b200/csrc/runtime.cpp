@@ -471,7 +471,8 @@ Report Context::run_impl(const RunConfig& cfg, const HostGraph* host_w_src, bool
   const unsigned long long launches0 = launches();
   if (peer) {
     prepare(cfg, host_w_src, peer_.rank, peer_.world);
-    if (ranks_[0].scores != peer_.view.scores[peer_.rank])
+    if (ranks_[0].scores != peer_.view.scores[peer_.rank] ||
+        ranks_[0].dirty != peer_.view.dirty[peer_.rank])
       throw Error(kRuntime, "peer mode: partition buffers moved since the peer setup; redo it");
   } else {
     prepare(cfg, host_w_src);
@@ -510,7 +511,7 @@ Report Context::run_impl(const RunConfig& cfg, const HostGraph* host_w_src, bool
   const double** dparts = as<const double*>(arena_.get("run.parts", nl * sizeof(void*)));
   DFS_CUDA(cudaMemcpyAsync(dctl, hctl.data(), nl * sizeof(void*), cudaMemcpyHostToDevice, s));
   DFS_CUDA(cudaMemcpyAsync(dparts, hparts.data(), nl * sizeof(void*), cudaMemcpyHostToDevice, s));
-  if (nl > 1) {
+  if (nl > 1 || peer) {
     ra.reduced = as<double>(arena_.get("run.reduced", std::max<uint32_t>(n, 1) * 8));
     argmax_src = ra.reduced;
   }
@@ -692,7 +693,7 @@ Report Context::run_impl(const RunConfig& cfg, const HostGraph* host_w_src, bool
 // collectives.cpp:44-64) become directly addressable by every other rank.
 namespace {
 struct PeerHandle {
-  cudaIpcMemHandle_t box, scores;
+  cudaIpcMemHandle_t box, scores, dirty;
   unsigned char uuid[16];
   int64_t pid;
 };
@@ -733,6 +734,7 @@ void Context::peer_export(void* out) {
   PeerHandle h{};
   DFS_CUDA(cudaIpcGetMemHandle(&h.box, box));
   DFS_CUDA(cudaIpcGetMemHandle(&h.scores, ranks_[0].scores));
+  DFS_CUDA(cudaIpcGetMemHandle(&h.dirty, ranks_[0].dirty));
   device_uuid(device_, h.uuid);
   h.pid = int64_t(getpid());
   std::memset(out, 0, kPeerHandleBytes);
@@ -761,6 +763,7 @@ void Context::peer_open(uint32_t rank, uint32_t world, const void* handles) {
     if (t == rank) {
       ps.view.box[t] = ps.box;
       ps.view.scores[t] = ranks_[0].scores;
+      ps.view.dirty[t] = ranks_[0].dirty;
       continue;
     }
     if (h.pid == int64_t(getpid()))
@@ -771,8 +774,12 @@ void Context::peer_open(uint32_t rank, uint32_t world, const void* handles) {
     ps.opened.push_back(pb);
     DFS_CUDA(cudaIpcOpenMemHandle(&psc, h.scores, cudaIpcMemLazyEnablePeerAccess));
     ps.opened.push_back(psc);
+    void* pd = nullptr;
+    DFS_CUDA(cudaIpcOpenMemHandle(&pd, h.dirty, cudaIpcMemLazyEnablePeerAccess));
+    ps.opened.push_back(pd);
     ps.view.box[t] = static_cast<PeerBox*>(pb);
     ps.view.scores[t] = static_cast<const double*>(psc);
+    ps.view.dirty[t] = static_cast<const uint32_t*>(pd);
   }
   if (ps.grid_share < 1) ps.grid_share = 1;
   peer_ = std::move(ps);
@@ -818,6 +825,7 @@ void Context::peer_link(const std::vector<Context*>& ctxs) {
       }
       ps.view.box[t] = o->peer_box();
       ps.view.scores[t] = o->ranks_[0].scores;
+      ps.view.dirty[t] = o->ranks_[0].dirty;
     }
     c->peer_ = std::move(ps);
   }

@@ -91,9 +91,9 @@ struct PeerState {
   std::vector<void*> opened;  // IPC mappings (closed on re-setup / destruction)
   unsigned long long timeouts_seen = 0;
 };
-// Exported handle: IPC handles of the mailbox and the partial-score vector,
-// the device UUID and the process id.
-constexpr size_t kPeerHandleBytes = 2 * 64 + 16 + 8;
+// Exported handle: IPC handles of the mailbox, the partial-score vector and
+// the dirty-row list, the device UUID and the process id.
+constexpr size_t kPeerHandleBytes = 3 * 64 + 16 + 8;
 
 class Context {
  public:

@@ -100,3 +100,19 @@ def test_peer_setup_errors():
     cy.prepare_partition(g, 1, 2, k=2, r=64)
     with pytest.raises(ValueError):  # same process + same device: one process per rank
         D.peer_link([cx, cy])
+
+
+def test_peer_processes_many_segments_and_rounds():
+    """Slices spanning many argmax-cache segments, rebuilds and 30 rounds at
+    world 3 (uneven slices)."""
+    world = 3
+    sp, cfg = ("rmat", 14, 150000, 4), dict(k=30, r=96, weights="const:0.05", seed=9)
+    out = _spawn(world, [(sp, cfg, 1, True)])
+    import paper_2410_14047_b200 as D
+    import peer_worker
+    g = peer_worker.make_graph(D, sp)
+    want = O.run(O.CSR(g.offsets, g.adj, np.array(g.orig_ids, np.uint64)), devices=world, **cfg)
+    for r in range(world):
+        rep = json.loads(out[r][0][0])
+        for key, val in want.items():
+            assert rep[key] == val, (key, r)
