@@ -2289,7 +2289,6 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
   };
   rebuild();
   bool rebuilt = true;
-  const double* argsrc = a.mu > 1 ? a.reduced : a.ranks[0].scores;
   // peer mode: this rank reduces and searches the id slice [plo, phi)
   unsigned long long ep = a.peer ? ld_volatile(&a.pv.box[a.pv.rank]->arrive) : 0;
   const uint32_t pslice = a.peer ? (a.n + a.pv.world - 1) / a.pv.world : 0;
@@ -2377,7 +2376,7 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
       rebuilt = false;
       // the cascade's commit (block 0, warp 0) reads the choice; the other
       // blocks wait on its release word, so no grid barrier is needed here
-    } else if (!rebuilt) {  // rows dirtied by the last cascade
+    } else if (!rebuilt) {  // peer mode: rows dirtied by the last cascade
       for (uint32_t t = 0; t < a.mu; ++t) {
         load_rank(t);
         score_body(s_r.regs, s_r.n, s_r.J, s_r.Jp, a.K, 0, s_r.dirty, s_r.ctl, s_r.scores,
@@ -2386,9 +2385,7 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
       grid.sync();
       if (tr) trace(5, step, ld_volatile(&a.ranks[0].ctl->dirty_count));
     }
-    if (!segs && !a.peer) rebuilt = false;
-    if (segs) {
-    } else if (a.peer) {
+    if (a.peer) {
       // reduce_to_root + root argmax + broadcast (runtime.cpp:88-121) as: every
       // rank publishes which rows it rescored -> barrier -> each rank re-sums
       // (binomial order, straight from the peers' partial vectors) only the
@@ -2453,17 +2450,6 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
       }
       grid.sync();
       rebuilt = false;
-    } else {
-      if (a.mu > 1) {
-        treesum_body(a.parts, a.mu, a.n, a.reduced);
-        grid.sync();
-      }
-      argmax_partial(argsrc, a.n, a.ra, sb);
-      grid.sync();
-      if (tr) trace(6, step, 0);
-      if (blockIdx.x == 0) argmax_finish(gridDim.x, a.ra, sb);
-      grid.sync();
-      if (tr) trace(7, step, ld_volatile(&a.ra.ctl->choice));
     }
     phase(2);
     for (uint32_t t = 0; t < a.mu; ++t) {
