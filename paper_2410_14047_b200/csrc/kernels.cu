@@ -1115,12 +1115,21 @@ __device__ __forceinline__ uint32_t simulate_body(const RankDev& r, const SimOpt
         for (int q = 0; q < 4; ++q) {
           if (!mq[q]) continue;
           const uint32_t b = bq[q];
-          acc_max(&acc[b * 4 + w0[q]], s0[q], (mq[q] >> (8 * w0[q])) & 0xFFu);
           const unsigned long long* sp =
               reinterpret_cast<const unsigned long long*>(srcm + uint64_t(vq[q]) * Jp + b * 32);
-          for (int wv = w0[q] + 1; wv < 4; ++wv) {
-            const uint32_t m8 = (mq[q] >> (8 * wv)) & 0xFFu;
-            if (m8) acc_max(&acc[b * 4 + wv], __ldcg(sp + wv), m8);
+          // the item's further live words are loaded together (one round trip)
+          unsigned long long sx[3];
+#pragma unroll
+          for (int t = 0; t < 3; ++t) {
+            const int wv = w0[q] + 1 + t;
+            sx[t] = (wv < 4 && ((mq[q] >> (8 * wv)) & 0xFFu)) ? __ldcg(sp + wv) : 0;
+          }
+          acc_max(&acc[b * 4 + w0[q]], s0[q], (mq[q] >> (8 * w0[q])) & 0xFFu);
+#pragma unroll
+          for (int t = 0; t < 3; ++t) {
+            const int wv = w0[q] + 1 + t;
+            const uint32_t m8 = wv < 4 ? (mq[q] >> (8 * wv)) & 0xFFu : 0u;
+            if (m8) acc_max(&acc[b * 4 + wv], sx[t], m8);
           }
           atomicOr(&touched[b >> 5], 1u << (b & 31));
           upd += __popc(mq[q]);
