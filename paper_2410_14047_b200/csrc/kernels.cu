@@ -973,16 +973,27 @@ __device__ __forceinline__ void sim_pair(uint32_t ua, uint32_t mka, uint32_t bba
   }
   ca = pa && cas_merge(dpa + wa, d0, s0, (mka >> (8 * wa)) & 0xFFu);
   cb = pb && cas_merge(dpb + wb, d1, s1, (mkb >> (8 * wb)) & 0xFFu);
-  if (pa)
-    for (int w = wa + 1; w < 4; ++w) {
-      const uint32_t m8 = (mka >> (8 * w)) & 0xFFu;
-      if (m8) ca |= cas_merge(dpa + w, __ldcg(dpa + w), __ldcg(spa + w), m8);
+  // further live words of each item: all its loads issued together
+  auto rest = [](unsigned long long* dp, const unsigned long long* sp, uint32_t mk, int w0) {
+    unsigned long long sx[3], dx[3];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      const int w = w0 + 1 + t;
+      const bool live = w < 4 && ((mk >> (8 * w)) & 0xFFu);
+      sx[t] = live ? __ldcg(sp + w) : 0;
+      dx[t] = live ? __ldcg(dp + w) : 0;
     }
-  if (pb)
-    for (int w = wb + 1; w < 4; ++w) {
-      const uint32_t m8 = (mkb >> (8 * w)) & 0xFFu;
-      if (m8) cb |= cas_merge(dpb + w, __ldcg(dpb + w), __ldcg(spb + w), m8);
+    bool ch = false;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      const int w = w0 + 1 + t;
+      const uint32_t m8 = w < 4 ? (mk >> (8 * w)) & 0xFFu : 0u;
+      if (m8) ch |= cas_merge(dp + w, dx[t], sx[t], m8);
     }
+    return ch;
+  };
+  if (pa && (uint64_t(mka) >> (8 * (wa + 1)))) ca |= rest(dpa, spa, mka, wa);
+  if (pb && (uint64_t(mkb) >> (8 * (wb + 1)))) cb |= rest(dpb, spb, mkb, wb);
 }
 
 struct SimArgs {
