@@ -32,8 +32,9 @@ class Graph:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value and _capi._lib is not None:
-            _capi._lib.dfs_graph_free(h)
+        capi = globals().get("_capi")  # None while the interpreter tears modules down
+        if h is not None and h.value and capi is not None and capi._lib is not None:
+            capi._lib.dfs_graph_free(h)
             self._h = None
 
     @property
@@ -167,8 +168,9 @@ class Context:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value and _capi._lib is not None:
-            _capi._lib.dfs_ctx_destroy(h)
+        capi = globals().get("_capi")  # None while the interpreter tears modules down
+        if h is not None and h.value and capi is not None and capi._lib is not None:
+            capi._lib.dfs_ctx_destroy(h)
             self._h = None
 
     # ---- hot path
