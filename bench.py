@@ -376,6 +376,20 @@ def run_ours(args, rank, world, local_rank):
                 ts3.append(e0.elapsed_time(e1) / 1e3)
         north = {"workload": desc3, "n": g3.n, "m": g3.m, "seconds": round(statistics.mean(ts3), 5),
                  "runs": len(ts3), "n_gpus": 1, "target_seconds_8gpu": 1.0}
+        # BASELINE configs[2] (same graph, weighted cascade: ~37 convergences)
+        _, _, _, w4, r4, k4, desc4 = CONFIGS["c3"]
+        flush.add_(1)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rep4 = json.loads(ctx.run_json(None, k=k4, r=r4, devices=1, weights=w4, seed=SEED,
+                                       timings=False, resident=True))
+        e1.record(stream)
+        e1.synchronize()
+        north["c3_weighted_cascade"] = {"workload": desc4,
+                                        "seconds": round(e0.elapsed_time(e1) / 1e3, 4),
+                                        "rebuilds": rep4["rebuilds"], "runs": 1}
         del g3
 
     cpu = None
