@@ -75,6 +75,7 @@ struct Items {
   // flat list of the item indices of small rows (flat full passes)
   uint32_t* small_items = nullptr;
   uint64_t nsmall_items = 0;
+  uint64_t live = 0;  // live (item, simulation) pairs (host copy; fwd only)
 };
 constexpr uint32_t kSmallRow = 32;
 
@@ -277,6 +278,9 @@ void launch_run(const RankDev* ranks_dev, uint32_t mu, uint32_t k, uint32_t R, u
                 double eps, int cap, int jacobi, int count, int K, RunArrays& ra,
                 const double* const* parts, RankCtl* const* ctls, double* reduced,
                 unsigned long long* phase_ns, const PeerView* peer, int grid_share,
-                cudaStream_t s);
+                int sim_pull_f, int cas_pull_f, cudaStream_t s);
+// *out += live (item, simulation) pairs of `count` masks.
+void launch_popc_sum(const uint32_t* mask, uint64_t count, unsigned long long* out,
+                     cudaStream_t s);
 
 }  // namespace dfs

@@ -2666,6 +2666,26 @@ void launch_mc_influence(const DevGraph& g, const uint32_t* w, uint64_t base, ui
   ++g_launches;
 }
 
+// Live (item, simulation) pairs of a direction: the density that decides how
+// early sweeps / cascade levels switch to pull.
+__global__ void k_popc_sum(const uint32_t* __restrict__ mask, uint64_t count,
+                           unsigned long long* out) {
+  unsigned long long c = 0;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    c += __popc(mask[i]);
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane_id() == 0 && c) atomicAdd(out, c);
+}
+
+void launch_popc_sum(const uint32_t* mask, uint64_t count, unsigned long long* out,
+                     cudaStream_t s) {
+  if (!count) return;
+  k_popc_sum<<<grid_for(count), kThreads, 0, s>>>(mask, count, out);
+  DFS_CUDA(cudaGetLastError());
+  ++g_launches;
+}
+
 void launch_xlut_of(const uint32_t* x, uint32_t J, uint32_t* lut, cudaStream_t s) {
   k_xlut<<<(((1u << kLutBits) + 1) + kThreads - 1) / kThreads, kThreads, 0, s>>>(x, J, lut);
   DFS_CUDA(cudaGetLastError());
@@ -2839,10 +2859,12 @@ void launch_run(const RankDev* ranks_dev, uint32_t mu, uint32_t k, uint32_t R, u
                 double eps, int cap, int jacobi, int count, int K, RunArrays& ra,
                 const double* const* parts, RankCtl* const* ctls, double* reduced,
                 unsigned long long* phase_ns, const PeerView* peer, int grid_share,
-                cudaStream_t s) {
+                int sim_pull_f, int cas_pull_f, cudaStream_t s) {
   static const int dbg = getenv("DFS_DBG") ? atoi(getenv("DFS_DBG")) : 0;
-  static const int spf = getenv("DFS_SIM_PULL") ? atoi(getenv("DFS_SIM_PULL")) : 4;
-  static const int cpf = getenv("DFS_CAS_PULL") ? atoi(getenv("DFS_CAS_PULL")) : 8;
+  static const int spf_env = getenv("DFS_SIM_PULL") ? atoi(getenv("DFS_SIM_PULL")) : 0;
+  static const int cpf_env = getenv("DFS_CAS_PULL") ? atoi(getenv("DFS_CAS_PULL")) : 0;
+  const int spf = spf_env > 0 ? spf_env : sim_pull_f;
+  const int cpf = cpf_env > 0 ? cpf_env : cas_pull_f;
   RunArgs a{ranks_dev, mu, k, R, n, eps, cap, dbg, spf, cpf, K, ra, parts, ctls, reduced, phase_ns,
             peer ? 1 : 0, peer ? *peer : PeerView{}};
   void* args[] = {&a};

@@ -239,6 +239,7 @@ void Context::build_items(RankDev& r) {
   DFS_CUDA(cudaMemsetAsync(meta, 0, 8 * 8, stream_));
   finish_items(r, 0, pos_f, meta);
   finish_items(r, 1, pos_r, meta + 4);
+  launch_popc_sum(f.mask, f.count, reinterpret_cast<unsigned long long*>(meta + 3), stream_);
   uint64_t hm[8];  // the partition's one metadata readback
   DFS_CUDA(cudaMemcpyAsync(hm, meta, sizeof hm, cudaMemcpyDeviceToHost, stream_));
   sync();
@@ -249,6 +250,7 @@ void Context::build_items(RankDev& r) {
     it.nbig = uint32_t(hm[4 * d + 1] >> 32);
     it.nsmall_items = hm[4 * d + 2];
   }
+  f.live = hm[3];
 }
 
 void Context::reset_rank_state(RankDev& r) {
@@ -538,6 +540,13 @@ Report Context::run_impl(const RunConfig& cfg, const HostGraph* host_w_src, bool
 
   // Default: the whole loop as one persistent kernel (launch_run).
   // DFS_RUN_MODE=launches selects the per-phase launch sequence (same results).
+  // When sweeps / cascade levels switch to pull (frontier chunks * f > all
+  // chunks): dense items (many live simulations each, e.g. weighted cascade)
+  // make full pull passes pay off earlier (A/B: C3 simulate -19%, cascade
+  // -21%; sparse IC items keep the later switch).  DFS_SIM_PULL /
+  // DFS_CAS_PULL override.
+  const double density = ranks_[0].fwd.count ? double(ranks_[0].fwd.live) / ranks_[0].fwd.count : 0;
+  const int pull_sim = density >= 6.0 ? 2 : 4, pull_cas = density >= 6.0 ? 4 : 8;
   static const bool multi_env =
       getenv("DFS_RUN_MODE") && std::string(getenv("DFS_RUN_MODE")) == "launches";
   const bool multi = multi_env && !peer;  // peer mode exchanges inside k_run only
@@ -555,7 +564,7 @@ Report Context::run_impl(const RunConfig& cfg, const HostGraph* host_w_src, bool
     krun0 = mark();
     launch_run(dranks, nl, k, cfg.r, n, cfg.rebuild_eps, cfg.sim_cap, cfg.jacobi, cfg.count, 53 - lj,
                ra, dparts, dctl, ra.reduced, phase_ns, peer ? &peer_.view : nullptr,
-               peer ? peer_.grid_share : 1, s);
+               peer ? peer_.grid_share : 1, pull_sim, pull_cas, s);
   } else {
     size_t e0 = mark();
     for (uint32_t t = 0; t < nl; ++t) launch_fill(ranks_[t], nullptr, 0, s);
