@@ -70,6 +70,7 @@ typedef struct dfs_stats {
    * device-graph out-edges, cascades started */
   uint64_t cnt_cas_rows, cnt_cas_edges, cnt_cascades;
   double run_kernel; /* seconds of the whole-loop kernel launch (CUDA events) */
+  double item_density; /* live simulations per sampled item (sets the pull switch points) */
 } dfs_stats;
 
 const char *dfs_last_error(void);

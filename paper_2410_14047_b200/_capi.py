@@ -46,7 +46,8 @@ class Stats(C.Structure):
                                           "cnt_convergences", "launches")] + \
                [("sim_active", C.c_double), ("sim_launches", C.c_uint32), ("n", C.c_uint32),
                 ("m", C.c_uint64), ("cnt_cas_rows", C.c_uint64), ("cnt_cas_edges", C.c_uint64),
-                ("cnt_cascades", C.c_uint64), ("run_kernel", C.c_double)]
+                ("cnt_cascades", C.c_uint64), ("run_kernel", C.c_double),
+                ("item_density", C.c_double)]
 
 
 class ReportFields(C.Structure):

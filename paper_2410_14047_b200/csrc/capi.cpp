@@ -277,6 +277,7 @@ int dfs_last_stats(const dfs_ctx* ctx, dfs_stats* out) {
     out->cnt_cas_edges = r.cnt_cas_edges;
     out->cnt_cascades = r.cnt_cascades;
     out->run_kernel = r.run_kernel;
+    out->item_density = r.item_density;
   });
 }
 

@@ -546,7 +546,8 @@ Report Context::run_impl(const RunConfig& cfg, const HostGraph* host_w_src, bool
   // -21%; sparse IC items keep the later switch).  DFS_SIM_PULL /
   // DFS_CAS_PULL override.
   const double density = ranks_[0].fwd.count ? double(ranks_[0].fwd.live) / ranks_[0].fwd.count : 0;
-  const int pull_sim = density >= 6.0 ? 2 : 4, pull_cas = density >= 6.0 ? 4 : 8;
+  const int pull_sim = density >= 10.0 ? 1 : density >= 6.0 ? 2 : 4;
+  const int pull_cas = density >= 6.0 ? 4 : 8;
   static const bool multi_env =
       getenv("DFS_RUN_MODE") && std::string(getenv("DFS_RUN_MODE")) == "launches";
   const bool multi = multi_env && !peer;  // peer mode exchanges inside k_run only
@@ -690,6 +691,7 @@ Report Context::run_impl(const RunConfig& cfg, const HostGraph* host_w_src, bool
   pt.upload = last_.upload;
   pt.total = since(t_total);
   rep.launches = launches() - launches0;
+  rep.item_density = density;
   rep.timings = pt;
   last_ = pt;
   return rep;

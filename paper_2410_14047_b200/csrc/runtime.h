@@ -72,6 +72,7 @@ struct Report {  // runtime.hpp:29-41
   uint64_t cnt_edges = 0, cnt_batches = 0, cnt_touched = 0, cnt_sweeps = 0, cnt_convergences = 0;
   uint64_t cnt_cas_rows = 0, cnt_cas_edges = 0, cnt_cascades = 0;
   double run_kernel = 0;        // seconds of the k_run launch (CUDA events on the stream)
+  double item_density = 0;      // live simulations per forward item (partition 0)
   uint64_t launches = 0;        // kernels launched by run()
   double sim_active = 0;        // seconds of simulate launches that ran (not gated off)
   uint32_t sim_launches = 0;    // simulate launches that ran
