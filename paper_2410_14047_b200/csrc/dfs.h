@@ -77,7 +77,10 @@ struct Items {
   uint64_t nsmall_items = 0;
   uint64_t live = 0;  // live (item, simulation) pairs (host copy; fwd only)
 };
-constexpr uint32_t kSmallRow = 32;
+#ifndef DFS_SMALL_ROW
+#define DFS_SMALL_ROW 32
+#endif
+constexpr uint32_t kSmallRow = DFS_SMALL_ROW;  // rows with <= kSmallRow items: item-parallel
 
 // Device-resident control block of one rank (sample-space partition tau).
 struct RankCtl {

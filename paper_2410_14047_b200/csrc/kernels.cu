@@ -897,7 +897,10 @@ __device__ __forceinline__ void for_frontier_items(const Items& it, const uint32
 }
 
 constexpr unsigned long long kNeg8 = 0x8080808080808080ull;  // "no contribution"
-constexpr uint32_t kSoloChunks = 16;  // frontier (chunks) a single block iterates alone
+#ifndef DFS_SOLO_CHUNKS
+#define DFS_SOLO_CHUNKS 16
+#endif
+constexpr uint32_t kSoloChunks = DFS_SOLO_CHUNKS;  // frontier (chunks) a single block iterates alone
 constexpr uint32_t kSoloDirty = 512;  // dirty rows block 0 rescores alone
 constexpr uint32_t kPullMaxJp = 4096;  // pull accumulators live in shared memory
 
