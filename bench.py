@@ -314,6 +314,17 @@ def run_ours(args, rank, world, local_rank):
     h2d = 8 * (g.n + 1) + 4 * g.m
     d2h = 64 + 12 * k + 4 * k + devices * 256
 
+    # multi-GPU: sketch-edge updates (live (item, simulation) merges actually
+    # performed) summed over the ranks per second of the slowest simulate phase
+    upd_multi = None
+    if dist:
+        dev = "cpu" if args.share_gpu else f"cuda:{local_rank}"
+        u = torch.tensor([float(stats[-1]["sketch_edge_updates"])], dtype=torch.float64, device=dev)
+        t = torch.tensor([float(stats[-1]["sim_active"])], dtype=torch.float64, device=dev)
+        dist.all_reduce(u, op=dist.ReduceOp.SUM)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        upd_multi = float(u.item()) / max(float(t.item()), 1e-12)
+
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -353,6 +364,8 @@ def run_ours(args, rank, world, local_rank):
                     "units": {x: alg[x] for x in ("E", "B", "T", "S", "L", "convergences",
                                                   "cascade_rows", "cascade_edges", "cascades")}}
         upd_per_s = alg["L"] / max(sim_active, 1e-12)
+    elif upd_multi is not None:
+        upd_per_s = upd_multi
 
     # North-star workload (BASELINE.json north_star): R-MAT scale 23 (100M
     # edges), IC p=0.01, R=1024, K=50 — end-to-end seconds with the graph resident.
