@@ -222,7 +222,7 @@ void launch_items_pass(const DevGraph& g, const uint32_t* w, const uint32_t* tw,
 // Weights in transposed order (kind 0 const, 1 wc, 2 gather of w).
 void launch_tweights(const DevGraph& g, int kind, uint32_t W, const uint32_t* w, uint32_t* tw,
                      cudaStream_t s);
-// Reverse items from forward items (no sampling recomputation).
+// Slot LUT of a partition (first slot with x >= k << 19, FASST windows).
 void launch_xlut(const RankDev& r, cudaStream_t s);
 void launch_xlut_of(const uint32_t* x, uint32_t J, uint32_t* lut, cudaStream_t s);
 // Monte-Carlo influence (oracle.cpp:30-79) of batches [batch0, batch0+nbatch)
@@ -237,10 +237,6 @@ void launch_mc_influence(const DevGraph& g, const uint32_t* w, uint64_t base, ui
 void launch_fasst_stats(const DevGraph& g, const uint32_t* w, const uint32_t* x,
                         const uint32_t* xlut, uint32_t R, uint32_t mu, int sorted, int fill,
                         unsigned long long* out, cudaStream_t s);
-void launch_rev_counts(const DevGraph& g, const uint32_t* cnt_f, uint32_t* cnt_r, cudaStream_t s);
-void launch_rev_copy(const DevGraph& g, const uint32_t* cnt_f, const uint32_t* cnt_r,
-                     const uint64_t* pos_f, const uint64_t* pos_r, const Items& f, Items& rv,
-                     cudaStream_t s);
 // row_off[r] = pos_off[graph row start]; then per-row chunk counts.
 void launch_row_offsets(const DevGraph& g, int dir, const uint64_t* pos_off, Items& it,
                         uint32_t* row_cnt, cudaStream_t s);

@@ -214,42 +214,11 @@ __global__ void k_items(uint64_t npos, const uint32_t* __restrict__ p_hash,
   }
 }
 
-// Reverse items are the forward items of each edge re-keyed by target:
-// rev count of transposed position p = fwd count of edge tedge[p].
+// Slot LUT: lut[k] = first slot with x >= k << kLutShift (sorted slices).
 __global__ void k_xlut(const uint32_t* __restrict__ x, uint32_t J, uint32_t* __restrict__ lut) {
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k <= (1u << kLutBits);
        k += gridDim.x * blockDim.x)
     lut[k] = lower_bound_x(x, J, uint64_t(k) << kLutShift);
-}
-
-__global__ void k_gather_cnt(uint64_t m, const uint32_t* __restrict__ tedge,
-                             const uint32_t* __restrict__ cnt_f, uint32_t* __restrict__ cnt_r) {
-  for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < m;
-       p += uint64_t(gridDim.x) * blockDim.x)
-    cnt_r[p] = cnt_f[tedge[p]];
-}
-
-// Output-ordered (coalesced writes): transposed position p holds edge
-// tedge[p]; its forward items are gathered from pos_f[e].
-__global__ void k_rev_copy(uint64_t m, const uint32_t* __restrict__ tedge,
-                           const uint32_t* __restrict__ cnt_r, const uint64_t* __restrict__ pos_f,
-                           const uint64_t* __restrict__ pos_r, const uint32_t* __restrict__ f_row,
-                           const uint32_t* __restrict__ f_other, const uint32_t* __restrict__ f_mask,
-                           const uint8_t* __restrict__ f_batch, uint32_t* __restrict__ r_row,
-                           uint32_t* __restrict__ r_other, uint32_t* __restrict__ r_mask,
-                           uint8_t* __restrict__ r_batch) {
-  for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < m;
-       p += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t c = cnt_r[p];
-    if (!c) continue;
-    const uint64_t src = pos_f[tedge[p]], dst = pos_r[p];
-    for (uint32_t k = 0; k < c; ++k) {
-      r_row[dst + k] = f_other[src + k];   // row of a reverse item: target v
-      r_other[dst + k] = f_row[src + k];   // other: source u
-      r_mask[dst + k] = f_mask[src + k];
-      r_batch[dst + k] = f_batch[src + k];
-    }
-  }
 }
 
 // Transposed position p holds edge tedge[p]; its target is the sort key
@@ -2697,25 +2666,6 @@ void launch_xlut_of(const uint32_t* x, uint32_t J, uint32_t* lut, cudaStream_t s
 
 void launch_xlut(const RankDev& r, cudaStream_t s) {
   k_xlut<<<(((1u << kLutBits) + 1) + kThreads - 1) / kThreads, kThreads, 0, s>>>(r.x, r.J, r.xlut);
-  DFS_CUDA(cudaGetLastError());
-  ++g_launches;
-}
-
-void launch_rev_counts(const DevGraph& g, const uint32_t* cnt_f, uint32_t* cnt_r, cudaStream_t s) {
-  if (!g.m) return;
-  k_gather_cnt<<<grid_for(g.m), kThreads, 0, s>>>(g.m, g.tedge, cnt_f, cnt_r);
-  DFS_CUDA(cudaGetLastError());
-  ++g_launches;
-}
-
-void launch_rev_copy(const DevGraph& g, const uint32_t* cnt_f, const uint32_t* cnt_r_,
-                     const uint64_t* pos_f, const uint64_t* pos_r, const Items& f, Items& rv,
-                     cudaStream_t s) {
-  if (!g.m) return;
-  (void)cnt_f;
-  k_rev_copy<<<grid_for(g.m), kThreads, 0, s>>>(g.m, g.tedge, cnt_r_, pos_f, pos_r, f.row,
-                                                f.other, f.mask, f.batch, rv.row, rv.other,
-                                                rv.mask, rv.batch);
   DFS_CUDA(cudaGetLastError());
   ++g_launches;
 }
