@@ -132,24 +132,48 @@ __device__ __forceinline__ uint32_t lower_bound_x(const uint32_t* sx, uint32_t J
   return a;
 }
 
+__device__ __forceinline__ uint32_t lower_bound_in(const uint32_t* sx, uint32_t a, uint32_t z,
+                                                   uint64_t key) {
+  while (a < z) {
+    const uint32_t mid = (a + z) >> 1;
+    if (uint64_t(sx[mid]) < key) a = mid + 1; else z = mid;
+  }
+  return a;
+}
+
+// Window [lo, hi) plus its all-live half [alo, ahi): inside the block, bit b
+// of x splits the sorted window in two; where it equals bit b of h, x ^ h <
+// 2^b <= W, so every slot of that half samples the edge without a test (the
+// other half still needs (x ^ h) < W).  Naive plans: the whole slice, tested.
 __device__ __forceinline__ void edge_window(const uint32_t* sx, const uint32_t* lut, uint32_t J,
                                             uint32_t h, uint32_t W, int fasst, uint32_t& lo,
-                                            uint32_t& hi) {
+                                            uint32_t& hi, uint32_t& alo, uint32_t& ahi) {
   if (!fasst) {
     lo = 0;
     hi = J;
+    alo = ahi = 0;
     return;
   }
   const int b = 31 - __clz(W);  // W >= 1
-  const uint64_t span = uint64_t(1) << (b + 1);
+  const uint64_t half = uint64_t(1) << b;
+  const uint64_t span = half << 1;
   const uint64_t lx = uint64_t(h) & ~(span - 1);
   const uint64_t hx = lx + span;  // exclusive
+  const uint64_t mx = lx + half;  // first value with bit b set
   if (b + 1 >= kLutShift) {       // block boundaries are LUT bucket boundaries: exact
     lo = lut[lx >> kLutShift];
     hi = (hx >> kLutShift) > (1u << kLutBits) ? J : lut[hx >> kLutShift];
   } else {
     lo = lower_bound_x(sx, J, lx);
     hi = lower_bound_x(sx, J, hx);
+  }
+  const uint32_t mid = b >= kLutShift ? lut[mx >> kLutShift] : lower_bound_in(sx, lo, hi, mx);
+  if ((h >> b) & 1u) {
+    alo = mid;
+    ahi = hi;
+  } else {
+    alo = lo;
+    ahi = mid;
   }
 }
 
@@ -179,23 +203,31 @@ __global__ void k_items(uint64_t npos, const uint32_t* __restrict__ p_hash,
     uint32_t c = 0;
     if (W != 0) {  // fasst.cpp:71 — W = 0 never samples
       const uint32_t h = p_hash[p];
-      uint32_t lo, hi;
-      edge_window(sx, lut, J, h, W, fasst, lo, hi);
+      uint32_t lo, hi, alo, ahi;
+      edge_window(sx, lut, J, h, W, fasst, lo, hi, alo, ahi);
       if (hi > lo) {
         uint64_t o = WRITE ? pos_off[p] : 0;
         const uint32_t other = WRITE ? p_other[p] : 0;
         const uint32_t rowv = WRITE ? p_row[p] : 0;
         for (uint32_t b = lo >> 5; b <= (hi - 1) >> 5; ++b) {
-          // Only slots inside the window can pass the test (DESIGN.md
-          // §window), and any slot outside it fails on its own, so the
-          // window is covered by aligned 4-slot vector loads without masking.
+          const uint32_t bb = b * 32;
+          const uint32_t i0 = max(lo, bb), i1 = min(hi, bb + 32);
+          // all-live half: a contiguous run of bits, no test
+          const uint32_t a0 = max(alo, i0), a1 = min(ahi, i1);
           uint32_t mk = 0;
-          const uint32_t i0 = max(lo, b * 32), i1 = min(hi, b * 32 + 32);
-          for (uint32_t g = i0 & ~3u; g < i1; g += 4) {
-            const uint4 xv = *reinterpret_cast<const uint4*>(sx + g);  // sampling.hpp:37-39
+          if (a1 > a0)
+            mk = (a1 - a0 == 32 ? 0xFFFFFFFFu : ((1u << (a1 - a0)) - 1u)) << (a0 - bb);
+          // the other half (one range, [alo, ahi) being a prefix or suffix of
+          // the window) is tested with aligned 4-slot vector loads; a group's
+          // slots outside the window fail on their own and slots of the live
+          // half pass, so no masking is needed (sampling.hpp:37-39)
+          const uint32_t t0 = alo == lo ? max(i0, ahi) : i0;
+          const uint32_t t1 = alo == lo ? i1 : min(i1, alo);
+          for (uint32_t g = t0 & ~3u; g < t1; g += 4) {
+            const uint4 xv = *reinterpret_cast<const uint4*>(sx + g);
             const uint32_t m4 = uint32_t((xv.x ^ h) < W) | (uint32_t((xv.y ^ h) < W) << 1) |
                                 (uint32_t((xv.z ^ h) < W) << 2) | (uint32_t((xv.w ^ h) < W) << 3);
-            mk |= m4 << (g - b * 32);
+            mk |= m4 << (g - bb);
           }
           if (mk) {
             if (WRITE) {
@@ -377,8 +409,8 @@ __global__ void k_fasst_stats(uint64_t m, const uint32_t* __restrict__ ehash,
       continue;
     }
     const uint32_t h = ehash[e];
-    uint32_t lo = 0, hi = R;
-    if (sorted) edge_window(sx, lut, R, h, W, 1, lo, hi);
+    uint32_t lo = 0, hi = R, alo, ahi;
+    if (sorted) edge_window(sx, lut, R, h, W, 1, lo, hi, alo, ahi);
     unsigned long long hits = 0;  // chunks sampling e (mu <= 64)
     uint32_t bc = 0, cur_b = lo >> 5;
     unsigned long long lanes = 0, batches = 0;
