@@ -200,6 +200,7 @@ struct PeerView {
   PeerBox* box[kMaxPeers] = {};          // box[t]: rank t's mailbox (own one for t == rank)
   const double* scores[kMaxPeers] = {};  // rank t's partial score vector (n doubles)
   const uint32_t* dirty[kMaxPeers] = {}; // rank t's rescored rows of the round
+  unsigned long long timeout_ns = 120ull * 1000 * 1000 * 1000;  // a barrier's patience
 };
 
 // ---------------------------------------------------------------- launchers

@@ -2179,24 +2179,27 @@ template <class T>
 __device__ __forceinline__ T ld_relaxed_sys(const T* p) {
   return *reinterpret_cast<const volatile T*>(p);
 }
-constexpr unsigned long long kPeerTimeoutNs = 120ull * 1000 * 1000 * 1000;
 
 // Cross-GPU barrier of epoch `ep`, called by every thread of the grid: after
 // it, every write any rank made before arriving is visible here.  Lane t of
 // block 0's first warp waits for rank t; a peer that never arrives (dead
-// process) releases the wait after kPeerTimeoutNs and is reported by the host.
+// process) releases the wait after pv.timeout_ns (DFS_PEER_TIMEOUT_S) and is
+// reported by the host; once that happened, later barriers of the launch do
+// not wait any more (the results are discarded anyway).
 __device__ __noinline__ void peer_sync(const PeerView& pv, unsigned long long ep) {
   cg::grid_group grid = cg::this_grid();
   __threadfence_system();
   grid.sync();
   if (blockIdx.x == 0 && threadIdx.x < 32) {
     const unsigned lane = threadIdx.x;
-    if (lane == 0) st_release_sys(&pv.box[pv.rank]->arrive, ep);
-    if (lane < pv.world && lane != pv.rank) {
+    PeerBox* mine = pv.box[pv.rank];
+    if (lane == 0) st_release_sys(&mine->arrive, ep);
+    const bool failed = ld_volatile(&mine->timeouts) != 0;
+    if (!failed && lane < pv.world && lane != pv.rank) {
       const unsigned long long t0 = global_ns();
       while (ld_acquire_sys(&pv.box[lane]->arrive) < ep) {
-        if (global_ns() - t0 > kPeerTimeoutNs) {
-          atomicAdd(&pv.box[pv.rank]->timeouts, 1ull);
+        if (global_ns() - t0 > pv.timeout_ns) {
+          atomicAdd(&mine->timeouts, 1ull);
           break;
         }
         __nanosleep(64);

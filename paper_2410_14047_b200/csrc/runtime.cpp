@@ -717,6 +717,13 @@ void device_uuid(int dev, unsigned char out[16]) {
 }
 }  // namespace
 
+// How long a peer barrier waits for a rank (DFS_PEER_TIMEOUT_S, default 120 s).
+static unsigned long long peer_timeout_ns() {
+  const char* e = getenv("DFS_PEER_TIMEOUT_S");
+  const double sec = e ? atof(e) : 120.0;
+  return static_cast<unsigned long long>((sec > 0 ? sec : 120.0) * 1e9);
+}
+
 PeerBox* Context::peer_box() {
   return as<PeerBox>(arena_.get("peer.box", sizeof(PeerBox)));
 }
@@ -763,6 +770,7 @@ void Context::peer_open(uint32_t rank, uint32_t world, const void* handles) {
   ps.box = peer_box();
   ps.view.world = world;
   ps.view.rank = rank;
+  ps.view.timeout_ns = peer_timeout_ns();
   unsigned char me[16];
   device_uuid(device_, me);
   const auto* hs = static_cast<const unsigned char*>(handles);
@@ -815,6 +823,7 @@ void Context::peer_link(const std::vector<Context*>& ctxs) {
     ps.box = c->peer_box();
     ps.view.world = world;
     ps.view.rank = i;
+    ps.view.timeout_ns = peer_timeout_ns();
     ps.grid_share = 0;
     for (uint32_t t = 0; t < world; ++t) {
       Context* o = ctxs[t];

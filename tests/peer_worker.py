@@ -26,11 +26,23 @@ def worker(rank, world, port, cases, q):
         from paper_2410_14047_b200.dist import PeerRunner
         ctx = D.Context(0)
         out = []
-        for spec, cfg, repeat, resident in cases:
+        for case in cases:
+            spec, cfg, repeat, resident = case[:4]
+            dead = case[4] if len(case) > 4 else None  # rank that sets up but never runs
             g = make_graph(D, spec)
             ctx.upload(g)
             pr = PeerRunner(ctx, g, rank, world)
             kw = {k: v for k, v in cfg.items() if k != "devices"}
+            if dead is not None:
+                pr.setup(**kw)
+                if rank == dead:
+                    out.append(["dead"])
+                    continue
+                try:
+                    out.append([pr.run_json(resident=resident, timings=False, **kw)])
+                except RuntimeError as ex:
+                    out.append(["ERR:" + str(ex)])
+                continue
             reps = [pr.run_json(resident=resident, timings=False, **kw) for _ in range(repeat)]
             out.append(reps)
         q.put((rank, out, None))

@@ -116,3 +116,18 @@ def test_peer_processes_many_segments_and_rounds():
         rep = json.loads(out[r][0][0])
         for key, val in want.items():
             assert rep[key] == val, (key, r)
+
+
+def test_peer_dead_rank_fails_instead_of_hanging():
+    """A rank that never reaches the round barriers (failed process): the
+    survivors' kernels give up after DFS_PEER_TIMEOUT_S and the call raises
+    RuntimeError (SURVEY §5 failure detection) instead of hanging the GPU."""
+    os.environ["DFS_PEER_TIMEOUT_S"] = "3"
+    try:
+        out = _spawn(2, [(("er", 2000, 16000, 5), dict(k=4, r=64, weights="const:0.1", seed=1),
+                          1, True, 1)])
+    finally:
+        del os.environ["DFS_PEER_TIMEOUT_S"]
+    assert out[1][0] == ["dead"]
+    msg = out[0][0][0]
+    assert msg.startswith("ERR:") and "peer" in msg, msg
