@@ -20,10 +20,17 @@
 #include <unistd.h>
 
 #include "hash.cuh"
+#include <nvtx3/nvToolsExt.h>
 
 namespace dfs {
 
 namespace {
+// NVTX range for the host-side phases (upload, build, run, peer setup): they
+// show up in Nsight timelines and can scope ncu (--nvtx --nvtx-include).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 using Clock = std::chrono::steady_clock;
 double since(Clock::time_point t0) {
   return std::chrono::duration<double>(Clock::now() - t0).count();
@@ -96,6 +103,7 @@ Context::~Context() {
 void Context::sync() { DFS_CUDA(cudaStreamSynchronize(stream_)); }
 
 void Context::upload(const HostGraph& hg) {
+  NvtxRange nv("dfs.upload");
   DFS_CUDA(cudaSetDevice(device_));
   auto t0 = Clock::now();
   g_ = DevGraph{};
@@ -272,6 +280,7 @@ void Context::reset_rank_state(RankDev& r) {
 
 void Context::prepare(const RunConfig& cfg, const HostGraph* host_w_src, uint32_t part_rank,
                       uint32_t part_world) {
+  NvtxRange nv("dfs.build");
   auto t0 = Clock::now();
   static const bool ptrace = getenv("DFS_PREP_TRACE") != nullptr;  // diagnostics
   auto mark = [&](const char* what) {
@@ -469,6 +478,7 @@ Report Context::run_peer(const RunConfig& cfg, const HostGraph* host_w_src) {
 }
 
 Report Context::run_impl(const RunConfig& cfg, const HostGraph* host_w_src, bool peer) {
+  NvtxRange nv(peer ? "dfs.run_peer" : "dfs.run");
   auto t_total = Clock::now();
   const unsigned long long launches0 = launches();
   if (peer) {
@@ -760,6 +770,7 @@ void Context::peer_export(void* out) {
 }
 
 void Context::peer_open(uint32_t rank, uint32_t world, const void* handles) {
+  NvtxRange nv("dfs.peer_open");
   DFS_CUDA(cudaSetDevice(device_));
   check_partition(ranks_, cfg_, rank, world);
   for (void* p : peer_.opened) cudaIpcCloseMemHandle(p);
