@@ -322,3 +322,15 @@ def test_mc_influence_gpu_equals_host_rmat(D, ctx):
         ctx.influence(g, [g.n], trials=10)
     with pytest.raises(ValueError):
         ctx.influence(g, [0], trials=0)
+
+
+def test_widest_partition_matches_oracle(D, ctx):
+    """J = 8192 simulations in one partition (byte batch index at its limit;
+    pull paths disabled above 4096, push only) and a 4096-wide one."""
+    g = D.generate("er", 1500, 9000, 13)
+    cg = _oracle_csr(g)
+    for r in (8192, 4096):
+        got = json.loads(ctx.run_json(g, k=3, r=r, weights="const:0.05", seed=2, timings=False))
+        want = O.run(cg, k=3, r=r, devices=1, weights="const:0.05", seed=2)
+        for key, val in want.items():
+            assert got[key] == val, (r, key)
