@@ -56,6 +56,14 @@ void Arena::release() {
   total_ = 0;
 }
 
+void Arena::drop(const std::string& name) {
+  auto it = bufs_.find(name);
+  if (it == bufs_.end()) return;
+  if (it->second.p) cudaFree(it->second.p);
+  total_ -= it->second.bytes;
+  bufs_.erase(it);
+}
+
 void* Arena::get(const std::string& name, size_t bytes) {
   if (bytes == 0) bytes = 16;
   bytes = (bytes + 255) & ~size_t(255);
@@ -127,6 +135,7 @@ void Context::upload(const HostGraph& hg) {
   launch_graph_prepare(g_, arena_.get("tmp.prep", tb), tb, stream_);
   orig_id_ = hg.orig_id;
   sync();
+  arena_.drop("tmp.prep");  // sort scratch (~16 B/edge): upload-only, return it to HBM
   last_.upload = since(t0);
 }
 
@@ -214,22 +223,20 @@ void Context::build_items(RankDev& r) {
   const std::string p = "r" + std::to_string(r.tau) + ".";
   const uint64_t m = g_.m;
   const uint32_t n = g_.n;
-  uint32_t* cnt_f = as<uint32_t>(arena_.get("tmp.cntf", (m + 2) * 4));
-  uint32_t* cnt_r = as<uint32_t>(arena_.get("tmp.cntr", (m + 2) * 4));
-  uint64_t* pos_f = as<uint64_t>(arena_.get("tmp.posf", (m + 2) * 8));
-  uint64_t* pos_r = as<uint64_t>(arena_.get("tmp.posr", (m + 2) * 8));
+  // One count/position scratch pair serves both directions in turn (12 B per
+  // edge instead of 24: at 1B edges the difference decides whether eight
+  // partitions fit one GPU).  Both directions hold the same number of items.
+  uint32_t* cnt = as<uint32_t>(arena_.get("tmp.cnt", (m + 2) * 4));
+  uint64_t* pos = as<uint64_t>(arena_.get("tmp.pos", (m + 2) * 8));
   const size_t sb = scan_tmp_bytes(std::max<uint64_t>(m, n) + 2);
   void* stmp = arena_.get("tmp.scan", sb);
   Items& f = r.fwd;
   Items& rv = r.rev;
-  DFS_CUDA(cudaMemsetAsync(cnt_f, 0, (m + 1) * 4, stream_));
-  DFS_CUDA(cudaMemsetAsync(cnt_r, 0, (m + 1) * 4, stream_));
   const int fa = cfg_.fasst ? 1 : 0;
-  launch_items_pass(g_, w_, tw_, r, 0, fa, 0, cnt_f, nullptr, f, stream_);
-  launch_items_pass(g_, w_, tw_, r, 1, fa, 0, cnt_r, nullptr, rv, stream_);
-  scan_u32_u64(cnt_f, pos_f, m, stmp, sb, stream_);
-  scan_u32_u64(cnt_r, pos_r, m, stmp, sb, stream_);
-  DFS_CUDA(cudaMemcpyAsync(&f.count, pos_f + m, 8, cudaMemcpyDeviceToHost, stream_));
+  DFS_CUDA(cudaMemsetAsync(cnt, 0, (m + 1) * 4, stream_));
+  launch_items_pass(g_, w_, tw_, r, 0, fa, 0, cnt, nullptr, f, stream_);
+  scan_u32_u64(cnt, pos, m, stmp, sb, stream_);
+  DFS_CUDA(cudaMemcpyAsync(&f.count, pos + m, 8, cudaMemcpyDeviceToHost, stream_));
   sync();
   rv.count = f.count;
   const size_t ic = std::max<uint64_t>(f.count, 1);
@@ -241,12 +248,15 @@ void Context::build_items(RankDev& r) {
     it.mask = as<uint32_t>(arena_.get(q + "mask", ic * 4));
     it.batch = as<uint8_t>(arena_.get(q + "batch", ic));
   }
-  launch_items_pass(g_, w_, tw_, r, 0, fa, 1, cnt_f, pos_f, f, stream_);
-  launch_items_pass(g_, w_, tw_, r, 1, fa, 1, cnt_r, pos_r, rv, stream_);
   uint64_t* meta = as<uint64_t>(arena_.get("tmp.meta", 8 * 8));
   DFS_CUDA(cudaMemsetAsync(meta, 0, 8 * 8, stream_));
-  finish_items(r, 0, pos_f, meta);
-  finish_items(r, 1, pos_r, meta + 4);
+  launch_items_pass(g_, w_, tw_, r, 0, fa, 1, cnt, pos, f, stream_);
+  finish_items(r, 0, pos, meta);
+  DFS_CUDA(cudaMemsetAsync(cnt, 0, (m + 1) * 4, stream_));
+  launch_items_pass(g_, w_, tw_, r, 1, fa, 0, cnt, nullptr, rv, stream_);
+  scan_u32_u64(cnt, pos, m, stmp, sb, stream_);
+  launch_items_pass(g_, w_, tw_, r, 1, fa, 1, cnt, pos, rv, stream_);
+  finish_items(r, 1, pos, meta + 4);
   launch_popc_sum(f.mask, f.count, reinterpret_cast<unsigned long long*>(meta + 3), stream_);
   uint64_t hm[8];  // the partition's one metadata readback
   DFS_CUDA(cudaMemcpyAsync(hm, meta, sizeof hm, cudaMemcpyDeviceToHost, stream_));

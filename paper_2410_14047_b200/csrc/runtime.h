@@ -27,6 +27,7 @@ class Arena {
     return it != bufs_.end() && it->second.bytes >= bytes;
   }
   size_t bytes() const { return total_; }
+  void drop(const std::string& name);  // free one buffer (stream-ordered callers sync first)
   void release();
 
  private:
