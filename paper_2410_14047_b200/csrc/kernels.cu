@@ -797,33 +797,110 @@ __device__ __forceinline__ void push_row(uint32_t u, uint32_t stamp, uint32_t* l
   for (uint32_t c = c0; c < c1; ++c) chunks[ci + (c - c0)] = c;
 }
 
-// Cascade bookkeeping of a row that just received new VISITED bits: one
-// 64-bit stamp (round base << 32 | level stamp) deduplicates both the dirty
-// list (rows to rescore after this cascade) and the next-level frontier.
-__device__ __forceinline__ void cascade_mark(uint32_t v, uint32_t base, uint32_t stamp,
-                                             unsigned long long* cstamp, uint32_t* dirty,
-                                             unsigned int* dirty_count, const uint32_t* row_chunk,
-                                             uint32_t* rows, uint32_t* chunks,
-                                             unsigned long long* qcg) {
-  const unsigned long long want = (static_cast<unsigned long long>(base) << 32) | stamp;
-  if (ld_volatile(&cstamp[v]) == want) return;
-  const unsigned long long old = atomicExch(&cstamp[v], want);
-  if (old == want) return;
-  if (uint32_t(old >> 32) != base) dirty[agg_reserve(dirty_count, 1u)] = v;
-  if (uint32_t(old) != stamp) {
-    const uint32_t c0 = row_chunk[v], c1 = row_chunk[v + 1];
-    const unsigned long long o = agg_reserve64(qcg, (1ull << 32) | (c1 - c0));
-    rows[o >> 32] = v;
-    const uint32_t ci = uint32_t(o);
-    for (uint32_t c = c0; c < c1; ++c) chunks[ci + (c - c0)] = c;
-  }
-}
-
-// Per-warp staging for the flattened item distribution.
+// Per-warp staging for the flattened item distribution, plus the warp's
+// pending cascade marks (rows for the next frontier, rows newly dirty).
+constexpr unsigned kMarkCap = 96;    // >= kMarkFlush + 64 (one item pair per lane per step)
+constexpr unsigned kMarkFlush = 32;  // flush at a convergent point once this many are pending
 struct WarpStage {
   uint32_t incl[32];
   uint32_t row[32];
   unsigned long long beg[32];
+  uint32_t mrows[kMarkCap];
+  uint32_t mdirty[kMarkCap];
+  unsigned nr, nd;
+};
+
+// Cascade bookkeeping of a row that just received new VISITED bits: one
+// 64-bit stamp (round base << 32 | level stamp) deduplicates both the dirty
+// list (rows to rescore after this cascade) and the next-level frontier.
+// The queue/dirty reservations are deferred into the warp's buffer (a level
+// of a large cascade marks ~10^5 rows: one global counter atomic per row
+// serialises at that address) and published by mark_flush.
+__device__ __forceinline__ void cascade_mark(uint32_t v, uint32_t base, uint32_t stamp,
+                                             unsigned long long* cstamp, uint32_t* dirty,
+                                             unsigned int* dirty_count, const uint32_t* row_chunk,
+                                             uint32_t* rows, uint32_t* chunks,
+                                             unsigned long long* qcg, WarpStage& ws) {
+  const unsigned long long want = (static_cast<unsigned long long>(base) << 32) | stamp;
+  if (ld_volatile(&cstamp[v]) == want) return;
+  const unsigned long long old = atomicExch(&cstamp[v], want);
+  if (old == want) return;
+  if (uint32_t(old >> 32) != base) {
+    const unsigned i = atomicAdd(&ws.nd, 1u);
+    if (i < kMarkCap) ws.mdirty[i] = v;
+    else dirty[agg_reserve(dirty_count, 1u)] = v;
+  }
+  if (uint32_t(old) != stamp) {
+    const unsigned i = atomicAdd(&ws.nr, 1u);
+    if (i < kMarkCap) {
+      ws.mrows[i] = v;
+    } else {
+      const uint32_t c0 = row_chunk[v], c1 = row_chunk[v + 1];
+      const unsigned long long o = agg_reserve64(qcg, (1ull << 32) | (c1 - c0));
+      rows[o >> 32] = v;
+      const uint32_t ci = uint32_t(o);
+      for (uint32_t c = c0; c < c1; ++c) chunks[ci + (c - c0)] = c;
+    }
+  }
+}
+
+// Publish the warp's pending marks (warp-converged): one counter atomic per
+// list, rows with their chunk ids laid out by a warp prefix sum.
+__device__ __forceinline__ void mark_flush(WarpStage& ws, uint32_t* dirty,
+                                           unsigned int* dirty_count, const uint32_t* row_chunk,
+                                           uint32_t* rows, uint32_t* chunks,
+                                           unsigned long long* qcg) {
+  __syncwarp();
+  const unsigned lane = lane_id();
+  const unsigned nd = min(ws.nd, kMarkCap), nr = min(ws.nr, kMarkCap);
+  if (nd) {
+    unsigned o = 0;
+    if (lane == 0) o = atomicAdd(dirty_count, nd);
+    o = __shfl_sync(0xffffffffu, o, 0);
+    for (unsigned i = lane; i < nd; i += 32) dirty[o + i] = ws.mdirty[i];
+  }
+  if (nr) {
+    uint32_t c0[kMarkCap / 32], cn[kMarkCap / 32], ex[kMarkCap / 32];
+    uint32_t run = 0;
+#pragma unroll
+    for (unsigned k = 0; k < kMarkCap / 32; ++k) {
+      const unsigned i = k * 32 + lane;
+      c0[k] = cn[k] = 0;
+      if (i < nr) {
+        const uint32_t v = ws.mrows[i];
+        c0[k] = row_chunk[v];
+        cn[k] = row_chunk[v + 1] - c0[k];
+      }
+      uint32_t incl = cn[k];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= unsigned(o)) incl += t;
+      }
+      ex[k] = run + incl - cn[k];
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    unsigned long long o = 0;
+    if (lane == 0) o = atomicAdd(qcg, (static_cast<unsigned long long>(nr) << 32) | run);
+    o = __shfl_sync(0xffffffffu, o, 0);
+    const uint32_t ro = uint32_t(o >> 32), co = uint32_t(o);
+#pragma unroll
+    for (unsigned k = 0; k < kMarkCap / 32; ++k) {
+      const unsigned i = k * 32 + lane;
+      if (i < nr) {
+        rows[ro + i] = ws.mrows[i];
+        for (uint32_t c = 0; c < cn[k]; ++c) chunks[co + ex[k] + c] = c0[k] + c;
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0) ws.nr = ws.nd = 0;
+  __syncwarp();
+}
+
+// Per-step hook of for_frontier_items (warp-converged): none by default.
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
 };
 
 // Warp-cooperative work distribution over a frontier of chunks: one atomic
@@ -831,11 +908,13 @@ struct WarpStage {
 // prefix sum of their sizes) and dealt to lanes 32 at a time, so lanes stay
 // busy even when most rows have only a handful of items (R-MAT tails) and
 // hub rows are spread over many warps.  f(row_a, item_a, ok_a, row_b, item_b,
-// ok_b) per pair of items (two independent load chains in flight per lane).
-template <class F>
+// ok_b) per pair of items (two independent load chains in flight per lane);
+// hook() after each pair step, all lanes converged.
+template <class F, class H = NoHook>
 __device__ __forceinline__ void for_frontier_items(const Items& it, const uint32_t* frontier,
                                                    uint32_t nc, unsigned int* work_ctr,
-                                                   WarpStage& ws, uint64_t n_warps, F&& f) {
+                                                   WarpStage& ws, uint64_t n_warps, F&& f,
+                                                   H&& hook = H()) {
   const unsigned lane = lane_id();
   // Chunks claimed per warp: 32 when the frontier is large (tiny R-MAT rows
   // keep lanes busy), fewer when it is small so that a few full chunks
@@ -892,6 +971,8 @@ __device__ __forceinline__ void for_frontier_items(const Items& it, const uint32
         ib = ws.beg[lo] + (tb - (lo ? ws.incl[lo - 1] : 0));
       }
       f(rowa, ia, oka, rowb, ib, okb);
+      __syncwarp();
+      hook();
     }
     __syncwarp();
   }
@@ -1825,6 +1906,8 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
   const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   const uint32_t W32 = r.W32;
   WarpStage& ws = stage[threadIdx.x >> 5];
+  if (lane == 0) ws.nr = ws.nd = 0;
+  __syncwarp();
   unsigned long long marked = 0;
   const bool pull_ok = r.Jp <= kPullMaxJp;
   uint32_t* cacc = cas_smem + (threadIdx.x >> 5) * (kPullMaxJp / 32);
@@ -1911,7 +1994,13 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
       atomicOr(fnxt + uint64_t(v) * W32 + b, nb);
       marked += __popc(nb);
       cascade_mark(v, base, stamp, r.cstamp, r.dirty, &r.ctl->dirty_count, r.fwd.row_chunk, rows_n,
-                   chunks_n, &qc[gn]);
+                   chunks_n, &qc[gn], ws);
+    };
+    auto flush = [&] {
+      mark_flush(ws, r.dirty, &r.ctl->dirty_count, r.fwd.row_chunk, rows_n, chunks_n, &qc[gn]);
+    };
+    auto hook = [&] {  // warp-converged, after a __syncwarp
+      if (ws.nr >= kMarkFlush || ws.nd >= kMarkFlush) flush();
     };
     // Top-down pair: frontier row u -> targets of two forward items.
     auto visit = [&](uint32_t ua, uint64_t ia, bool pa, uint32_t ub, uint64_t ib, bool pb) {
@@ -1933,6 +2022,8 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
       // a shared accumulator, then claims the unvisited ones with one update
       // per batch word (direction-optimising BFS, Beamer et al.).
       for (uint64_t k = my_warp; k < r.rev.nbig; k += n_warps) {
+        __syncwarp();
+        hook();
         const uint32_t c = r.rev.big[k];
         const uint32_t v = r.rev.chunk_row[c];
         const uint64_t beg = r.rev.chunk_beg[c], end = r.rev.chunk_beg[c + 1];
@@ -1999,7 +2090,7 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
         __syncwarp();
         if (__any_sync(0xffffffffu, got) && lane == 0)
           cascade_mark(v, base, stamp, r.cstamp, r.dirty, &r.ctl->dirty_count, r.fwd.row_chunk,
-                       rows_n, chunks_n, &qc[gn]);
+                       rows_n, chunks_n, &qc[gn], ws);
       }
       // Small target rows: item-parallel, one atomicOr per newly reached word.
       for_frontier_items(r.rev, r.rev.small, r.rev.nsmall, &cnt[8 + g], ws, n_warps,
@@ -2015,10 +2106,12 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
         const uint32_t cb = nb2 ? __ldcg(fcur + uint64_t(ub) * W32 + bb) & nb2 : 0;
         if (ca) claim(va, ba, ca);
         if (cb) claim(vb, bb, cb);
-      });
+      }, hook);
     } else {
-      for_frontier_items(r.fwd, r.q.chunks[g], nc, &cnt[8 + g], ws, n_warps, visit);
+      for_frontier_items(r.fwd, r.q.chunks[g], nc, &cnt[8 + g], ws, n_warps, visit, hook);
     }
+    __syncwarp();
+    if (ws.nr || ws.nd) flush();
   };
   // Final clean-up: fresh bits left by the last two levels.
   auto finish = [&](uint32_t L, bool solo) {
