@@ -799,7 +799,7 @@ __device__ __forceinline__ void push_row(uint32_t u, uint32_t stamp, uint32_t* l
 
 // Per-warp staging for the flattened item distribution, plus the warp's
 // pending cascade marks (rows for the next frontier, rows newly dirty).
-constexpr unsigned kMarkCap = 96;    // >= kMarkFlush + 64 (one item pair per lane per step)
+constexpr unsigned kMarkCap = 160;   // >= kMarkFlush + 128 (four items per lane per step)
 constexpr unsigned kMarkFlush = 32;  // flush at a convergent point once this many are pending
 struct WarpStage {
   uint32_t incl[32];
@@ -809,6 +809,26 @@ struct WarpStage {
   uint32_t mdirty[kMarkCap];
   unsigned nr, nd;
 };
+
+// push_row with the queue reservation deferred into the warp's buffer
+// (published by mark_flush; overflow falls back to a direct reservation).
+__device__ __forceinline__ void push_row_buf(uint32_t u, uint32_t stamp, uint32_t* lstamp,
+                                             const uint32_t* row_chunk, uint32_t* rows,
+                                             uint32_t* chunks, unsigned long long* qcg,
+                                             WarpStage& ws) {
+  if (ld_volatile(&lstamp[u]) == stamp) return;
+  if (atomicExch(&lstamp[u], stamp) == stamp) return;
+  const unsigned i = atomicAdd(&ws.nr, 1u);
+  if (i < kMarkCap) {
+    ws.mrows[i] = u;
+    return;
+  }
+  const uint32_t c0 = row_chunk[u], c1 = row_chunk[u + 1];
+  const unsigned long long o = agg_reserve64(qcg, (1ull << 32) | (c1 - c0));
+  rows[o >> 32] = u;
+  const uint32_t ci = uint32_t(o);
+  for (uint32_t c = c0; c < c1; ++c) chunks[ci + (c - c0)] = c;
+}
 
 // Cascade bookkeeping of a row that just received new VISITED bits: one
 // 64-bit stamp (round base << 32 | level stamp) deduplicates both the dirty
@@ -1123,6 +1143,8 @@ __device__ __forceinline__ uint32_t simulate_body(const RankDev& r, const SimOpt
   const uint64_t gwarp = gtid >> 5;
   const uint64_t nw = gthreads >> 5;
   WarpStage& ws = stage[threadIdx.x >> 5];
+  if (lane == 0) ws.nr = ws.nd = 0;
+  __syncwarp();
   // Pull accumulator: Jp bytes of running maxima + touched-batch bits per warp.
   const uint32_t W32 = r.W32;
   const bool pull_ok = r.Jp <= kPullMaxJp;
@@ -1164,6 +1186,12 @@ __device__ __forceinline__ uint32_t simulate_body(const RankDev& r, const SimOpt
     const uint32_t stamp = base + s;
     uint32_t* rows_n = r.q.rows[gn];
     uint32_t* chunks_n = r.q.chunks[gn];
+    auto flush = [&] {
+      mark_flush(ws, nullptr, nullptr, r.rev.row_chunk, rows_n, chunks_n, &qc[gn]);
+    };
+    auto hook = [&] {  // warp-converged, after a __syncwarp
+      if (ws.nr >= kMarkFlush) flush();
+    };
     if ((a.dbg & 4) && blockIdx.x == 0 && threadIdx.x == 0) trace(solo ? 1 : 0, s, nc);
     // Large frontiers (and sweep 1) run PULL-style over row-owned forward
     // chunks: a warp gathers the sources of one destination row chunk into a
@@ -1176,6 +1204,8 @@ __device__ __forceinline__ uint32_t simulate_body(const RankDev& r, const SimOpt
     if (pull) {
       const uint32_t need = base + s - 1;  // source changed in sweep s-1 (or later)
       for (uint64_t k = my_warp; k < ((a.dbg & 1) ? 0 : r.fwd.nbig); k += n_warps) {
+        __syncwarp();
+        hook();
         const uint32_t c = r.fwd.big[k];
         const uint32_t u = r.fwd.chunk_row[c];
         const uint64_t beg = r.fwd.chunk_beg[c], end = r.fwd.chunk_beg[c + 1];
@@ -1278,7 +1308,7 @@ __device__ __forceinline__ uint32_t simulate_body(const RankDev& r, const SimOpt
         if (lane < 4) touched[lane] = 0;
         __syncwarp();
         if (__any_sync(0xffffffffu, changed) && lane == 0)
-          push_row(u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &qc[gn]);
+          push_row_buf(u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &qc[gn], ws);
       }
       // Small destination rows (<= kSmallRow items): item-parallel over the
       // flattened chunks, one CAS per item on a lightly contended row.
@@ -1340,8 +1370,10 @@ __device__ __forceinline__ uint32_t simulate_body(const RankDev& r, const SimOpt
             upd += __popc(mq[q]);
             ++nitems;
             if (ch)
-              push_row(uq[q], stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &qc[gn]);
+              push_row_buf(uq[q], stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &qc[gn], ws);
           }
+          __syncwarp();
+          hook();
         }
       }
     } else {
@@ -1379,11 +1411,13 @@ __device__ __forceinline__ uint32_t simulate_body(const RankDev& r, const SimOpt
               }
             }
             if (ca)
-              push_row(A.u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &qc[gn]);
+              push_row_buf(A.u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &qc[gn], ws);
             if (cb)
-              push_row(B.u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &qc[gn]);
-          });
+              push_row_buf(B.u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &qc[gn], ws);
+          }, hook);
     }
+    __syncwarp();
+    if (ws.nr) flush();
   };
   // engine.cpp:81-82: re-sync snapshot rows that moved (Jacobi schedule).
   auto resync = [&](uint32_t s, bool solo) {
@@ -2092,21 +2126,40 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
           cascade_mark(v, base, stamp, r.cstamp, r.dirty, &r.ctl->dirty_count, r.fwd.row_chunk,
                        rows_n, chunks_n, &qc[gn], ws);
       }
-      // Small target rows: item-parallel, one atomicOr per newly reached word.
-      for_frontier_items(r.rev, r.rev.small, r.rev.nsmall, &cnt[8 + g], ws, n_warps,
-                         [&](uint32_t va, uint64_t ia, bool pa, uint32_t vb, uint64_t ib, bool pb) {
-        const uint32_t ba = pa ? __ldg(r.rev.batch + ia) : 0, bb = pb ? __ldg(r.rev.batch + ib) : 0;
-        const uint32_t ma = pa ? __ldg(r.rev.mask + ia) : 0, mb = pb ? __ldg(r.rev.mask + ib) : 0;
-        const uint32_t ua = pa ? __ldg(r.rev.other + ia) : 0, ub = pb ? __ldg(r.rev.other + ib) : 0;
-        // bottom-up: unvisited simulations of the target first, then parents
-        const uint32_t xa = pa ? __ldcg(r.vis + uint64_t(va) * W32 + ba) : 0xFFFFFFFFu;
-        const uint32_t xb = pb ? __ldcg(r.vis + uint64_t(vb) * W32 + bb) : 0xFFFFFFFFu;
-        const uint32_t na = ma & ~xa, nb2 = mb & ~xb;
-        const uint32_t ca = na ? __ldcg(fcur + uint64_t(ua) * W32 + ba) & na : 0;
-        const uint32_t cb = nb2 ? __ldcg(fcur + uint64_t(ub) * W32 + bb) & nb2 : 0;
-        if (ca) claim(va, ba, ca);
-        if (cb) claim(vb, bb, cb);
-      }, hook);
+      // Small target rows: item-parallel straight over their flat item list
+      // (no chunk indirection), four items per lane with every load stage
+      // issued for all four first; one atomicOr per newly reached word.
+      const uint64_t nsi = r.rev.nsmall_items;
+      for (uint64_t k0 = my_warp * 128; k0 < nsi; k0 += n_warps * 128) {
+        uint64_t iq[4];
+        uint32_t vq[4], uq[4], mq[4], bq[4], xq[4], fq[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint64_t kk = k0 + lane + 32 * q;
+          iq[q] = kk < nsi ? __ldg(r.rev.small_items + kk) : 0;
+          mq[q] = kk < nsi ? 1u : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          vq[q] = mq[q] ? __ldg(r.rev.row + iq[q]) : 0;
+          uq[q] = mq[q] ? __ldg(r.rev.other + iq[q]) : 0;
+          bq[q] = mq[q] ? __ldg(r.rev.batch + iq[q]) : 0;
+          mq[q] = mq[q] ? __ldg(r.rev.mask + iq[q]) : 0;
+        }
+        // the target's visited word and the parent's fresh word together
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          xq[q] = mq[q] ? __ldcg(r.vis + uint64_t(vq[q]) * W32 + bq[q]) : 0xFFFFFFFFu;
+          fq[q] = mq[q] ? __ldcg(fcur + uint64_t(uq[q]) * W32 + bq[q]) : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t c = fq[q] & mq[q] & ~xq[q];
+          if (c) claim(vq[q], bq[q], c);
+        }
+        __syncwarp();
+        hook();
+      }
     } else {
       for_frontier_items(r.fwd, r.q.chunks[g], nc, &cnt[8 + g], ws, n_warps, visit, hook);
     }
