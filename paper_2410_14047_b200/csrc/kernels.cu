@@ -1120,6 +1120,9 @@ struct SimArgs {
 #ifndef DFS_SIM_MINB
 #define DFS_SIM_MINB 3
 #endif
+#ifndef DFS_SIM_CLAIM
+#define DFS_SIM_CLAIM 128
+#endif
 struct SimOpts {
   int cap;
   int dbg;
@@ -1314,12 +1317,27 @@ __device__ __forceinline__ uint32_t simulate_body(const RankDev& r, const SimOpt
       // flattened chunks, one CAS per item on a lightly contended row.
       {
         const uint64_t nsi = (a.dbg & 2) ? 0 : r.fwd.nsmall_items;
-        // dynamic: a warp claims 128 items at a time (balances the big-row tail)
+        // dynamic: a warp claims DFS_SIM_CLAIM items at a time (balances the
+        // big-row tail), 128 per step; 0 = static grid-stride
+        unsigned long long kc = 0, ke = 0;
+        uint64_t kst = my_warp * 128;
         for (;;) {
-          unsigned long long k0 = 0;
-          if (lane == 0)
-            k0 = atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[12 + 2 * (s & 1)]), 128ull);
-          k0 = __shfl_sync(0xffffffffu, k0, 0);
+          unsigned long long k0;
+          if (DFS_SIM_CLAIM == 0) {
+            k0 = kst;
+            kst += n_warps * 128;
+          } else {
+            if (kc >= ke) {
+              unsigned long long b = 0;
+              if (lane == 0)
+                b = atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[12 + 2 * (s & 1)]),
+                              (unsigned long long)(DFS_SIM_CLAIM));
+              kc = __shfl_sync(0xffffffffu, b, 0);
+              ke = kc + DFS_SIM_CLAIM;
+            }
+            k0 = kc;
+            kc += 128;
+          }
           if (k0 >= nsi) break;
           // four items per lane, every load stage issued for all four first
           uint64_t iq[4];
@@ -2129,6 +2147,7 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
       // Small target rows: item-parallel straight over their flat item list
       // (no chunk indirection), four items per lane with every load stage
       // issued for all four first; one atomicOr per newly reached word.
+      // Static grid-stride (dynamic claiming measured slower here: C2/C3 IC).
       const uint64_t nsi = r.rev.nsmall_items;
       for (uint64_t k0 = my_warp * 128; k0 < nsi; k0 += n_warps * 128) {
         uint64_t iq[4];
