@@ -88,17 +88,40 @@ __global__ void k_src(uint32_t n, const uint64_t* __restrict__ off, uint32_t* __
     for (uint64_t e = off[u] + lane_id(); e < off[u + 1]; e += 32) src[e] = uint32_t(u);
 }
 
-__global__ void k_ehash_indeg(uint64_t m, const uint32_t* __restrict__ src,
-                              const uint32_t* __restrict__ adj, uint32_t* __restrict__ ehash,
-                              uint32_t* __restrict__ indeg, uint32_t* __restrict__ iota) {
+__global__ void k_ehash(uint64_t m, const uint32_t* __restrict__ src,
+                        const uint32_t* __restrict__ adj, uint32_t* __restrict__ ehash,
+                        uint32_t* __restrict__ iota) {
   for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < m;
        e += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t v = adj[e];
-    ehash[e] = edge_hash(src[e], v);  // graph.cpp:180, on dense ids
-    atomicAdd(&indeg[v], 1u);
+    ehash[e] = edge_hash(src[e], adj[e]);  // graph.cpp:180, on dense ids
     iota[e] = uint32_t(e);
   }
 }
+
+// In-degrees from the sorted targets instead of one atomic per edge (R-MAT
+// hubs serialise those): the last position of each target's run records the
+// run end; an inclusive max-scan of the ends gives toff[1..n].
+__global__ void k_run_ends(uint64_t m, const uint32_t* __restrict__ tdst,
+                           uint32_t* __restrict__ ends) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t v = tdst[i];
+    if (i + 1 == m || tdst[i + 1] != v) ends[v] = uint32_t(i + 1);
+  }
+}
+
+__global__ void k_indeg(uint32_t n, const uint64_t* __restrict__ toff,
+                        uint32_t* __restrict__ indeg) {
+  for (uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n;
+       v += uint64_t(gridDim.x) * blockDim.x)
+    indeg[v] = uint32_t(toff[v + 1] - toff[v]);
+}
+
+struct MaxU64 {
+  __device__ __forceinline__ uint64_t operator()(uint64_t a, uint64_t b) const {
+    return a > b ? a : b;
+  }
+};
 
 // ---------------------------------------------------------------- weights
 // graph.cpp:30-35 + :250-258: W = llround(w * 2^31), wc w = 1/indeg(v).
@@ -2701,14 +2724,16 @@ void dump_trace() {
   DFS_CUDA(cudaMemcpyToSymbol(g_trace_n, &z, sizeof z));
 }
 size_t graph_prepare_tmp_bytes(uint64_t m, uint32_t n) {
-  size_t sort_bytes = 0, scan_bytes = 0;
+  size_t sort_bytes = 0, scan_bytes = 0, max_bytes = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (const uint32_t*)nullptr,
                                   (uint32_t*)nullptr, (const uint32_t*)nullptr,
                                   (uint32_t*)nullptr, m ? m : 1);
   scan_bytes = scan_tmp_bytes(n + 1);
-  // layout: iota(m) | keys_out(m) | counts64 (n+1) | cub temp
-  return 2 * (m + 16) * sizeof(uint32_t) + (n + 16) * sizeof(uint64_t) +
-         std::max(sort_bytes, scan_bytes) + 1024;
+  cub::DeviceScan::InclusiveScan(nullptr, max_bytes, (const uint32_t*)nullptr, (uint64_t*)nullptr,
+                                 MaxU64{}, n ? n : 1);
+  // layout: iota(m) | cub temp
+  return (m + 16) * sizeof(uint32_t) + std::max(sort_bytes, std::max(scan_bytes, max_bytes)) +
+         1024;
 }
 
 size_t scan_tmp_bytes(uint64_t n) {
@@ -2732,36 +2757,32 @@ void launch_graph_prepare(DevGraph& g, void* tmp, size_t tmp_bytes, cudaStream_t
   char* p = static_cast<char*>(tmp);
   uint32_t* iota = reinterpret_cast<uint32_t*>(p);
   p += (m + 16) * sizeof(uint32_t);
-  uint32_t* keys_out = reinterpret_cast<uint32_t*>(p);
-  p += (m + 16) * sizeof(uint32_t);
-  uint64_t* off64 = reinterpret_cast<uint64_t*>(p);
-  (void)off64;
-  p += (g.n + 16) * sizeof(uint64_t);
   void* cubtmp = p;
   size_t cub_bytes = tmp_bytes - size_t(p - static_cast<char*>(tmp));
 
+  // indeg doubles as the run-end array until the in-degrees are written
   DFS_CUDA(cudaMemsetAsync(g.indeg, 0, (size_t(g.n) + 1) * sizeof(uint32_t), s));
-  if (m) {
-    k_src<<<grid_for(uint64_t(g.n) * 32), kThreads, 0, s>>>(g.n, g.off, g.src);
-    k_ehash_indeg<<<grid_for(m), kThreads, 0, s>>>(m, g.src, g.adj, g.ehash, g.indeg, iota);
-    int end_bit = 1;
-    while (end_bit < 32 && (uint64_t(1) << end_bit) < g.n) ++end_bit;
-    size_t bytes = cub_bytes;
-    // keys out = the targets in transposed order (tdst), values out = edge ids
-    DFS_CUDA(cub::DeviceRadixSort::SortPairs(cubtmp, bytes, g.adj, g.tdst, iota, g.tedge, m, 0,
-                                             end_bit, s));
-    (void)keys_out;
-
+  DFS_CUDA(cudaMemsetAsync(g.toff, 0, sizeof(uint64_t), s));
+  if (!m) {
+    DFS_CUDA(cudaMemsetAsync(g.toff, 0, (size_t(g.n) + 1) * sizeof(uint64_t), s));
+    return;
   }
-  // toff = exclusive scan of in-degrees (indeg[n] == 0 by the memset above)
+  k_src<<<grid_for(uint64_t(g.n) * 32), kThreads, 0, s>>>(g.n, g.off, g.src);
+  k_ehash<<<grid_for(m), kThreads, 0, s>>>(m, g.src, g.adj, g.ehash, iota);
+  int end_bit = 1;
+  while (end_bit < 32 && (uint64_t(1) << end_bit) < g.n) ++end_bit;
   size_t bytes = cub_bytes;
-  DFS_CUDA(cub::DeviceScan::ExclusiveScan(cubtmp, bytes, g.indeg, g.toff,
-                                          cuda::std::plus<uint64_t>{}, uint64_t(0), g.n + 1, s));
-  if (m)
-    k_transpose_fields<<<grid_for(m), kThreads, 0, s>>>(m, g.tedge, g.src, g.tdst, g.tsrc,
-                                                       g.thash);
+  // keys out = the targets in transposed order (tdst), values out = edge ids
+  // (stable: a target's in-edges stay in CSR order)
+  DFS_CUDA(cub::DeviceRadixSort::SortPairs(cubtmp, bytes, g.adj, g.tdst, iota, g.tedge, m, 0,
+                                           end_bit, s));
+  k_run_ends<<<grid_for(m), kThreads, 0, s>>>(m, g.tdst, g.indeg);
+  bytes = cub_bytes;
+  DFS_CUDA(cub::DeviceScan::InclusiveScan(cubtmp, bytes, g.indeg, g.toff + 1, MaxU64{}, g.n, s));
+  k_indeg<<<grid_for(g.n), kThreads, 0, s>>>(g.n, g.toff, g.indeg);
+  k_transpose_fields<<<grid_for(m), kThreads, 0, s>>>(m, g.tedge, g.src, g.tdst, g.tsrc, g.thash);
   DFS_CUDA(cudaGetLastError());
-  ++g_launches;
+  g_launches += 5;  // own kernels (the sort and scan are cub's)
 }
 
 void launch_tweights(const DevGraph& g, int kind, uint32_t W, const uint32_t* w, uint32_t* tw,

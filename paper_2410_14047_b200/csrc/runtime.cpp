@@ -56,12 +56,19 @@ void Arena::release() {
   total_ = 0;
 }
 
-void Arena::drop(const std::string& name) {
-  auto it = bufs_.find(name);
-  if (it == bufs_.end()) return;
-  if (it->second.p) cudaFree(it->second.p);
-  total_ -= it->second.bytes;
-  bufs_.erase(it);
+bool Arena::reclaim() {
+  bool any = false;
+  for (const std::string& name : reclaimable_) {
+    auto it = bufs_.find(name);
+    if (it == bufs_.end()) continue;
+    if (it->second.p) {
+      cudaFree(it->second.p);
+      any = true;
+    }
+    total_ -= it->second.bytes;
+    bufs_.erase(it);
+  }
+  return any;
 }
 
 void* Arena::get(const std::string& name, size_t bytes) {
@@ -76,6 +83,16 @@ void* Arena::get(const std::string& name, size_t bytes) {
     b.p = nullptr;
     b.bytes = 0;
     cudaError_t e = cudaMalloc(&b.p, bytes);
+    if (e == cudaErrorMemoryAllocation && reclaim()) {  // HBM pressure: drop idle scratch, retry
+      cudaGetLastError();
+      Buf& nb = bufs_[name];  // (reclaim may have rehashed the map)
+      e = cudaMalloc(&nb.p, bytes);
+      if (e == cudaSuccess) {
+        nb.bytes = bytes;
+        total_ += bytes;
+        return nb.p;
+      }
+    }
     if (e != cudaSuccess) {
       cudaGetLastError();
       throw Error(kNoMem, "device allocation of " + std::to_string(bytes) + " bytes for " + name +
@@ -135,7 +152,7 @@ void Context::upload(const HostGraph& hg) {
   launch_graph_prepare(g_, arena_.get("tmp.prep", tb), tb, stream_);
   orig_id_ = hg.orig_id;
   sync();
-  arena_.drop("tmp.prep");  // sort scratch (~16 B/edge): upload-only, return it to HBM
+  arena_.set_reclaimable("tmp.prep");  // sort scratch (~12 B/edge): upload-only
   last_.upload = since(t0);
 }
 
@@ -330,6 +347,13 @@ void Context::prepare(const RunConfig& cfg, const HostGraph* host_w_src, uint32_
       size_t fr = 0, tot = 0;
       DFS_CUDA(cudaMemGetInfo(&fr, &tot));
       take = fr > bytes + (size_t(4) << 30);
+      if (!take) {  // idle scratch first (the build above is stream-ordered: drain it)
+        sync();
+        if (arena_.reclaim()) {
+          DFS_CUDA(cudaMemGetInfo(&fr, &tot));
+          take = fr > bytes + (size_t(4) << 30);
+        }
+      }
     }
     if (take) r.pristine = as<int8_t>(arena_.get(name, bytes));
   }

@@ -27,7 +27,14 @@ class Arena {
     return it != bufs_.end() && it->second.bytes >= bytes;
   }
   size_t bytes() const { return total_; }
-  void drop(const std::string& name);  // free one buffer (stream-ordered callers sync first)
+  // Scratch that may be freed whenever an allocation would otherwise fail
+  // (no work in flight uses it: its users synchronise before returning).
+  void set_reclaimable(const std::string& name) {
+    for (const std::string& x : reclaimable_)
+      if (x == name) return;
+    reclaimable_.push_back(name);
+  }
+  bool reclaim();  // frees the reclaimable buffers; true if any bytes were freed
   void release();
 
  private:
@@ -36,6 +43,7 @@ class Arena {
     size_t bytes = 0;
   };
   std::unordered_map<std::string, Buf> bufs_;
+  std::vector<std::string> reclaimable_;
   size_t total_ = 0;
 };
 
