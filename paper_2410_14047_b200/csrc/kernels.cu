@@ -956,14 +956,9 @@ struct NoHook {
 template <class F, class H = NoHook>
 __device__ __forceinline__ void for_frontier_items(const Items& it, const uint32_t* frontier,
                                                    uint32_t nc, unsigned int* work_ctr,
-                                                   WarpStage& ws, uint64_t n_warps,
-                                                   uint64_t my_warp, F&& f, H&& hook = H()) {
+                                                   WarpStage& ws, uint64_t n_warps, F&& f,
+                                                   H&& hook = H()) {
   const unsigned lane = lane_id();
-  // Fewer chunks than warps: warp w takes chunk w (no claim round trip; the
-  // solo levels of small cascades are latency chains).  my_warp = ~0: always
-  // claim (simulate: A/B showed no gain there).
-  const bool fixed = my_warp != ~0ull && uint64_t(nc) < n_warps;
-  bool taken = false;
   // Chunks claimed per warp: 32 when the frontier is large (tiny R-MAT rows
   // keep lanes busy), fewer when it is small so that a few full chunks
   // (<= 128 items each) are spread over many warps instead of serialised.
@@ -971,14 +966,8 @@ __device__ __forceinline__ void for_frontier_items(const Items& it, const uint32
   const uint32_t G = per >= 32 ? 32u : (per < 1 ? 1u : uint32_t(per));
   for (;;) {
     unsigned b0 = 0;
-    if (fixed) {
-      if (taken) break;
-      taken = true;
-      b0 = uint32_t(my_warp);
-    } else {
-      if (lane == 0) b0 = atomicAdd(work_ctr, G);
-      b0 = __shfl_sync(0xffffffffu, b0, 0);
-    }
+    if (lane == 0) b0 = atomicAdd(work_ctr, G);
+    b0 = __shfl_sync(0xffffffffu, b0, 0);
     if (b0 >= nc) break;
     const uint32_t idx = b0 + lane;
     uint32_t row = 0, cntc = 0;
@@ -1430,7 +1419,7 @@ __device__ __forceinline__ uint32_t simulate_body(const RankDev& r, const SimOpt
       }
     } else {
       for_frontier_items(
-          r.rev, s == 1 ? nullptr : r.q.chunks[g], nc, &cnt[8 + g], ws, n_warps, ~0ull,
+          r.rev, s == 1 ? nullptr : r.q.chunks[g], nc, &cnt[8 + g], ws, n_warps,
           [&](uint32_t va, uint64_t ia, bool pa, uint32_t vb, uint64_t ib, bool pb) {
             SimItem A, B;
             if (pa) sim_fields(A, r.rev, ia);
@@ -2214,7 +2203,7 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
         hook();
       }
     } else {
-      for_frontier_items(r.fwd, r.q.chunks[g], nc, &cnt[8 + g], ws, n_warps, my_warp, visit, hook);
+      for_frontier_items(r.fwd, r.q.chunks[g], nc, &cnt[8 + g], ws, n_warps, visit, hook);
     }
     __syncwarp();
     if (ws.nr || ws.nd) flush();
