@@ -806,22 +806,9 @@ __device__ __forceinline__ uint32_t qrows(const unsigned long long* qc, int g) {
   return uint32_t(ld_volatile(&qc[g]) >> 32);
 }
 
-// Push of row u into the next generation (deduplicated by stamp): appends u
-// to rows[gn] and all of u's chunks to chunks[gn].
-__device__ __forceinline__ void push_row(uint32_t u, uint32_t stamp, uint32_t* lstamp,
-                                         const uint32_t* row_chunk, uint32_t* rows,
-                                         uint32_t* chunks, unsigned long long* qcg) {
-  if (ld_volatile(&lstamp[u]) == stamp) return;
-  if (atomicExch(&lstamp[u], stamp) == stamp) return;
-  const uint32_t c0 = row_chunk[u], c1 = row_chunk[u + 1];
-  const unsigned long long o = agg_reserve64(qcg, (1ull << 32) | (c1 - c0));
-  rows[o >> 32] = u;
-  const uint32_t ci = uint32_t(o);
-  for (uint32_t c = c0; c < c1; ++c) chunks[ci + (c - c0)] = c;
-}
-
 // Per-warp staging for the flattened item distribution, plus the warp's
-// pending cascade marks (rows for the next frontier, rows newly dirty).
+// pending frontier marks (rows for the next generation; cascade: rows newly
+// dirty).
 constexpr unsigned kMarkCap = 160;   // >= kMarkFlush + 128 (four items per lane per step)
 constexpr unsigned kMarkFlush = 32;  // flush at a convergent point once this many are pending
 struct WarpStage {
@@ -833,8 +820,9 @@ struct WarpStage {
   unsigned nr, nd;
 };
 
-// push_row with the queue reservation deferred into the warp's buffer
-// (published by mark_flush; overflow falls back to a direct reservation).
+// Push of row u into the next generation, deduplicated by stamp: u is parked
+// in the warp's buffer and published with its chunk ids by mark_flush
+// (overflow falls back to a direct reservation).
 __device__ __forceinline__ void push_row_buf(uint32_t u, uint32_t stamp, uint32_t* lstamp,
                                              const uint32_t* row_chunk, uint32_t* rows,
                                              uint32_t* chunks, unsigned long long* qcg,
