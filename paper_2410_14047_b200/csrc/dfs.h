@@ -217,6 +217,9 @@ void scan_u32_u64(const uint32_t* in, uint64_t* out, uint64_t n, void* tmp, size
 // Sampled-item construction for one rank and direction (dir 0 = by source u
 // over the CSR, dir 1 = by target v over the transpose).  write = 0 counts
 // items per edge position into cnt; write = 1 emits them at pos_off.
+// Reverse-direction item counts per transposed position, gathered from the
+// forward item offsets (an edge has the same items in both directions).
+void launch_rev_counts(const DevGraph& g, const uint64_t* pos_f, uint32_t* cnt, cudaStream_t s);
 void launch_items_pass(const DevGraph& g, const uint32_t* w, const uint32_t* tw, const RankDev& r,
                        int dir, int fasst, int write, uint32_t* cnt, const uint64_t* pos_off,
                        Items& it, cudaStream_t s);

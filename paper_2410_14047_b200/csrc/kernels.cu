@@ -269,6 +269,22 @@ __global__ void k_items(uint64_t npos, const uint32_t* __restrict__ p_hash,
   }
 }
 
+// Transposed position p holds edge tedge[p], whose item count is its forward
+// count (the sampling test depends on (edge hash, weight, slot) only): one
+// gather instead of re-evaluating the windows.  cnt[m] = 0 closes the scan.
+__global__ void k_rev_counts(uint64_t m, const uint32_t* __restrict__ tedge,
+                             const uint64_t* __restrict__ pos_f, uint32_t* __restrict__ cnt) {
+  for (uint64_t p = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; p <= m;
+       p += uint64_t(gridDim.x) * blockDim.x) {
+    if (p == m) {
+      cnt[m] = 0;
+      continue;
+    }
+    const uint32_t e = tedge[p];
+    cnt[p] = uint32_t(pos_f[e + 1] - pos_f[e]);
+  }
+}
+
 // Slot LUT: lut[k] = first slot with x >= k << kLutShift (sorted slices).
 __global__ void k_xlut(const uint32_t* __restrict__ x, uint32_t J, uint32_t* __restrict__ lut) {
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k <= (1u << kLutBits);
@@ -2784,6 +2800,12 @@ void launch_tweights(const DevGraph& g, int kind, uint32_t W, const uint32_t* w,
 void launch_weights(const DevGraph& g, int kind, uint32_t W, uint32_t* w, cudaStream_t s) {
   if (!g.m) return;
   k_weights<<<grid_for(g.m), kThreads, 0, s>>>(g.m, kind, W, g.adj, g.indeg, w);
+  DFS_CUDA(cudaGetLastError());
+  ++g_launches;
+}
+
+void launch_rev_counts(const DevGraph& g, const uint64_t* pos_f, uint32_t* cnt, cudaStream_t s) {
+  k_rev_counts<<<grid_for(g.m + 1), kThreads, 0, s>>>(g.m, g.tedge, pos_f, cnt);
   DFS_CUDA(cudaGetLastError());
   ++g_launches;
 }
