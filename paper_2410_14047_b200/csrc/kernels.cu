@@ -1233,12 +1233,17 @@ __device__ __forceinline__ uint32_t simulate_body(const RankDev& r, const SimOpt
         !CNT && !solo && pull_ok && (s == 1 || uint64_t(nc) * a.pull_f > r.rev.chunks);
     if (pull) {
       const uint32_t need = base + s - 1;  // source changed in sweep s-1 (or later)
-      for (uint64_t k = my_warp; k < ((a.dbg & 1) ? 0 : r.fwd.nbig); k += n_warps) {
+      const uint64_t nbig = (a.dbg & 1) ? 0 : r.fwd.nbig;
+      // chunk headers one iteration ahead (their two dependent loads overlap
+      // the current chunk instead of heading its latency chain)
+      uint32_t c_nx = my_warp < nbig ? r.fwd.big[my_warp] : 0;
+      for (uint64_t k = my_warp; k < nbig; k += n_warps) {
         __syncwarp();
         hook();
-        const uint32_t c = r.fwd.big[k];
+        const uint32_t c = c_nx;
         const uint32_t u = r.fwd.chunk_row[c];
         const uint64_t beg = r.fwd.chunk_beg[c], end = r.fwd.chunk_beg[c + 1];
+        if (k + n_warps < nbig) c_nx = r.fwd.big[k + n_warps];
         // A chunk has <= 4*32 items: each lane stages its (up to) 4 items'
         // fields, stamps and first live source word before any is consumed.
         uint32_t vq[4], mq[4], bq[4];
@@ -2100,12 +2105,15 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
       // A warp ORs the fresh bits of all in-neighbours of one target row into
       // a shared accumulator, then claims the unvisited ones with one update
       // per batch word (direction-optimising BFS, Beamer et al.).
-      for (uint64_t k = my_warp; k < r.rev.nbig; k += n_warps) {
+      const uint64_t nbig = r.rev.nbig;
+      uint32_t c_nx = my_warp < nbig ? r.rev.big[my_warp] : 0;  // one iteration ahead
+      for (uint64_t k = my_warp; k < nbig; k += n_warps) {
         __syncwarp();
         hook();
-        const uint32_t c = r.rev.big[k];
+        const uint32_t c = c_nx;
         const uint32_t v = r.rev.chunk_row[c];
         const uint64_t beg = r.rev.chunk_beg[c], end = r.rev.chunk_beg[c + 1];
+        if (k + n_warps < nbig) c_nx = r.rev.big[k + n_warps];
         bool any = false;
         uint32_t uq[4], mq[4], bq[4], fq[4];
 #pragma unroll
