@@ -140,55 +140,142 @@ def make_graph(D, cfgname):
 
 
 # ----------------------------------------------------------------- reference arm
+GOLDEN = os.path.join(ROOT, "tests", "golden", "bench_reports.json")
+
+
+def golden_report(cfgname, devices):
+    """The unmodified reference's report (timings=False) of this workload at
+    `devices`, produced by oracle/make_bench_golden.py; None if not recorded."""
+    try:
+        with open(GOLDEN) as f:
+            return json.load(f)[cfgname]["reports"].get(str(devices))
+    except (OSError, KeyError):
+        return None
+
+
+def strip_timings(rep_json):
+    d = json.loads(rep_json)
+    d.pop("timings", None)
+    return d
+
+
+def parity_of(cfgname, devices, rep_json):
+    """'identical' when the report equals the reference's byte for byte
+    (minus timings), 'DIFFERS' when not, 'no reference report recorded'."""
+    want = golden_report(cfgname, devices)
+    if want is None:
+        return "no reference report recorded"
+    return "identical" if strip_timings(rep_json) == json.loads(want) else "DIFFERS"
+
+
+def reference_graph(cfgname):
+    """The workload graph written by the ORACLE-side synthesizer (oracle/synth.c,
+    byte-identical to the product generator) and loaded by the reference's own
+    load_graph: the reference arm never loads the product library."""
+    import oracle as O
+    gen, a, m, *_ = CONFIGS[cfgname]
+    ref, _ = O.load_reference()
+    if ref is None:
+        return None, None
+    path = f"/tmp/difuser_ref_{cfgname}_{os.getpid()}.bin"
+    t0 = time.time()
+    O.generate_cache(gen, a, m, SEED, path)
+    rg = ref.load_graph(path)
+    os.unlink(path)
+    log(f"[bench] reference graph {cfgname}: n={rg.n} m={rg.m} in {time.time() - t0:.1f}s")
+    return ref, rg
+
+
+def host_cores():
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+
+
 def reference_devices(r):
-    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     d = 1
-    while d * 2 <= min(cores, 64, r):
+    while d * 2 <= min(host_cores(), 64, r):
         d *= 2
     return d
 
 
-def run_reference(D, cfgname, steps, warmup, graph=None):
-    """The reference's own run_json (compiled from /root/reference into
-    oracle/_ref) on host threads; falls back to the plain-C oracle port."""
-    import oracle as O
+def time_reference(ref, rg, cfgname, devices, steps, budget_s):
+    """Full reference run_json(devices) runs (devices host threads, its
+    proj/src/runtime.cpp thread-per-device driver), at most `steps`, stopping
+    once `budget_s` of CPU time is spent (at least one).  Returns (mean s,
+    runs, last report)."""
     gen, a, m, wspec, r, k, desc = CONFIGS[cfgname]
-    g = graph if graph is not None else make_graph(D, cfgname)
-    ref, _ = O.load_reference()
-    devices = reference_devices(r)
-    times = []
-    if ref is not None:
-        path = f"/tmp/difuser_bench_{cfgname}_{os.getpid()}.bin"
-        D.save_cache(g, path)
-        rg = ref.load_graph(path)
-        os.unlink(path)
-        kind = "reference"
-        for i in range(warmup + steps):
-            t0 = time.perf_counter()
-            rep = json.loads(ref.run_json(rg, k=k, r=r, devices=devices, mode="fasst",
-                                          weights=wspec, rebuild_eps=0.01, seed=SEED,
-                                          timings=True))
-            dt = time.perf_counter() - t0
-            if i >= warmup:
-                times.append(dt)
-        inner = rep["timings"]
-    else:
-        import numpy as np
-        kind = "port"
-        devices = 1
-        cg = O.CSR(g.offsets, g.adj, np.array(g.orig_ids, np.uint64))
-        for i in range(warmup + steps):
-            t0 = time.perf_counter()
-            O.run(cg, k=k, r=r, devices=1, weights=wspec, seed=SEED)
-            dt = time.perf_counter() - t0
-            if i >= warmup:
-                times.append(dt)
-        inner = None
-    value = statistics.mean(times)
-    return {"value": value, "unit": "s", "cores": devices, "kind": kind,
-            "sample": f"full {desc} run_json(devices={devices}) x{steps}"
-                      f" (reference timings.total of last step: "
-                      f"{inner['total'] if inner else 'n/a'})"}
+    times, rep = [], None
+    while len(times) < max(1, steps):
+        t0 = time.perf_counter()
+        rep = ref.run_json(rg, k=k, r=r, devices=devices, mode="fasst", weights=wspec,
+                           rebuild_eps=0.01, seed=SEED, timings=False)
+        times.append(time.perf_counter() - t0)
+        if sum(times) + times[-1] > budget_s:
+            break
+    return statistics.mean(times), len(times), rep
+
+
+def cpu_baseline_leg(cfgname, devices):
+    """cpu_baseline of our arm (rank 0, N=1): one run of the unmodified
+    reference on this host at the SAME devices (identical report), plus its
+    all-cores configuration as context."""
+    ref, rg = reference_graph(cfgname)
+    if ref is None:
+        return {"value": None, "unit": "s", "cores": 0, "kind": "unavailable",
+                "sample": "oracle/_ref not built"}
+    v, runs, rep = time_reference(ref, rg, cfgname, devices, 1, 60)
+    out = {"value": round(v, 4), "unit": "s", "cores": devices, "kind": "reference",
+           "sample": f"{runs} full run_json(devices={devices}) of the same workload "
+                     f"(unmodified reference, oracle/_ref), report parity: "
+                     f"{parity_of(cfgname, devices, rep)}"}
+    dall = reference_devices(CONFIGS[cfgname][4])
+    if dall != devices:
+        va, ra, _ = time_reference(ref, rg, cfgname, dall, 1, 30)
+        out["all_cores"] = {"value": round(va, 4), "cores": dall, "devices": dall,
+                            "note": "the reference's fastest setting (one thread per FASST "
+                                    "device); a different mu, hence a different seed set"}
+    return out
+
+
+def run_reference_arm(args, rank, world):
+    """--impl reference: the unmodified reference (oracle/_ref, compiled from
+    /root/reference/proj) through its own pybind run_json on this host's
+    cores, on the SAME workload and devices as our arm (devices = N), each
+    step one full greedy run.  Rank 0 alone works under torchrun."""
+    if rank != 0:
+        return
+    gen, a, m, wspec, r, k, desc = CONFIGS[args.config]
+    devices = world
+    ref, rg = reference_graph(args.config)
+    if ref is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}), flush=True)
+        return
+    # CPU runs need no warm-up; the step count is bounded by a time budget so
+    # that the arm ends within minutes (C2 at devices=1 is ~40 s per run).
+    budget = float(os.environ.get("DFS_REF_BUDGET_S", "150"))
+    value, runs, rep = time_reference(ref, rg, args.config, devices, args.steps, budget)
+    cores = devices
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "s",
+            "n_gpus": args.gpus, "steps": runs, "steps_requested": args.steps, "warmup": 0,
+            "warmup_requested": args.warmup, "ms_per_step": round(value * 1e3, 3),
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "int8",
+            "data": "synthetic (deterministic R-MAT generator, seed 7; oracle/synth.c)",
+            "config": config_of(args.config, rg.n, m, devices, world),
+            "report_parity": parity_of(args.config, devices, rep),
+            "cpu_baseline": {"value": round(value, 6), "unit": "s", "cores": cores,
+                             "kind": "reference",
+                             "sample": f"{runs} full run_json(devices={devices}) runs, "
+                                       f"{host_cores()} host cores available"},
+            "e2e": {"value": round(value, 6), "unit": "s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_of(cfgname, n, m, devices, world):
+    gen, a, _, wspec, r, k, desc = CONFIGS[cfgname]
+    return {"workload": desc, "n": n, "m": m, "r": r, "k": k, "weights": wspec,
+            "devices": devices, "mode": "fasst", "rebuild_eps": 0.01, "seed": SEED,
+            "l2": "flushed between steps (256 MiB write)",
+            "parallelism": f"fasst-sample-space x{world}"}
 
 
 # ----------------------------------------------------------------- our arm
@@ -311,6 +398,8 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     assert json.loads(rep_e2e)["seeds"] == json.loads(rep)["seeds"]
+    # our report vs the unmodified reference's (byte-identical minus timings)
+    parity = parity_of(args.config, devices, rep)
     h2d = 8 * (g.n + 1) + 4 * g.m
     d2h = 64 + 12 * k + 4 * k + devices * 256
 
@@ -412,7 +501,7 @@ def run_ours(args, rank, world, local_rank):
     cpu = None
     if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
         try:
-            cpu = run_reference(D, args.config, steps=1, warmup=0, graph=g)
+            cpu = cpu_baseline_leg(args.config, devices)
         except Exception as ex:  # reported, never fatal
             cpu = {"value": None, "unit": "s", "cores": 0, "kind": "unavailable",
                    "sample": repr(ex)}
@@ -423,10 +512,8 @@ def run_ours(args, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 3),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "int8",
         "data": "synthetic (deterministic R-MAT generator, seed 7)",
-        "config": {"workload": desc, "n": g.n, "m": g.m, "r": r, "k": k, "weights": wspec,
-                   "devices": devices, "mode": "fasst", "rebuild_eps": 0.01, "seed": SEED,
-                   "l2": "flushed between steps (256 MiB write)",
-                   "parallelism": f"fasst-sample-space x{world}"},
+        "config": config_of(args.config, g.n, g.m, devices, world),
+        "report_parity": parity,
         "sketch_edge_updates_per_s": upd_per_s,
         "phases_s": {x: round(last[x], 6) for x in ("build", "fill", "simulate", "select",
                                                     "cascade", "total")},
@@ -459,22 +546,7 @@ def main():
     args = ap.parse_args()
     rank, world, local_rank = env_rank()
     if args.impl == "reference":
-        if rank != 0:
-            return
-        import paper_2410_14047_b200 as D
-        gen, a, m, wspec, r, k, desc = CONFIGS[args.config]
-        res = run_reference(D, args.config, steps=args.steps, warmup=args.warmup)
-        line = {"impl": "reference", "metric": METRIC, "value": round(res["value"], 6),
-                "unit": "s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": round(res["value"] * 1e3, 3), "higher_is_better": False,
-                "scaling": "strong", "vs_baseline": None, "dtype": "int8",
-                "data": "synthetic (deterministic R-MAT generator, seed 7)",
-                "config": {"workload": desc, "r": r, "k": k, "weights": wspec,
-                           "devices": res["cores"], "mode": "fasst"},
-                "cpu_baseline": res,
-                "e2e": {"value": round(res["value"], 6), "unit": "s", "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
+        run_reference_arm(args, rank, world)
         return
     run_ours(args, rank, world, local_rank)
 

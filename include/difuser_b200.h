@@ -71,6 +71,9 @@ typedef struct dfs_stats {
   uint64_t cnt_cas_rows, cnt_cas_edges, cnt_cascades;
   double run_kernel; /* seconds of the whole-loop kernel launch (CUDA events) */
   double item_density; /* live simulations per sampled item (sets the pull switch points) */
+  uint32_t max_sweeps;   /* most simulate sweeps of one convergence */
+  uint32_t rerun_jacobi; /* 1: a convergence came near sim_cap; the run was decided by the
+                            reference's Jacobi schedule (engine.cpp:88-96) */
 } dfs_stats;
 
 const char *dfs_last_error(void);
@@ -150,6 +153,9 @@ int dfs_scores(dfs_ctx *ctx, uint32_t tau, double *out_n);                  /* s
 int dfs_commit_cascade(dfs_ctx *ctx, uint32_t tau, uint32_t seed, uint64_t *visited); /* engine.cpp:106-144 */
 int dfs_visited_count(dfs_ctx *ctx, uint32_t tau, uint64_t *out);          /* sketch.cpp:139 */
 int dfs_get_registers(dfs_ctx *ctx, uint32_t tau, int8_t *out_nJ);
+/* VISITED bitset of partition tau in the reference layout (SketchMatrix::vis_row,
+ * sketch.hpp:35-87): n rows of ceil(J/64) u64 words, bit j = register j VISITED. */
+int dfs_get_visited(dfs_ctx *ctx, uint32_t tau, uint64_t *out_words);
 int dfs_set_registers(dfs_ctx *ctx, uint32_t tau, const int8_t *in_nJ);
 /* {updates, items, edges, batches, touched, sweeps, convergences, visited} */
 int dfs_rank_counters(dfs_ctx *ctx, uint32_t tau, uint64_t out[8]);

@@ -77,6 +77,9 @@ def lib():
         L.dor_commit_cascade.restype = C.c_uint64
         L.dor_commit_cascade.argtypes = [C.c_uint32, _u64p, _u32p, _u64p, C.c_uint32,
                                          _i8p, _u64p, C.c_uint32]
+        L.dor_generate_cache.restype = C.c_int
+        L.dor_generate_cache.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_char_p,
+                                         C.POINTER(C.c_uint32)]
         L.dor_fasst_stats.restype = None
         L.dor_fasst_stats.argtypes = [C.c_uint64, _u32p, _u32p, _u32p, _u32p, C.c_uint32,
                                       C.c_uint32, _u64p, _u64p, C.POINTER(C.c_uint64),
@@ -208,6 +211,18 @@ def edge_hash_np(u, v):
         h2 = _np_fmix64(h2)
         h1 = h1 + h2
     return (h1 & np.uint64(0x7FFFFFFF)).astype(np.uint32)
+
+
+def generate_cache(kind, a, m, seed, path):
+    """Write the deterministic R-MAT ("rmat", a = scale) / ER ("er", a = n)
+    graph as a DFSG0001 cache the reference's load_graph reads (synth.c);
+    returns n.  Same graph as the product's generate(kind, a, m, seed)."""
+    n = C.c_uint32(0)
+    rc = lib().dor_generate_cache({"rmat": 0, "er": 1}[kind], a, m, seed, path.encode(),
+                                  C.byref(n))
+    if rc:
+        raise RuntimeError(f"generate_cache failed ({rc})")
+    return n.value
 
 
 def er_edges(n, m, seed):

@@ -84,6 +84,12 @@ int dor_run(uint32_t n, uint64_t m, const uint64_t *offsets,
             uint32_t *rebuild_rounds, uint32_t *n_rebuilds, int *saturated,
             int *degraded, uint64_t counters[3]);
 
+/* ---- synthetic inputs (synth.c): DFSG0001 cache of the deterministic R-MAT
+ * (kind 0, a = scale) / ER (kind 1, a = n) graph the product's generator
+ * builds, for the reference arm.  Returns 0 or a negative code. */
+int dor_generate_cache(int kind, uint64_t a, uint64_t m, uint64_t seed, const char *path,
+                       uint32_t *n_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -12,7 +12,10 @@
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
 
+#include <algorithm>
+#include <bit>
 #include <cstring>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -160,6 +163,111 @@ PYBIND11_MODULE(_refprobe, mod) {
       },
       py::arg("offsets"), py::arg("adj"), py::arg("weights"), py::arg("r"), py::arg("mu"),
       py::arg("mode"), py::arg("seed"));
+
+  // Reference-schedule work units of a whole devices=1 run,
+  // the numerator of bench.py's roofline: the reference's own stages
+  // (build_device_graph fasst.cpp:50-88, fill_sketches sketch.cpp:55-66,
+  // simulate_iteration engine.cpp:57-86, commit_seed/cascade engine.cpp:106-144)
+  // driven with the seeds and rebuild rounds of the reference's report; the
+  // counters are read off the reference's own state between its calls:
+  //   per sweep  E = edges whose source changed in the previous sweep
+  //              (changed_prev, engine.cpp:70), B = their non-zero 32-sim
+  //              mask halves, L = their live bits, T = distinct (row, batch)
+  //              pairs among them;  S = sweeps (simulate_to_convergence's count)
+  //   cascades   F = frontier rows summed over levels, Ec = their device-graph
+  //              out-edges, C = cascades started (frontier non-empty after
+  //              commit_seed).  The level loop below mirrors engine.cpp:120-144
+  //              on copies and is checked against the reference's cascade().
+  mod.def(
+      "run_units",
+      [](const std::vector<uint64_t>& offsets, const std::vector<uint32_t>& adj,
+         const std::vector<uint32_t>& weights, uint32_t r, uint64_t seed,
+         const std::vector<uint32_t>& seeds, const std::vector<uint32_t>& rebuild_rounds) {
+        WeightedGraph g = make_graph(offsets, adj, weights);
+        PartitionPlan plan = make_plan(
+            gen_random_vector(r, derive_seed(seed, kSeedTagSamples)), 1, PartitionMode::Fasst);
+        DeviceGraph dg = build_device_graph(g, plan, 0);
+        SketchMatrix m(g.n, plan.chunk, 0, derive_seed(seed, kSeedTagRegisters));
+        const uint32_t words = dg.mask_words, halves = (plan.chunk + 31) / 32;
+        uint64_t E = 0, B = 0, L = 0, T = 0, S = 0, conv = 0, F = 0, Ec = 0, Cn = 0;
+        std::vector<uint8_t> touched(size_t(g.n) * halves);
+        auto simulate = [&]() {
+          SimulateBuffers buf;
+          buf.reset(m);
+          for (int it = 1; it <= 256; ++it) {
+            std::fill(touched.begin(), touched.end(), 0);
+            for (vertex_t u = 0; u < dg.n; ++u)
+              for (uint64_t e = dg.offsets[u]; e < dg.offsets[u + 1]; ++e) {
+                if (!buf.changed_prev[dg.adj[e]]) continue;
+                ++E;
+                const uint64_t* em = dg.edge_mask(e);
+                for (uint32_t h = 0; h < halves; ++h) {
+                  const uint32_t bits = uint32_t(em[h / 2] >> (32 * (h & 1)));
+                  if (!bits) continue;
+                  ++B;
+                  L += std::popcount(bits);
+                  uint8_t& t = touched[size_t(u) * halves + h];
+                  if (!t) {
+                    t = 1;
+                    ++T;
+                  }
+                }
+              }
+            ++S;
+            if (!simulate_iteration(dg, m, buf)) break;
+          }
+          ++conv;
+        };
+        fill_sketches(m);
+        simulate();
+        CascadeState cs;
+        cs.init(g.n, m.words());
+        for (uint32_t step = 0; step < seeds.size(); ++step) {
+          commit_seed(m, cs, seeds[step]);
+          // counting replica of the level loop on copies of the state
+          SketchMatrix m2 = m;
+          CascadeState c2 = cs;
+          if (!c2.q.empty()) ++Cn;
+          while (!c2.q.empty()) {
+            for (vertex_t u : c2.q.items) {
+              ++F;
+              Ec += dg.offsets[u + 1] - dg.offsets[u];
+              const uint64_t* fu = c2.fresh_row(c2.fresh_cur, u);
+              for (uint64_t e = dg.offsets[u]; e < dg.offsets[u + 1]; ++e) {
+                const vertex_t v = dg.adj[e];
+                const uint64_t* em = dg.edge_mask(e);
+                for (uint32_t w = 0; w < c2.words; ++w) {
+                  const uint64_t cand = fu[w] & em[w] & ~m2.vis_row(v)[w];
+                  if (!cand) continue;
+                  m2.mark_visited_word(v, w, cand);
+                  c2.fresh_row(c2.fresh_next, v)[w] |= cand;
+                  c2.q_next.push(v);
+                }
+              }
+            }
+            for (vertex_t u : c2.q.items) std::memset(c2.fresh_row(c2.fresh_cur, u), 0, c2.words * 8);
+            c2.q.clear();
+            std::swap(c2.q.items, c2.q_next.items);
+            std::swap(c2.q.member, c2.q_next.member);
+            std::swap(c2.fresh_cur, c2.fresh_next);
+          }
+          cascade(dg, m, cs);  // the reference's own cascade advances the real state
+          if (count_visited(m) != count_visited(m2) ||
+              std::memcmp(m.row(0), m2.row(0), size_t(g.n) * m.j_local()) != 0)
+            throw std::runtime_error("run_units: counting replica diverged from cascade()");
+          if (std::find(rebuild_rounds.begin(), rebuild_rounds.end(), step) != rebuild_rounds.end()) {
+            fill_sketches(m);
+            simulate();
+          }
+        }
+        (void)words;
+        py::dict d;
+        d["E"] = E; d["B"] = B; d["T"] = T; d["L"] = L; d["S"] = S; d["convergences"] = conv;
+        d["cascade_rows"] = F; d["cascade_edges"] = Ec; d["cascades"] = Cn;
+        return d;
+      },
+      py::arg("offsets"), py::arg("adj"), py::arg("weights"), py::arg("r"), py::arg("seed"),
+      py::arg("seeds"), py::arg("rebuild_rounds"));
 
   mod.def("fmix64", [](uint64_t k) { return fmix64(k); });
   mod.def("splitmix64_at", [](uint64_t s, uint64_t i) { return splitmix64_at(s, i); });

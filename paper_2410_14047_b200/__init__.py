@@ -156,10 +156,33 @@ def _config(k, r, devices, mode, weights, rebuild_eps, seed, sim_cap=256, jacobi
                   sim_cap, jacobi, count)
 
 
+def _serialized(cls):
+    """Every public method of a Context holds the context's lock: the library
+    is loaded with ctypes.CDLL, which releases the GIL, and a context (its
+    arena, partitions, stream, last report) is not re-entrant
+    (include/difuser_b200.h).  The reference's run_json is a pure function
+    under the GIL, so concurrent callers must not race here either."""
+    import functools
+    for name, fn in list(vars(cls).items()):
+        if name.startswith("_") or not callable(fn):
+            continue
+
+        def wrap(f):
+            @functools.wraps(f)
+            def locked(self, *a, **kw):
+                with self._lock:
+                    return f(self, *a, **kw)
+            return locked
+        setattr(cls, name, wrap(fn))
+    return cls
+
+
+@_serialized
 class Context:
     """One CUDA device: resident graph, prepared partitions, stage entry points."""
 
     def __init__(self, device: int = 0):
+        self._lock = threading.RLock()
         h = C.c_void_p()
         check(lib().dfs_ctx_create(device, C.byref(h)))
         self._h = h
@@ -269,6 +292,13 @@ class Context:
         out = np.zeros(max(self._graph.n * self._J, 1), np.int8)
         check(lib().dfs_get_registers(self._h, tau, out.ctypes.data))
         return out[: self._graph.n * self._J]
+
+    def visited(self, tau: int) -> np.ndarray:
+        """VISITED bitset, reference layout: n rows of ceil(J/64) u64 words."""
+        words = (self._J + 63) // 64
+        out = np.zeros(max(self._graph.n * words, 1), np.uint64)
+        check(lib().dfs_get_visited(self._h, tau, out.ctypes.data))
+        return out[: self._graph.n * words]
 
     def set_registers(self, tau: int, regs) -> None:
         regs = np.ascontiguousarray(regs, np.int8)

@@ -21,7 +21,7 @@ SYMBOLS = [
     "dfs_ctx_create", "dfs_ctx_destroy", "dfs_upload", "dfs_run_json", "dfs_run_resident_json",
     "dfs_last_stats", "dfs_prepare", "dfs_plan", "dfs_device_graph_size", "dfs_device_graph",
     "dfs_fill", "dfs_simulate", "dfs_scores", "dfs_commit_cascade", "dfs_visited_count",
-    "dfs_get_registers", "dfs_set_registers", "dfs_influence", "dfs_greedy_exact",
+    "dfs_get_registers", "dfs_get_visited", "dfs_set_registers", "dfs_influence", "dfs_greedy_exact",
     "dfs_ctx_stream", "dfs_graph_pin", "dfs_rank_counters", "dfs_prepare_partition",
     "dfs_scores_device", "dfs_rebuild", "dfs_format_report", "dfs_peer_export", "dfs_peer_open",
     "dfs_peer_link", "dfs_peer_run_json", "dfs_fasst_stats", "dfs_mc_influence",
@@ -47,7 +47,8 @@ class Stats(C.Structure):
                [("sim_active", C.c_double), ("sim_launches", C.c_uint32), ("n", C.c_uint32),
                 ("m", C.c_uint64), ("cnt_cas_rows", C.c_uint64), ("cnt_cas_edges", C.c_uint64),
                 ("cnt_cascades", C.c_uint64), ("run_kernel", C.c_double),
-                ("item_density", C.c_double)]
+                ("item_density", C.c_double), ("max_sweeps", C.c_uint32),
+                ("rerun_jacobi", C.c_uint32)]
 
 
 class ReportFields(C.Structure):
@@ -114,6 +115,7 @@ def lib():
         "dfs_commit_cascade": (i32, [vp, u32, u32, C.POINTER(u64)]),
         "dfs_visited_count": (i32, [vp, u32, C.POINTER(u64)]),
         "dfs_get_registers": (i32, [vp, u32, vp]),
+        "dfs_get_visited": (i32, [vp, u32, vp]),
         "dfs_set_registers": (i32, [vp, u32, vp]),
         "dfs_influence": (i32, [vp, vp, u32, u32, u64, u32, C.c_char_p, C.POINTER(C.c_double),
                                 C.POINTER(C.c_double)]),

@@ -278,6 +278,8 @@ int dfs_last_stats(const dfs_ctx* ctx, dfs_stats* out) {
     out->cnt_cascades = r.cnt_cascades;
     out->run_kernel = r.run_kernel;
     out->item_density = r.item_density;
+    out->max_sweeps = r.max_sweeps;
+    out->rerun_jacobi = r.rerun_jacobi ? 1u : 0u;
   });
 }
 
@@ -467,6 +469,13 @@ int dfs_get_registers(dfs_ctx* ctx, uint32_t tau, int8_t* out_nJ) {
     need(ctx, "ctx");
     need(out_nJ, "out");
     ctx->c->stage_get_registers(tau, out_nJ);
+  });
+}
+int dfs_get_visited(dfs_ctx* ctx, uint32_t tau, uint64_t* out_words) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(out_words, "out");
+    ctx->c->stage_get_visited(tau, out_words);
   });
 }
 int dfs_set_registers(dfs_ctx* ctx, uint32_t tau, const int8_t* in_nJ) {

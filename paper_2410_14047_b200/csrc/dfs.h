@@ -93,7 +93,8 @@ struct RankCtl {
   unsigned int levels;          // cascade levels (last)
   int error;                    // 1 = simulate cap exceeded
   unsigned int dirty_count;     // rows to rescore
-  unsigned int pad[6];
+  unsigned int max_sweeps;      // most sweeps one convergence took (async sim_cap check)
+  unsigned int pad[5];
   // reference-schedule work counters (count mode):
   // E edges processed, B live 32-sim batches, T touched (row, batch) pairs
   unsigned long long cnt_edges, cnt_batches, cnt_touched, cnt_sweeps, cnt_convergences;

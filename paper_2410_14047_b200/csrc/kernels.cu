@@ -1583,6 +1583,7 @@ __device__ __forceinline__ uint32_t simulate_body(const RankDev& r, const SimOpt
   if (gwarp == 0 && lane == 0) {
     const uint32_t sw = err ? s : s - 1;
     r.ctl->sweeps = sw;
+    r.ctl->max_sweeps = max(r.ctl->max_sweeps, sw);
     r.ctl->total_sweeps += sw;
     r.ctl->cnt_sweeps += sw;
     r.ctl->cnt_convergences += 1;
@@ -2386,7 +2387,8 @@ __device__ __forceinline__ T ld_relaxed_sys(const T* p) {
 // process) releases the wait after pv.timeout_ns (DFS_PEER_TIMEOUT_S) and is
 // reported by the host; once that happened, later barriers of the launch do
 // not wait any more (the results are discarded anyway).
-__device__ __noinline__ void peer_sync(const PeerView& pv, unsigned long long ep) {
+__device__ __noinline__ void peer_sync(const PeerView& pv, unsigned long long ep,
+                                      unsigned long long timeouts0) {
   cg::grid_group grid = cg::this_grid();
   __threadfence_system();
   grid.sync();
@@ -2394,7 +2396,9 @@ __device__ __noinline__ void peer_sync(const PeerView& pv, unsigned long long ep
     const unsigned lane = threadIdx.x;
     PeerBox* mine = pv.box[pv.rank];
     if (lane == 0) st_release_sys(&mine->arrive, ep);
-    const bool failed = ld_volatile(&mine->timeouts) != 0;
+    // a barrier of THIS launch already timed out (timeouts0: the count when
+    // the launch started): stop waiting, the host discards the results
+    const bool failed = ld_volatile(&mine->timeouts) != timeouts0;
     if (!failed && lane < pv.world && lane != pv.rank) {
       const unsigned long long t0 = global_ns();
       while (ld_acquire_sys(&pv.box[lane]->arrive) < ep) {
@@ -2518,6 +2522,7 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
   bool rebuilt = true;
   // peer mode: this rank reduces and searches the id slice [plo, phi)
   unsigned long long ep = a.peer ? ld_volatile(&a.pv.box[a.pv.rank]->arrive) : 0;
+  const unsigned long long to0 = a.peer ? ld_volatile(&a.pv.box[a.pv.rank]->timeouts) : 0;
   const uint32_t pslice = a.peer ? (a.n + a.pv.world - 1) / a.pv.world : 0;
   const uint32_t plo = a.peer ? min(a.n, a.pv.rank * pslice) : 0;
   const uint32_t phi = a.peer ? min(a.n, plo + pslice) : 0;
@@ -2622,7 +2627,7 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
       if (blockIdx.x == 0 && threadIdx.x == 0)
         a.pv.box[a.pv.rank]->ndirty =
             rebuilt ? kAllDirty : ld_volatile(&a.ranks[0].ctl->dirty_count);
-      peer_sync(a.pv, ++ep);
+      peer_sync(a.pv, ++ep, to0);
       const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
       const uint64_t gthreads = uint64_t(gridDim.x) * blockDim.x;
       const uint64_t gw = gtid >> 5, nw = gthreads >> 5;
@@ -2665,7 +2670,7 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
           mine->minu = t.minu;
         }
       }
-      peer_sync(a.pv, ++ep);
+      peer_sync(a.pv, ++ep, to0);
       if (blockIdx.x == 0 && threadIdx.x == 0) {
         Best t{0.0, 0xFFFFFFFFu, 0xFFFFFFFFu};
         for (uint32_t q = 0; q < a.pv.world; ++q) {  // ascending id slices
@@ -2697,7 +2702,7 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
     if (a.peer) {  // allreduce(count_visited) (runtime.cpp:129, collectives.cpp:96-113)
       if (blockIdx.x == 0 && threadIdx.x == 0)
         a.pv.box[a.pv.rank]->visited = ld_volatile(&a.ranks[0].ctl->visited);
-      peer_sync(a.pv, ++ep);
+      peer_sync(a.pv, ++ep, to0);
       if (blockIdx.x == 0 && threadIdx.x == 0) {
         unsigned long long covered = 0;
         for (uint32_t q = 0; q < a.pv.world; ++q) covered += ld_relaxed_sys(&a.pv.box[q]->visited);

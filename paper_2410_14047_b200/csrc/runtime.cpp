@@ -346,7 +346,11 @@ void Context::prepare(const RunConfig& cfg, const HostGraph* host_w_src, uint32_
   }
   // Cached first fill per partition (rebuild fills become a copy), only while
   // HBM allows once every partition's working set is allocated.
+  // DFS_NO_PRISTINE=1 forces the re-hashing fill (tests of the HBM-pressure path).
+  const char* np_env = getenv("DFS_NO_PRISTINE");
+  const bool no_pristine = np_env && atoi(np_env) != 0;
   for (RankDev& r : ranks_) {
+    if (no_pristine) break;
     const size_t bytes = std::max<size_t>(r.n, 1) * r.Jp;
     const std::string name = "r" + std::to_string(r.tau) + ".pristine";
     bool take = arena_.has(name, bytes);
@@ -423,7 +427,23 @@ void Context::plan_weights(const RunConfig& cfg, const HostGraph* host_w_src) {
 }
 
 Report Context::run(const RunConfig& cfg, const HostGraph* host_w_src) {
-  return run_impl(cfg, host_w_src, false);
+  Report rep = run_impl(cfg, host_w_src, false);
+  // sim_cap contract (engine.cpp:88-96): the reference throws when a Jacobi
+  // convergence needs more than cap sweeps.  The async schedule needs at most
+  // as many sweeps as Jacobi, so exceeding the cap there already throws; a
+  // convergence that came within a factor 2 of the cap is decided exactly by
+  // re-running with the reference's Jacobi schedule (same report or the
+  // reference's runtime_error).  Deep sample graphs only: C2 takes <= 20
+  // sweeps per convergence.
+  if (!cfg.jacobi && 2 * uint64_t(rep.max_sweeps) >= uint64_t(cfg.sim_cap)) {
+    RunConfig exact = cfg;
+    exact.jacobi = 1;
+    Report jr = run_impl(exact, host_w_src, false);
+    jr.config.jacobi = cfg.jacobi;
+    jr.rerun_jacobi = true;
+    return jr;
+  }
+  return rep;
 }
 
 std::vector<uint32_t> Context::mc_influence(const std::vector<uint32_t>& seeds, uint32_t trials,
@@ -659,9 +679,11 @@ Report Context::run_impl(const RunConfig& cfg, const HostGraph* host_w_src, bool
     PeerBox b{};
     DFS_CUDA(cudaMemcpy(&b, peer_.box, sizeof b, cudaMemcpyDeviceToHost));
     if (b.timeouts != peer_.timeouts_seen) {
-      peer_.timeouts_seen = b.timeouts;
+      // the ranks' barrier epochs have drifted apart: the mapping is unusable
+      // until every rank redoes the setup (export/open zero the mailboxes)
+      peer_close();
       throw Error(kRuntime, "peer mode: a peer did not reach a round barrier in time "
-                            "(peer process failed?); results are invalid");
+                            "(peer process failed?); results are invalid; redo the peer setup");
     }
   }
   if (getenv("DFS_DBG") && (atoi(getenv("DFS_DBG")) & 4)) dump_trace();
@@ -695,6 +717,7 @@ Report Context::run_impl(const RunConfig& cfg, const HostGraph* host_w_src, bool
     rep.sketch_edge_updates += c.updates;
     rep.items_processed += c.items_processed;
     rep.sweeps_total += c.total_sweeps;
+    rep.max_sweeps = std::max(rep.max_sweeps, c.max_sweeps);
     rep.items_fwd += ranks_[t].fwd.count;
     rep.items_rev += ranks_[t].rev.count;
     rep.cnt_edges += c.cnt_edges;
@@ -996,6 +1019,24 @@ void Context::stage_get_registers(uint32_t tau, int8_t* out) {
   if (!r.n) return;
   DFS_CUDA(cudaMemcpy2DAsync(out, r.J, r.regs, r.Jp, r.J, r.n, cudaMemcpyDeviceToHost, stream_));
   sync();
+}
+
+// VISITED bitset in the reference layout (sketch.hpp:35-87): per row ceil(J/64)
+// u64 words; the device mirror holds W32 = Jp/32 u32 words per row (pads 0).
+void Context::stage_get_visited(uint32_t tau, uint64_t* out) {
+  check_tau(tau, ranks_.size());
+  const RankDev& r = ranks_[tau];
+  if (!r.n) return;
+  std::vector<uint32_t> v(size_t(r.n) * r.W32);
+  DFS_CUDA(cudaMemcpyAsync(v.data(), r.vis, v.size() * 4, cudaMemcpyDeviceToHost, stream_));
+  sync();
+  const uint32_t words = (r.J + 63) / 64;
+  for (size_t u = 0; u < r.n; ++u)
+    for (uint32_t w = 0; w < words; ++w) {
+      const uint64_t lo = v[u * r.W32 + 2 * w];
+      const uint64_t hi = 2 * w + 1 < r.W32 ? v[u * r.W32 + 2 * w + 1] : 0;
+      out[u * words + w] = lo | (hi << 32);
+    }
 }
 
 void Context::stage_set_registers(uint32_t tau, const int8_t* in) {

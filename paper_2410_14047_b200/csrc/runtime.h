@@ -85,6 +85,8 @@ struct Report {  // runtime.hpp:29-41
   uint64_t launches = 0;        // kernels launched by run()
   double sim_active = 0;        // seconds of simulate launches that ran (not gated off)
   uint32_t sim_launches = 0;    // simulate launches that ran
+  uint32_t max_sweeps = 0;      // most sweeps of one convergence (any partition)
+  bool rerun_jacobi = false;    // decided by a Jacobi re-run (near sim_cap)
 };
 
 std::string report_to_json(const Report& rep, bool include_timings);
@@ -135,6 +137,7 @@ class Context {
   // Multi-process round pieces (device pointers; no host round-trip).
   void stage_scores_device(uint32_t tau, int full, double* dst);
   void stage_rebuild(uint32_t tau);
+  void stage_get_visited(uint32_t tau, uint64_t* out);
   void stage_get_registers(uint32_t tau, int8_t* out);
   void stage_set_registers(uint32_t tau, const int8_t* in);
   void stage_device_graph(uint32_t tau, std::vector<uint64_t>& off, std::vector<uint32_t>& adj,

@@ -207,9 +207,14 @@ class PeerRunner:
         if self._key != (self.g.n, self.g.m, r, mode):
             self.setup(k=k, r=r, mode=mode, weights=weights, rebuild_eps=rebuild_eps, seed=seed,
                        resident=True)
-        return self.ctx.run_peer_json(None if resident else self.g, k=k, r=r, devices=self.world,
-                                      mode=mode, weights=weights, rebuild_eps=rebuild_eps,
-                                      seed=seed, timings=timings, resident=resident)
+        try:
+            return self.ctx.run_peer_json(None if resident else self.g, k=k, r=r,
+                                          devices=self.world, mode=mode, weights=weights,
+                                          rebuild_eps=rebuild_eps, seed=seed, timings=timings,
+                                          resident=resident)
+        except RuntimeError:
+            self._key = None  # a failed peer run invalidates the mapping: set up again next time
+            raise
 
 
 __all__ = ["binomial_sum", "select_seed", "allreduce_count", "DistRunner", "PeerRunner", "_capi"]

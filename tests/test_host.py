@@ -166,3 +166,26 @@ def test_no_gpu_fails_loudly():
         D.Context(0)
     with pytest.raises(RuntimeError):
         D.run(D.graph_from_text("0 1\n"), k=1, r=64)
+
+
+@pytest.mark.parametrize("kind,a,m", [("rmat", 12, 40000), ("rmat", 16, 400000), ("er", 5000, 20000)])
+def test_oracle_synthesizer_matches_product_generator(tmp_path, kind, a, m):
+    """bench.py's reference arm builds its graph with the oracle-side
+    synthesizer (oracle/synth.c) so that it never loads the product library:
+    the cache must be byte-identical to save_cache(generate(...))."""
+    po, pp = str(tmp_path / "o.bin"), str(tmp_path / "p.bin")
+    n = O.generate_cache(kind, a, m, 7, po)
+    g = D.generate(kind, a, m, 7)
+    D.save_cache(g, pp)
+    assert n == g.n
+    assert open(po, "rb").read() == open(pp, "rb").read()
+
+
+def test_bench_reference_reports_recorded():
+    """The reference reports bench.py checks its own report against exist for
+    the headline workload at every GPU count of the scaling run."""
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "bench_reports.json")))
+    assert set(gold["c2"]["reports"]) >= {"1", "2", "4", "8"}
+    for d, rep in gold["c2"]["reports"].items():
+        r = json.loads(rep)
+        assert r["config"]["devices"] == int(d) and len(r["seeds"]) == 50
