@@ -34,6 +34,9 @@ void cuda_check(cudaError_t e, const char* what);
 constexpr uint32_t kBatch = 32;
 // Items per work chunk: a warp owns one chunk (4 passes of 32 lanes).
 constexpr uint32_t kChunk = 128;
+// Items::big entries carry this flag when the chunk is its row's only chunk
+// (the processing warp owns the row: plain stores instead of CAS).
+constexpr uint32_t kBigOwner = 0x80000000u;
 
 // ---------------------------------------------------------------- device views
 // Full weighted graph, resident for the context (CSR by source u, plus its
@@ -70,7 +73,7 @@ struct Items {
   // chunk ids split by row size: rows with <= kSmallRow items (one chunk,
   // processed item-parallel) and larger rows (processed warp-per-chunk pull)
   uint32_t* small = nullptr;
-  uint32_t* big = nullptr;
+  uint32_t* big = nullptr;    // chunk id | kBigOwner
   uint32_t nsmall = 0, nbig = 0;
   // flat list of the item indices of small rows (flat full passes)
   uint32_t* small_items = nullptr;
@@ -242,6 +245,22 @@ void launch_mc_influence(const DevGraph& g, const uint32_t* w, uint64_t base, ui
 void launch_fasst_stats(const DevGraph& g, const uint32_t* w, const uint32_t* x,
                         const uint32_t* xlut, uint32_t R, uint32_t mu, int sorted, int fill,
                         unsigned long long* out, cudaStream_t s);
+// One-pass sampled-item build of one direction (count + scan + write in one
+// launch with a decoupled look-back; writes it.row_off too).  wconst != 0:
+// every edge has that fixed-point weight (w/tw unused).  Items beyond `cap`
+// are dropped (the host re-runs with the exact total, meta[0]); meta[1] +=
+// live (item, simulation) pairs.  tile_state: items_tiles(m) zeroed words,
+// tile_ctr zeroed.
+uint64_t items_tiles(uint64_t npos);
+void launch_items_onepass(const DevGraph& g, const uint32_t* w, const uint32_t* tw,
+                          uint32_t wconst, const RankDev& r, int dir, int fasst, Items& it,
+                          uint64_t cap, unsigned long long* tile_state, unsigned int* tile_ctr,
+                          unsigned long long* meta, cudaStream_t s);
+// meta[0] += items of every stride-th forward position (capacity estimate).
+void launch_items_sample(const DevGraph& g, const uint32_t* w, uint32_t wconst, const RankDev& r,
+                         int fasst, uint64_t stride, unsigned long long* meta, cudaStream_t s);
+// row_cnt[r] = chunks of row r (from it.row_off).
+void launch_row_chunks(uint32_t n, const Items& it, uint32_t* row_cnt, cudaStream_t s);
 // row_off[r] = pos_off[graph row start]; then per-row chunk counts.
 void launch_row_offsets(const DevGraph& g, int dir, const uint64_t* pos_off, Items& it,
                         uint32_t* row_cnt, cudaStream_t s);

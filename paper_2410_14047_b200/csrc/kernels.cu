@@ -269,6 +269,249 @@ __global__ void k_items(uint64_t npos, const uint32_t* __restrict__ p_hash,
   }
 }
 
+// ---- one-pass item build (count, scan and write in a single launch) --------
+// Positions are processed in tiles of kTileThreads x kPosPerThread consecutive
+// positions.  A thread evaluates the sampling windows of its 8 positions once
+// and keeps the masks of the first two batches of each window in registers
+// (IC windows rarely cover more); the block scans the per-thread item counts,
+// obtains the tile's global item offset by a decoupled look-back over the
+// tile status words, and writes the items in position order (= the order of
+// the count/scan/write formulation, fasst.cpp:50-88 CSR order).  The first
+// position of every row also writes that row's item offset (row_off), so no
+// per-position count or offset array exists.  Windows spanning more than two
+// batches are re-evaluated in the write phase.
+constexpr int kTileThreads = 256;
+constexpr int kPosPerThread = 8;
+constexpr uint32_t kTilePos = kTileThreads * kPosPerThread;
+constexpr unsigned long long kStAgg = 1ull << 62, kStInc = 2ull << 62,
+                             kStVal = (1ull << 62) - 1;
+
+// Mask of batch b of an edge's window (the live-half bit range plus tested
+// slots; sampling.hpp:37-39).
+__device__ __forceinline__ uint32_t window_batch_mask(const uint32_t* sx, uint32_t h, uint32_t W,
+                                                      uint32_t lo, uint32_t hi, uint32_t alo,
+                                                      uint32_t ahi, uint32_t b) {
+  const uint32_t bb = b * 32;
+  const uint32_t i0 = max(lo, bb), i1 = min(hi, bb + 32);
+  const uint32_t a0 = max(alo, i0), a1 = min(ahi, i1);
+  uint32_t mk = 0;
+  if (a1 > a0) mk = (a1 - a0 == 32 ? 0xFFFFFFFFu : ((1u << (a1 - a0)) - 1u)) << (a0 - bb);
+  const uint32_t t0 = alo == lo ? max(i0, ahi) : i0;
+  const uint32_t t1 = alo == lo ? i1 : min(i1, alo);
+  for (uint32_t g = t0 & ~3u; g < t1; g += 4) {
+    const uint4 xv = *reinterpret_cast<const uint4*>(sx + g);
+    const uint32_t m4 = uint32_t((xv.x ^ h) < W) | (uint32_t((xv.y ^ h) < W) << 1) |
+                        (uint32_t((xv.z ^ h) < W) << 2) | (uint32_t((xv.w ^ h) < W) << 3);
+    mk |= m4 << (g - bb);
+  }
+  return mk;
+}
+
+struct ItemsPass {
+  uint64_t npos;
+  uint32_t n;                // rows (row_off has n+1 entries)
+  const uint32_t* p_hash;
+  const uint32_t* p_w;       // nullptr: constant weight Wc
+  uint32_t Wc;
+  const uint32_t* p_other;
+  const uint32_t* p_row;
+  const uint32_t* x;
+  const uint32_t* glut;
+  uint32_t J, Jp;
+  int fasst;
+  uint64_t cap;              // item capacity (writes beyond it are dropped; host re-runs)
+  uint32_t* it_other;
+  uint32_t* it_mask;
+  uint8_t* it_batch;
+  uint32_t* it_row;
+  uint64_t* row_off;
+  unsigned long long* tile_state;  // per tile: flag (2 bits) | value
+  unsigned int* tile_ctr;          // dynamic tile ids (look-back forward progress)
+  unsigned long long* meta;        // [0] total items, [1] live (item, sim) pairs
+};
+
+__global__ void __launch_bounds__(kTileThreads, 2) k_items_onepass(ItemsPass a) {
+  extern __shared__ __align__(16) uint32_t sx[];
+  uint32_t* lut = sx + a.Jp;
+  using BlockScan = cub::BlockScan<uint32_t, kTileThreads>;
+  using BlockExch = cub::BlockExchange<uint32_t, kTileThreads, kPosPerThread>;
+  __shared__ union {
+    typename BlockScan::TempStorage scan;
+    typename BlockExch::TempStorage exch;
+  } tmp;
+  __shared__ unsigned long long s_prefix;
+  __shared__ unsigned int s_tile;
+  for (uint32_t i = threadIdx.x; i < a.Jp; i += blockDim.x) sx[i] = a.x[i];
+  if (a.fasst)
+    for (uint32_t k = threadIdx.x; k <= (1u << kLutBits); k += blockDim.x) lut[k] = a.glut[k];
+  const uint64_t ntiles = (a.npos + kTilePos - 1) / kTilePos;
+  // persistent blocks take tiles in order (a tile's look-back waits only on
+  // tiles already held by running blocks)
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_ctr, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= ntiles) break;
+    // striped positions: step i covers kTileThreads consecutive positions
+    // (coalesced loads, and consecutive lanes write consecutive items)
+    const uint64_t pbase = uint64_t(tile) * kTilePos + threadIdx.x;
+    // ---- phase 1: windows, counts, masks of the first two batches
+    uint32_t mA[kPosPerThread], mB[kPosPerThread], info[kPosPerThread];  // b0 << 24 | nb << 16 | count
+    uint32_t cnt[kPosPerThread];
+    uint32_t live = 0;
+    // every position's hash and weight in flight together
+    uint32_t hv[kPosPerThread], wv[kPosPerThread];
+#pragma unroll
+    for (int i = 0; i < kPosPerThread; ++i) {
+      const uint64_t p = pbase + uint64_t(i) * kTileThreads;
+      const bool ok = p < a.npos;
+      wv[i] = ok ? (a.p_w ? __ldcs(a.p_w + p) : a.Wc) : 0u;
+      hv[i] = ok ? __ldcs(a.p_hash + p) : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < kPosPerThread; ++i) {
+      mA[i] = mB[i] = 0;
+      info[i] = 0;
+      cnt[i] = 0;
+      const uint32_t W = wv[i], h = hv[i];
+      if (W == 0) continue;  // fasst.cpp:71 (and past the end)
+      uint32_t lo, hi, alo, ahi;
+      edge_window(sx, lut, a.J, h, W, a.fasst, lo, hi, alo, ahi);
+      if (hi <= lo) continue;
+      const uint32_t b0 = lo >> 5, b1 = (hi - 1) >> 5, nb = b1 - b0 + 1;
+      uint32_t c = 0;
+      for (uint32_t b = b0; b <= b1; ++b) {
+        const uint32_t mk = window_batch_mask(sx, h, W, lo, hi, alo, ahi, b);
+        if (b == b0) mA[i] = mk;
+        else if (b == b0 + 1) mB[i] = mk;
+        c += mk != 0;
+        live += __popc(mk);
+      }
+      info[i] = (b0 << 24) | (min(nb, 255u) << 16) | c;
+      cnt[i] = c;
+    }
+    // phase-2 inputs of all 8 positions (rows, previous rows, other endpoints)
+    // in flight while the tile offset is resolved
+    uint32_t rowv[kPosPerThread], prevv[kPosPerThread], othv[kPosPerThread];
+#pragma unroll
+    for (int i = 0; i < kPosPerThread; ++i) {
+      const uint64_t p = pbase + uint64_t(i) * kTileThreads;
+      const bool ok = p < a.npos;
+      rowv[i] = ok ? __ldcs(a.p_row + p) : 0u;
+      prevv[i] = ok && p ? __ldcs(a.p_row + p - 1) : 0xFFFFFFFFu;
+      othv[i] = ok && (info[i] & 0xFFFFu) ? __ldcs(a.p_other + p) : 0u;
+    }
+    // ---- tile scan in position order (striped -> blocked -> striped)
+    BlockExch(tmp.exch).StripedToBlocked(cnt);
+    __syncthreads();
+    uint32_t tile_total;
+    BlockScan(tmp.scan).ExclusiveSum(cnt, cnt, tile_total);
+    __syncthreads();
+    BlockExch(tmp.exch).BlockedToStriped(cnt);
+    // ---- decoupled look-back for the tile's global item offset: warp 0
+    // inspects 32 predecessors per step (lane l: tile - 1 - l) and stops at
+    // the nearest one that published its inclusive prefix
+    if (threadIdx.x < 32) {
+      unsigned long long* st = a.tile_state;
+      const unsigned lane = threadIdx.x;
+      if (lane == 0) __stcg(st + tile, (tile == 0 ? kStInc : kStAgg) | tile_total);
+      unsigned long long prefix = 0;
+      for (int64_t base = int64_t(tile) - 1; base >= 0; base -= 32) {
+        const int64_t t = base - int64_t(lane);
+        unsigned long long v = kStInc;  // before tile 0: inclusive prefix 0
+        if (t >= 0)
+          do {
+            v = ld_volatile(st + t);
+          } while ((v >> 62) == 0);
+        const unsigned inc = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+        const unsigned stop = inc ? unsigned(__ffs(inc) - 1) : 31u;
+        unsigned long long val = lane <= stop ? (v & kStVal) : 0ull;
+        for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+        prefix += val;
+        if (inc) break;
+      }
+      if (lane == 0) {
+        if (tile) __stcg(st + tile, kStInc | (prefix + tile_total));
+        s_prefix = prefix;
+        if (tile + 1 == ntiles) a.meta[0] = prefix + tile_total;
+      }
+    }
+    for (int o = 16; o; o >>= 1) live += __shfl_xor_sync(0xffffffffu, live, o);
+    if (lane_id() == 0 && live) atomicAdd(&a.meta[1], (unsigned long long)live);
+    __syncthreads();
+    const unsigned long long prefix = s_prefix;
+    // ---- phase 2: items and row offsets
+#pragma unroll
+    for (int i = 0; i < kPosPerThread; ++i) {
+      const uint64_t p = pbase + uint64_t(i) * kTileThreads;
+      if (p >= a.npos) break;
+      uint64_t o = prefix + cnt[i];
+      const uint32_t row = rowv[i];
+      // rows (prev_row, row] start at this position (rows without edges share it)
+      for (uint32_t r = prevv[i] + 1; r <= row; ++r) a.row_off[r] = o;
+      const uint32_t c = info[i] & 0xFFFFu;
+      if (p + 1 == a.npos)  // rows after the last edge's row end at the total
+        for (uint32_t r = row + 1; r <= a.n; ++r) a.row_off[r] = o + c;
+      if (!c) continue;
+      const uint32_t other = othv[i];
+      const uint32_t b0 = info[i] >> 24, nb = (info[i] >> 16) & 0xFFu;
+      auto emit = [&](uint32_t b, uint32_t mk) {
+        if (!mk) return;
+        if (o < a.cap) {
+          a.it_other[o] = other;
+          a.it_row[o] = row;
+          a.it_mask[o] = mk;
+          a.it_batch[o] = uint8_t(b);
+        }
+        ++o;
+      };
+      emit(b0, mA[i]);
+      if (nb >= 2) emit(b0 + 1, mB[i]);
+      if (nb > 2) {  // wide window: re-evaluate the remaining batches
+        const uint32_t h = hv[i], W = wv[i];
+        uint32_t lo, hi, alo, ahi;
+        edge_window(sx, lut, a.J, h, W, a.fasst, lo, hi, alo, ahi);
+        for (uint32_t b = b0 + 2; b <= (hi - 1) >> 5; ++b)
+          emit(b, window_batch_mask(sx, h, W, lo, hi, alo, ahi, b));
+      }
+    }
+    __syncthreads();  // s_tile / s_prefix / scan storage reused by the next tile
+  }
+}
+
+// Item count of every stride-th position (capacity estimate of a one-pass
+// build: the exact total is known only when the pass ends).
+__global__ void k_items_sample(ItemsPass a, uint64_t stride) {
+  extern __shared__ __align__(16) uint32_t sx[];
+  uint32_t* lut = sx + a.Jp;
+  for (uint32_t i = threadIdx.x; i < a.Jp; i += blockDim.x) sx[i] = a.x[i];
+  if (a.fasst)
+    for (uint32_t k = threadIdx.x; k <= (1u << kLutBits); k += blockDim.x) lut[k] = a.glut[k];
+  __syncthreads();
+  unsigned long long c = 0;
+  for (uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; k * stride < a.npos;
+       k += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t p = k * stride;
+    const uint32_t W = a.p_w ? a.p_w[p] : a.Wc, h = a.p_hash[p];
+    if (W == 0) continue;
+    uint32_t lo, hi, alo, ahi;
+    edge_window(sx, lut, a.J, h, W, a.fasst, lo, hi, alo, ahi);
+    if (hi <= lo) continue;
+    for (uint32_t b = lo >> 5; b <= (hi - 1) >> 5; ++b)
+      c += window_batch_mask(sx, h, W, lo, hi, alo, ahi, b) != 0;
+  }
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane_id() == 0 && c) atomicAdd(&a.meta[0], c);
+}
+
+// Per-row chunk counts from the row item offsets.
+__global__ void k_row_chunks(uint32_t n, const uint64_t* __restrict__ row_off,
+                             uint32_t* __restrict__ row_cnt) {
+  for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+       r += uint64_t(gridDim.x) * blockDim.x)
+    row_cnt[r] = uint32_t((row_off[r + 1] - row_off[r] + kChunk - 1) / kChunk);
+}
+
 // Transposed position p holds edge tedge[p], whose item count is its forward
 // count (the sampling test depends on (edge hash, weight, slot) only): one
 // gather instead of re-evaluating the windows.  cnt[m] = 0 closes the scan.
@@ -339,14 +582,13 @@ __global__ void k_row_offsets(uint32_t n, const uint64_t* __restrict__ graph_off
 
 __global__ void k_chunk_write(uint32_t n, const uint64_t* __restrict__ row_chunk64,
                               const uint64_t* __restrict__ row_off, uint32_t* __restrict__ row_chunk,
-                              uint32_t* __restrict__ chunk_row, uint64_t* __restrict__ chunk_beg,
-                              uint64_t total_items) {
+                              uint32_t* __restrict__ chunk_row, uint64_t* __restrict__ chunk_beg) {
   for (uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; r <= n;
        r += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t c0 = row_chunk64[r];
     row_chunk[r] = uint32_t(c0);
     if (r == n) {
-      chunk_beg[c0] = total_items;
+      chunk_beg[c0] = row_off[n];  // total items
       continue;
     }
     const uint64_t c1 = row_chunk64[r + 1];
@@ -366,10 +608,12 @@ __global__ void k_split_chunks(const uint64_t* __restrict__ chunks_dev,
   for (uint64_t c0 = uint64_t(blockIdx.x) * blockDim.x; c0 < chunks;
        c0 += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t c = c0 + threadIdx.x;
-    bool isb = false, valid = c < chunks;
+    bool isb = false, single = false, valid = c < chunks;
     if (valid) {
       const uint32_t r = chunk_row[c];
-      isb = row_off[r + 1] - row_off[r] > kSmallRow;
+      const uint64_t items = row_off[r + 1] - row_off[r];
+      isb = items > kSmallRow;
+      single = items <= kChunk;  // the row is this one chunk: its warp owns the row
     }
     const unsigned mb = __ballot_sync(0xffffffffu, valid && isb);
     const unsigned ms = __ballot_sync(0xffffffffu, valid && !isb);
@@ -381,7 +625,7 @@ __global__ void k_split_chunks(const uint64_t* __restrict__ chunks_dev,
     bb = __shfl_sync(0xffffffffu, bb, 0);
     bs = __shfl_sync(0xffffffffu, bs, 0);
     const unsigned below = (1u << lane_id()) - 1;
-    if (valid && isb) big[bb + __popc(mb & below)] = uint32_t(c);
+    if (valid && isb) big[bb + __popc(mb & below)] = uint32_t(c) | (single ? kBigOwner : 0u);
     if (valid && !isb) small[bs + __popc(ms & below)] = uint32_t(c);
   }
 }
@@ -1234,13 +1478,15 @@ __device__ __forceinline__ uint32_t simulate_body(const RankDev& r, const SimOpt
     if (pull) {
       const uint32_t need = base + s - 1;  // source changed in sweep s-1 (or later)
       const uint64_t nbig = (a.dbg & 1) ? 0 : r.fwd.nbig;
+      auto big_rows = [&]() {
       // chunk headers one iteration ahead (their two dependent loads overlap
       // the current chunk instead of heading its latency chain)
       uint32_t c_nx = my_warp < nbig ? r.fwd.big[my_warp] : 0;
       for (uint64_t k = my_warp; k < nbig; k += n_warps) {
         __syncwarp();
         hook();
-        const uint32_t c = c_nx;
+        const uint32_t c = c_nx & ~kBigOwner;
+        const bool owner = (c_nx & kBigOwner) != 0;
         const uint32_t u = r.fwd.chunk_row[c];
         const uint64_t beg = r.fwd.chunk_beg[c], end = r.fwd.chunk_beg[c + 1];
         if (k + n_warps < nbig) c_nx = r.fwd.big[k + n_warps];
@@ -1297,7 +1543,6 @@ __device__ __forceinline__ uint32_t simulate_body(const RankDev& r, const SimOpt
           ++nitems;
         }
         __syncwarp();
-        const bool owner = r.fwd.row_chunk[u + 1] - r.fwd.row_chunk[u] == 1;
         unsigned long long* drow = reinterpret_cast<unsigned long long*>(r.regs + uint64_t(u) * Jp);
         bool changed = false;
         // Write-back spread over the lanes by 8-byte word (word w = batch
@@ -1345,9 +1590,10 @@ __device__ __forceinline__ uint32_t simulate_body(const RankDev& r, const SimOpt
         if (__any_sync(0xffffffffu, changed) && lane == 0)
           push_row_buf(u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &qc[gn], ws);
       }
+      };
       // Small destination rows (<= kSmallRow items): item-parallel over the
       // flattened chunks, one CAS per item on a lightly contended row.
-      {
+      auto small_rows = [&]() {
         const uint64_t nsi = (a.dbg & 2) ? 0 : r.fwd.nsmall_items;
         // dynamic: a warp claims DFS_SIM_CLAIM items at a time (balances the
         // big-row tail), 128 per step; 0 = static grid-stride
@@ -1425,7 +1671,9 @@ __device__ __forceinline__ uint32_t simulate_body(const RankDev& r, const SimOpt
           __syncwarp();
           hook();
         }
-      }
+      };
+      big_rows();
+      small_rows();
     } else {
       for_frontier_items(
           r.rev, s == 1 ? nullptr : r.q.chunks[g], nc, &cnt[8 + g], ws, n_warps,
@@ -1599,7 +1847,7 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) 
   __shared__ WarpStage stage[kWarps];
   __shared__ unsigned long long s_release;
   __shared__ RankDev s_r;
-  extern __shared__ unsigned long long dyn_smem[];
+  extern __shared__ __align__(128) unsigned long long dyn_smem[];
   if (threadIdx.x == 0) s_r = a.r;
   __syncthreads();
   cg::grid_group grid = cg::this_grid();
@@ -2107,11 +2355,12 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
       // a shared accumulator, then claims the unvisited ones with one update
       // per batch word (direction-optimising BFS, Beamer et al.).
       const uint64_t nbig = r.rev.nbig;
-      uint32_t c_nx = my_warp < nbig ? r.rev.big[my_warp] : 0;  // one iteration ahead
+      uint32_t c_nx = my_warp < nbig ? r.rev.big[my_warp] : 0;  // one iteration ahead (| owner flag)
       for (uint64_t k = my_warp; k < nbig; k += n_warps) {
         __syncwarp();
         hook();
-        const uint32_t c = c_nx;
+        const uint32_t c = c_nx & ~kBigOwner;
+        const bool owner = (c_nx & kBigOwner) != 0;
         const uint32_t v = r.rev.chunk_row[c];
         const uint64_t beg = r.rev.chunk_beg[c], end = r.rev.chunk_beg[c + 1];
         if (k + n_warps < nbig) c_nx = r.rev.big[k + n_warps];
@@ -2151,7 +2400,6 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
           }
         if (!__any_sync(0xffffffffu, any)) continue;
         __syncwarp();
-        const bool owner = r.rev.row_chunk[v + 1] - r.rev.row_chunk[v] == 1;
         bool got = false;
         for (uint32_t b = lane; b < W32; b += 32) {
           uint32_t a = cacc[b];
@@ -2243,6 +2491,10 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
       for (;;) {
         const uint32_t nc = qchunks(qc, L % 4);
         if (nc == 0) {
+          // a last frontier of rows without device-graph out-edges is still a
+          // level of the reference's loop (engine.cpp:121-124): count its rows
+          if (a.cnt && threadIdx.x == 0)
+            r.ctl->cnt_cas_rows += qrows(qc, L % 4);
           finish(L, true);
           code = 1;
           break;
@@ -2295,7 +2547,7 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_cascade(CasArgs a) {
   __shared__ WarpStage stage[kWarps];
   __shared__ unsigned long long s_release;
   __shared__ RankDev s_r;
-  extern __shared__ unsigned long long dyn_smem[];
+  extern __shared__ __align__(128) unsigned long long dyn_smem[];
   if (threadIdx.x == 0) s_r = a.r;
   __syncthreads();
   cg::grid_group grid = cg::this_grid();
@@ -2451,7 +2703,7 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
   // returns the next one) so that no block reads a tick another block may
   // already have advanced.  Read once here, before the first grid barrier.
   __shared__ uint32_t s_tick[64];
-  extern __shared__ unsigned long long dyn_smem[];
+  extern __shared__ __align__(128) unsigned long long dyn_smem[];
   cg::grid_group grid = cg::this_grid();
   for (uint32_t t = threadIdx.x; t < a.mu; t += blockDim.x) s_tick[t] = ld_volatile(&a.ranks[t].ctl->tick);
   __syncthreads();
@@ -2849,6 +3101,79 @@ void launch_items_pass(const DevGraph& g, const uint32_t* w, const uint32_t* tw,
   ++g_launches;
 }
 
+uint64_t items_tiles(uint64_t npos) { return (npos + kTilePos - 1) / kTilePos; }
+
+static ItemsPass items_pass_args(const DevGraph& g, const uint32_t* w, const uint32_t* tw,
+                                 uint32_t wconst, const RankDev& r, int dir, int fasst) {
+  ItemsPass a{};
+  a.npos = g.m;
+  a.n = g.n;
+  a.p_hash = dir ? g.thash : g.ehash;
+  a.p_w = wconst ? nullptr : (dir ? tw : w);
+  a.Wc = wconst;
+  a.p_other = dir ? g.tsrc : g.adj;
+  a.p_row = dir ? g.tdst : g.src;
+  a.x = r.x;
+  a.glut = r.xlut;
+  a.J = r.J;
+  a.Jp = r.Jp;
+  a.fasst = fasst;
+  return a;
+}
+
+static size_t items_smem(const RankDev& r) {
+  static bool attr = false;
+  if (!attr) {
+    DFS_CUDA(cudaFuncSetAttribute(k_items_onepass, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
+    DFS_CUDA(cudaFuncSetAttribute(k_items_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
+    attr = true;
+  }
+  return (size_t(r.Jp) + (1u << kLutBits) + 1) * sizeof(uint32_t);
+}
+
+void launch_items_sample(const DevGraph& g, const uint32_t* w, uint32_t wconst, const RankDev& r,
+                         int fasst, uint64_t stride, unsigned long long* meta, cudaStream_t s) {
+  if (!g.m) return;
+  ItemsPass a = items_pass_args(g, w, nullptr, wconst, r, 0, fasst);
+  a.meta = meta;
+  const size_t smem = items_smem(r);
+  k_items_sample<<<grid_for((g.m + stride - 1) / stride, kThreads * 4), kThreads, smem, s>>>(a, stride);
+  DFS_CUDA(cudaGetLastError());
+  ++g_launches;
+}
+
+void launch_items_onepass(const DevGraph& g, const uint32_t* w, const uint32_t* tw,
+                          uint32_t wconst, const RankDev& r, int dir, int fasst, Items& it,
+                          uint64_t cap, unsigned long long* tile_state, unsigned int* tile_ctr,
+                          unsigned long long* meta, cudaStream_t s) {
+  if (!g.m) return;
+  ItemsPass a = items_pass_args(g, w, tw, wconst, r, dir, fasst);
+  a.cap = cap;
+  a.it_other = it.other;
+  a.it_mask = it.mask;
+  a.it_batch = it.batch;
+  a.it_row = it.row;
+  a.row_off = it.row_off;
+  a.tile_state = tile_state;
+  a.tile_ctr = tile_ctr;
+  a.meta = meta;
+  const size_t smem = items_smem(r);
+  int per = 0;
+  DFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_items_onepass, kTileThreads, smem));
+  const uint64_t tiles = items_tiles(g.m);
+  const int grid = int(std::min<uint64_t>(tiles, uint64_t(std::max(per, 1)) * num_sms()));
+  k_items_onepass<<<grid, kTileThreads, smem, s>>>(a);
+  DFS_CUDA(cudaGetLastError());
+  ++g_launches;
+}
+
+void launch_row_chunks(uint32_t n, const Items& it, uint32_t* row_cnt, cudaStream_t s) {
+  if (!n) return;
+  k_row_chunks<<<grid_for(n), kThreads, 0, s>>>(n, it.row_off, row_cnt);
+  DFS_CUDA(cudaGetLastError());
+  ++g_launches;
+}
+
 void launch_fasst_stats(const DevGraph& g, const uint32_t* w, const uint32_t* x,
                         const uint32_t* xlut, uint32_t R, uint32_t mu, int sorted, int fill,
                         unsigned long long* out, cudaStream_t s) {
@@ -2924,7 +3249,7 @@ void launch_row_offsets(const DevGraph& g, int dir, const uint64_t* pos_off, Ite
 
 void launch_chunk_write(uint32_t n, Items& it, const uint64_t* row_chunk64, cudaStream_t s) {
   k_chunk_write<<<grid_for(uint64_t(n) + 1), kThreads, 0, s>>>(
-      n, row_chunk64, it.row_off, it.row_chunk, it.chunk_row, it.chunk_beg, it.count);
+      n, row_chunk64, it.row_off, it.row_chunk, it.chunk_row, it.chunk_beg);
   DFS_CUDA(cudaGetLastError());
   ++g_launches;
 }

@@ -200,25 +200,24 @@ void Context::alloc_rank(RankDev& r, uint32_t tau) {
   launch_xlut(r, stream_);
 }
 
-// Chunk headers, small/big split and small-item list of one direction (row
-// offsets come from the per-position item offsets `pos`).  Sized by upper
-// bounds (chunks <= items/kChunk + n) so the host never waits here; the
-// exact counts land in meta[0..2] (chunks, small|big chunk counts, small
-// items) and are read back once per partition by build_items.
-void Context::finish_items(RankDev& r, int dir, const uint64_t* pos, uint64_t* meta) {
+// Chunk headers, small/big split and small-item list of one direction, from
+// the row item offsets the one-pass build wrote.  Sized by upper bounds
+// (chunks <= cap/kChunk + n) so the host never waits here; the exact counts
+// land in meta[0..2] (chunks, small|big chunk counts, small items) and are
+// read back once per partition by build_items.
+void Context::finish_items(RankDev& r, int dir, uint64_t cap_items, uint64_t* meta) {
   const std::string p = "r" + std::to_string(r.tau) + (dir ? ".rev." : ".fwd.");
   Items& it = dir ? r.rev : r.fwd;
   const uint32_t n = g_.n;
-  const size_t sb = scan_tmp_bytes(std::max<uint64_t>(g_.m, n) + 2);
+  const size_t sb = scan_tmp_bytes(uint64_t(n) + 2);
   void* stmp = arena_.get("tmp.scan", sb);
-  it.row_off = as<uint64_t>(arena_.get(p + "row_off", (size_t(n) + 1) * 8));
   uint32_t* row_cnt = as<uint32_t>(arena_.get("tmp.rowcnt", (size_t(n) + 2) * 4));
   DFS_CUDA(cudaMemsetAsync(row_cnt, 0, (size_t(n) + 1) * 4, stream_));
-  launch_row_offsets(g_, dir, pos, it, row_cnt, stream_);
+  launch_row_chunks(n, it, row_cnt, stream_);
   uint64_t* row_chunk64 = as<uint64_t>(arena_.get("tmp.rowchunk", (size_t(n) + 2) * 8));
   scan_u32_u64(row_cnt, row_chunk64, n, stmp, sb, stream_);
-  const uint64_t cap = it.count / kChunk + n + 1;  // >= chunks
-  if (cap >= (uint64_t(1) << 32)) throw Error(kRuntime, "too many work chunks");
+  const uint64_t cap = cap_items / kChunk + n + 1;  // >= chunks
+  if (cap >= (uint64_t(1) << 31)) throw Error(kRuntime, "too many work chunks");
   DFS_CUDA(cudaMemcpyAsync(meta, row_chunk64 + n, 8, cudaMemcpyDeviceToDevice, stream_));
   it.chunk_row = as<uint32_t>(arena_.get(p + "chunk_row", cap * 4));
   it.chunk_beg = as<uint64_t>(arena_.get(p + "chunk_beg", (cap + 1) * 8));
@@ -226,65 +225,76 @@ void Context::finish_items(RankDev& r, int dir, const uint64_t* pos, uint64_t* m
   launch_chunk_write(n, it, row_chunk64, stream_);
   it.small = as<uint32_t>(arena_.get(p + "small", cap * 4));
   it.big = as<uint32_t>(arena_.get(p + "big", cap * 4));
-  it.small_items = as<uint32_t>(arena_.get(p + "small_items", std::max<uint64_t>(it.count, 1) * 4));
+  it.small_items = as<uint32_t>(arena_.get(p + "small_items", std::max<uint64_t>(cap_items, 1) * 4));
   unsigned int* c2 = reinterpret_cast<unsigned int*>(meta + 1);
   launch_split_chunks(it, meta, cap, c2, stream_);
   launch_small_items(it, c2, cap, reinterpret_cast<unsigned long long*>(meta + 2), stream_);
   it.chunks = cap;  // provisional (exact after build_items' readback)
 }
 
-// Sampled items of one partition: forward items by evaluating the sampling
-// test once per (edge, batch) inside each edge's FASST window, then the
-// reverse items by re-keying the forward ones through the transpose.
+// Sampled items of one partition (fasst.cpp:50-88), both directions, each in
+// ONE pass over the edge positions (k_items_onepass: windows evaluated once,
+// block scan + decoupled look-back, items and row offsets written in place).
+// The item arrays are sized from a sampled estimate (every stride-th edge);
+// the rare underestimate re-runs the passes with the exact total.  Two host
+// readbacks per partition: the estimate and the final metadata.
 void Context::build_items(RankDev& r) {
   const std::string p = "r" + std::to_string(r.tau) + ".";
   const uint64_t m = g_.m;
   const uint32_t n = g_.n;
-  // One count/position scratch pair serves both directions in turn (12 B per
-  // edge instead of 24: at 1B edges the difference decides whether eight
-  // partitions fit one GPU).  Both directions hold the same number of items.
-  uint32_t* cnt = as<uint32_t>(arena_.get("tmp.cnt", (m + 2) * 4));
-  uint64_t* pos = as<uint64_t>(arena_.get("tmp.pos", (m + 2) * 8));
-  const size_t sb = scan_tmp_bytes(std::max<uint64_t>(m, n) + 2);
-  void* stmp = arena_.get("tmp.scan", sb);
   Items& f = r.fwd;
   Items& rv = r.rev;
   const int fa = cfg_.fasst ? 1 : 0;
-  DFS_CUDA(cudaMemsetAsync(cnt, 0, (m + 1) * 4, stream_));
-  launch_items_pass(g_, w_, tw_, r, 0, fa, 0, cnt, nullptr, f, stream_);
-  scan_u32_u64(cnt, pos, m, stmp, sb, stream_);
-  DFS_CUDA(cudaMemcpyAsync(&f.count, pos + m, 8, cudaMemcpyDeviceToHost, stream_));
-  sync();
-  rv.count = f.count;
-  const size_t ic = std::max<uint64_t>(f.count, 1);
-  for (int d = 0; d < 2; ++d) {
-    Items& it = d ? rv : f;
-    const std::string q = p + (d ? "rev." : "fwd.");
-    it.other = as<uint32_t>(arena_.get(q + "other", ic * 4));
-    it.row = as<uint32_t>(arena_.get(q + "row", ic * 4));
-    it.mask = as<uint32_t>(arena_.get(q + "mask", ic * 4));
-    it.batch = as<uint8_t>(arena_.get(q + "batch", ic));
+  const uint32_t wconst =
+      cfg_.weights.kind == WeightKind::Constant ? to_fixed_point(cfg_.weights.a) : 0u;
+  // meta: [0..3] fwd chunk meta, [4..7] rev chunk meta, [8] fwd total, [9] fwd
+  // live, [10] sample, [12] rev total, [13] rev live, [14] tile counters
+  uint64_t* meta = as<uint64_t>(arena_.get("tmp.meta", 16 * 8));
+  auto* um = reinterpret_cast<unsigned long long*>(meta);
+  const uint64_t tiles = items_tiles(m);
+  auto* tstate = as<unsigned long long>(arena_.get("tmp.tiles", (2 * tiles + 2) * 8));
+  f.row_off = as<uint64_t>(arena_.get(p + "fwd.row_off", (size_t(n) + 1) * 8));
+  rv.row_off = as<uint64_t>(arena_.get(p + "rev.row_off", (size_t(n) + 1) * 8));
+  DFS_CUDA(cudaMemsetAsync(meta, 0, 16 * 8, stream_));
+  if (!m) {
+    DFS_CUDA(cudaMemsetAsync(f.row_off, 0, (size_t(n) + 1) * 8, stream_));
+    DFS_CUDA(cudaMemsetAsync(rv.row_off, 0, (size_t(n) + 1) * 8, stream_));
   }
-  uint64_t* meta = as<uint64_t>(arena_.get("tmp.meta", 8 * 8));
-  DFS_CUDA(cudaMemsetAsync(meta, 0, 8 * 8, stream_));
-  launch_items_pass(g_, w_, tw_, r, 0, fa, 1, cnt, pos, f, stream_);
-  finish_items(r, 0, pos, meta);
-  // Reverse counts: gathered from the forward offsets while those fit in L2
-  // (random reads hit; C2 build -8%), else the sampling count pass again
-  // (at 100M edges the gather misses to HBM and loses to the recount).
-  if ((m + 1) * 8 <= (size_t(128) << 20)) {
-    launch_rev_counts(g_, pos, cnt, stream_);  // reads the forward offsets, before the scan
-  } else {
-    DFS_CUDA(cudaMemsetAsync(cnt, 0, (m + 1) * 4, stream_));
-    launch_items_pass(g_, w_, tw_, r, 1, fa, 0, cnt, nullptr, rv, stream_);
-  }
-  scan_u32_u64(cnt, pos, m, stmp, sb, stream_);
-  launch_items_pass(g_, w_, tw_, r, 1, fa, 1, cnt, pos, rv, stream_);
-  finish_items(r, 1, pos, meta + 4);
-  launch_popc_sum(f.mask, f.count, reinterpret_cast<unsigned long long*>(meta + 3), stream_);
-  uint64_t hm[8];  // the partition's one metadata readback
-  DFS_CUDA(cudaMemcpyAsync(hm, meta, sizeof hm, cudaMemcpyDeviceToHost, stream_));
+  // capacity: sampled estimate (exact below 2^20 edges) plus slack
+  const uint64_t stride = std::max<uint64_t>(1, m >> 20);
+  launch_items_sample(g_, w_, wconst, r, fa, stride, um + 10, stream_);
+  uint64_t sampled = 0;
+  DFS_CUDA(cudaMemcpyAsync(&sampled, meta + 10, 8, cudaMemcpyDeviceToHost, stream_));
   sync();
+  uint64_t cap = stride == 1 ? sampled : sampled * stride + sampled * stride / 8 + 65536;
+  uint64_t hm[16];
+  for (int attempt = 0;; ++attempt) {
+    const size_t ic = std::max<uint64_t>(cap, 1);
+    for (int d = 0; d < 2; ++d) {
+      Items& it = d ? rv : f;
+      const std::string q = p + (d ? "rev." : "fwd.");
+      it.other = as<uint32_t>(arena_.get(q + "other", ic * 4));
+      it.row = as<uint32_t>(arena_.get(q + "row", ic * 4));
+      it.mask = as<uint32_t>(arena_.get(q + "mask", ic * 4));
+      it.batch = as<uint8_t>(arena_.get(q + "batch", ic));
+    }
+    DFS_CUDA(cudaMemsetAsync(meta, 0, 10 * 8, stream_));
+    DFS_CUDA(cudaMemsetAsync(meta + 11, 0, 5 * 8, stream_));
+    DFS_CUDA(cudaMemsetAsync(tstate, 0, 2 * tiles * 8, stream_));
+    auto* ctr = reinterpret_cast<unsigned int*>(meta + 14);
+    launch_items_onepass(g_, w_, tw_, wconst, r, 0, fa, f, cap, tstate, ctr, um + 8, stream_);
+    launch_items_onepass(g_, w_, tw_, wconst, r, 1, fa, rv, cap, tstate + tiles, ctr + 1, um + 12,
+                         stream_);
+    finish_items(r, 0, cap, meta);
+    finish_items(r, 1, cap, meta + 4);
+    DFS_CUDA(cudaMemcpyAsync(hm, meta, sizeof hm, cudaMemcpyDeviceToHost, stream_));
+    sync();
+    if (hm[8] <= cap) break;
+    if (attempt) throw Error(kRuntime, "item build: capacity re-run overflowed");
+    cap = hm[8];  // underestimated: exact total, once more
+  }
+  if (hm[8] != hm[12]) throw Error(kRuntime, "item build: direction totals differ");
+  f.count = rv.count = hm[8];
   for (int d = 0; d < 2; ++d) {
     Items& it = d ? rv : f;
     it.chunks = hm[4 * d];
@@ -292,7 +302,7 @@ void Context::build_items(RankDev& r) {
     it.nbig = uint32_t(hm[4 * d + 1] >> 32);
     it.nsmall_items = hm[4 * d + 2];
   }
-  f.live = hm[3];
+  f.live = hm[9];
 }
 
 void Context::reset_rank_state(RankDev& r) {

@@ -178,7 +178,7 @@ class Context {
   void plan_weights(const RunConfig& cfg, const HostGraph* host_w_src);
   PeerBox* peer_box();
   void build_items(RankDev& r);
-  void finish_items(RankDev& r, int dir, const uint64_t* pos, uint64_t* meta);
+  void finish_items(RankDev& r, int dir, uint64_t cap_items, uint64_t* meta);
   void alloc_rank(RankDev& r, uint32_t tau);
   void reset_rank_state(RankDev& r);
 
