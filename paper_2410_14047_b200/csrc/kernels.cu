@@ -1478,7 +1478,7 @@ __device__ __forceinline__ uint32_t simulate_body(const RankDev& r, const SimOpt
     if (pull) {
       const uint32_t need = base + s - 1;  // source changed in sweep s-1 (or later)
       const uint64_t nbig = (a.dbg & 1) ? 0 : r.fwd.nbig;
-      auto big_rows = [&]() {
+      {
       // chunk headers one iteration ahead (their two dependent loads overlap
       // the current chunk instead of heading its latency chain)
       uint32_t c_nx = my_warp < nbig ? r.fwd.big[my_warp] : 0;
@@ -1590,10 +1590,10 @@ __device__ __forceinline__ uint32_t simulate_body(const RankDev& r, const SimOpt
         if (__any_sync(0xffffffffu, changed) && lane == 0)
           push_row_buf(u, stamp, r.lstamp, r.rev.row_chunk, rows_n, chunks_n, &qc[gn], ws);
       }
-      };
+      }
       // Small destination rows (<= kSmallRow items): item-parallel over the
       // flattened chunks, one CAS per item on a lightly contended row.
-      auto small_rows = [&]() {
+      {
         const uint64_t nsi = (a.dbg & 2) ? 0 : r.fwd.nsmall_items;
         // dynamic: a warp claims DFS_SIM_CLAIM items at a time (balances the
         // big-row tail), 128 per step; 0 = static grid-stride
@@ -1671,9 +1671,7 @@ __device__ __forceinline__ uint32_t simulate_body(const RankDev& r, const SimOpt
           __syncwarp();
           hook();
         }
-      };
-      big_rows();
-      small_rows();
+      }
     } else {
       for_frontier_items(
           r.rev, s == 1 ? nullptr : r.q.chunks[g], nc, &cnt[8 + g], ws, n_warps,
@@ -1847,7 +1845,7 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_simulate(SimArgs a) 
   __shared__ WarpStage stage[kWarps];
   __shared__ unsigned long long s_release;
   __shared__ RankDev s_r;
-  extern __shared__ __align__(128) unsigned long long dyn_smem[];
+  extern __shared__ unsigned long long dyn_smem[];
   if (threadIdx.x == 0) s_r = a.r;
   __syncthreads();
   cg::grid_group grid = cg::this_grid();
@@ -2227,7 +2225,10 @@ struct CasOpts {
   int cnt;  // count mode: tally the reference-schedule cascade work units
 };
 
-// `base` as in simulate_body; returns the next stamp base.
+// `base` as in simulate_body; returns the next stamp base.  CNT: count mode
+// (a compile-time switch: its bookkeeping stays out of the timed variant's
+// register allocation).
+template <int CNT>
 __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts& a,
                                              cg::grid_group& grid, WarpStage* stage,
                                              unsigned long long& s_release, uint32_t* cas_smem,
@@ -2276,7 +2277,7 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
     __syncwarp();
     if (lane == 0) {
       r.cstamp[s] = (static_cast<unsigned long long>(base) << 32) | (any ? base + 1 : 0u);
-      if (any && a.cnt) r.ctl->cnt_cascades += 1;
+      if (any && CNT) r.ctl->cnt_cascades += 1;
       if (any) {
         const uint32_t c0 = r.fwd.row_chunk[s], c1 = r.fwd.row_chunk[s + 1];
         qc[1] = (1ull << 32) | (c1 - c0);
@@ -2301,7 +2302,7 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
     }
     clear_rows(fprev, r.q.rows[gp], qrows(qc, gp), W32, my_warp, n_warps, lane);
     if ((a.dbg & 4) && blockIdx.x == 0 && threadIdx.x == 0) trace(2 + (solo ? 1 : 0), L, nc);
-    if (a.cnt) {  // frontier rows and their device-graph out-edges
+    if (CNT) {  // frontier rows and their device-graph out-edges
       const unsigned nr = qrows(qc, g);
       if (my_warp == 0 && lane == 0) atomicAdd(&r.ctl->cnt_cas_rows, (unsigned long long)nr);
       unsigned long long ne = 0;
@@ -2360,7 +2361,6 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
         __syncwarp();
         hook();
         const uint32_t c = c_nx & ~kBigOwner;
-        const bool owner = (c_nx & kBigOwner) != 0;
         const uint32_t v = r.rev.chunk_row[c];
         const uint64_t beg = r.rev.chunk_beg[c], end = r.rev.chunk_beg[c + 1];
         if (k + n_warps < nbig) c_nx = r.rev.big[k + n_warps];
@@ -2400,6 +2400,7 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
           }
         if (!__any_sync(0xffffffffu, any)) continue;
         __syncwarp();
+        const bool owner = r.rev.row_chunk[v + 1] - r.rev.row_chunk[v] == 1;
         bool got = false;
         for (uint32_t b = lane; b < W32; b += 32) {
           uint32_t a = cacc[b];
@@ -2493,7 +2494,7 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
         if (nc == 0) {
           // a last frontier of rows without device-graph out-edges is still a
           // level of the reference's loop (engine.cpp:121-124): count its rows
-          if (a.cnt && threadIdx.x == 0)
+          if (CNT && threadIdx.x == 0)
             r.ctl->cnt_cas_rows += qrows(qc, L % 4);
           finish(L, true);
           code = 1;
@@ -2547,14 +2548,14 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_cascade(CasArgs a) {
   __shared__ WarpStage stage[kWarps];
   __shared__ unsigned long long s_release;
   __shared__ RankDev s_r;
-  extern __shared__ __align__(128) unsigned long long dyn_smem[];
+  extern __shared__ unsigned long long dyn_smem[];
   if (threadIdx.x == 0) s_r = a.r;
   __syncthreads();
   cg::grid_group grid = cg::this_grid();
   const CasOpts o{a.choice, a.seed, a.dbg, a.pull_f, 0};
   const uint32_t base = ld_volatile(&a.r.ctl->tick);
   grid.sync();  // every block holds `base` before block 0 can finish a solo cascade
-  cascade_body(s_r, o, grid, stage, s_release, reinterpret_cast<uint32_t*>(dyn_smem), base);
+  cascade_body<0>(s_r, o, grid, stage, s_release, reinterpret_cast<uint32_t*>(dyn_smem), base);
 }
 
 // ---------------------------------------------------------------- round end
@@ -2686,11 +2687,12 @@ __device__ __noinline__ uint32_t run_simulate(const RankDev& r, const SimOpts& o
   cg::grid_group grid = cg::this_grid();
   return simulate_body<JAC, CNT>(r, o, grid, stage, s_release, dyn, base);
 }
+template <int CNT>
 __device__ __noinline__ uint32_t run_cascade(const RankDev& r, const CasOpts& o, WarpStage* stage,
                                              unsigned long long& s_release, uint32_t* dyn,
                                              uint32_t base) {
   cg::grid_group grid = cg::this_grid();
-  return cascade_body(r, o, grid, stage, s_release, dyn, base);
+  return cascade_body<CNT>(r, o, grid, stage, s_release, dyn, base);
 }
 
 template <int JAC, int CNT>
@@ -2703,7 +2705,7 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
   // returns the next one) so that no block reads a tick another block may
   // already have advanced.  Read once here, before the first grid barrier.
   __shared__ uint32_t s_tick[64];
-  extern __shared__ __align__(128) unsigned long long dyn_smem[];
+  extern __shared__ unsigned long long dyn_smem[];
   cg::grid_group grid = cg::this_grid();
   for (uint32_t t = threadIdx.x; t < a.mu; t += blockDim.x) s_tick[t] = ld_volatile(&a.ranks[t].ctl->tick);
   __syncthreads();
@@ -2940,7 +2942,7 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
       load_rank(t);
       const CasOpts co{&a.ra.ctl->choice, 0, a.dbg, a.cas_pull_f, CNT};
       const uint32_t nt =
-          run_cascade(s_r, co, stage, s_release, reinterpret_cast<uint32_t*>(dyn_smem), s_tick[t]);
+          run_cascade<CNT>(s_r, co, stage, s_release, reinterpret_cast<uint32_t*>(dyn_smem), s_tick[t]);
       grid.sync();
       if (threadIdx.x == 0) s_tick[t] = nt;
     }

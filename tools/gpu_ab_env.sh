@@ -1,0 +1,16 @@
+#!/bin/bash
+# A/B of environment settings on one config: ENVS="A=1 B=2|..." separated by |
+cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
+IFS='|' read -ra VS <<< "${ENVS:-X=0|X=1}"
+for cfg in ${CFGS:-c3ic}; do
+for rep in 1 2; do
+  for v in "${VS[@]}"; do
+    env $v timeout 300 python tools/profile_run.py $cfg 3 2>gpurun_out/ab_err.txt | tail -1 > gpurun_out/ph.txt
+    python - "$v" $cfg <<'PY'
+import ast, sys
+d = ast.literal_eval(open("gpurun_out/ph.txt").read())
+print(sys.argv[2], sys.argv[1], {k: round(d[k] * 1e3, 2) for k in ("build", "fill", "simulate", "select", "cascade", "total")}, "krun", round(d["run_kernel"] * 1e3, 2))
+PY
+  done
+done
+done
