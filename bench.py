@@ -44,6 +44,8 @@ CONFIGS = {
            "C3: R-MAT scale-23 (100M edges), weighted cascade, R=1024, K=50"),
     "c3ic": ("rmat", 23, 100_000_000, "const:0.01", 1024, 50,
              "north star: R-MAT scale-23 (100M edges), IC p=0.01, R=1024, K=50"),
+    "c2wc": ("rmat", 20, 16_000_000, "wc", 1024, 50,
+             "R-MAT scale-20 (16M edges), weighted cascade, R=1024, K=50 (profiling aid)"),
     "c4": ("rmat", 26, 1_000_000_000, "const:0.005", 1024, 100,
            "C4: R-MAT scale-26 (1B edges), IC p=0.005, R=1024, K=100"),
 }

@@ -2629,9 +2629,21 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-template <class T>
-__device__ __forceinline__ T ld_relaxed_sys(const T* p) {
-  return *reinterpret_cast<const volatile T*>(p);
+// Peer data read after a barrier's acquire: explicit system-scope relaxed
+// loads (the barrier's acquire orders them; L1 is never consulted).
+__device__ __forceinline__ unsigned int ld_relaxed_sys(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ double ld_relaxed_sys(const double* p) {
+  return __longlong_as_double(
+      static_cast<long long>(ld_relaxed_sys(reinterpret_cast<const unsigned long long*>(p))));
 }
 
 // Cross-GPU barrier of epoch `ep`, called by every thread of the grid: after
@@ -2673,7 +2685,7 @@ __device__ __noinline__ void peer_sync(const PeerView& pv, unsigned long long ep
 __device__ __forceinline__ double peer_reduced(const PeerView& pv, uint32_t v) {
   double acc[kMaxPeers];
 #pragma unroll 4
-  for (uint32_t t = 0; t < pv.world; ++t) acc[t] = __ldcg(pv.scores[t] + v);
+  for (uint32_t t = 0; t < pv.world; ++t) acc[t] = ld_relaxed_sys(pv.scores[t] + v);
   for (uint32_t st = 1; st < pv.world; st <<= 1)
     for (uint32_t t = 0; t + st < pv.world; t += 2 * st) acc[t] = __dadd_rn(acc[t], acc[t + st]);
   return acc[0];
@@ -2894,7 +2906,7 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
           const uint32_t c = ld_relaxed_sys(&a.pv.box[q]->ndirty);
           const uint32_t* dq = a.pv.dirty[q];
           for (uint64_t i = gtid; i < c; i += gthreads) {
-            const uint32_t v = __ldcg(dq + i);
+            const uint32_t v = ld_relaxed_sys(dq + i);
             if (v >= plo && v < phi) a.reduced[v] = peer_reduced(a.pv, v);
           }
         }
@@ -2904,7 +2916,7 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
           const uint32_t c = ld_relaxed_sys(&a.pv.box[q]->ndirty);
           const uint32_t* dq = a.pv.dirty[q];
           for (uint64_t i = gw; i < c; i += nw) {
-            const uint32_t v = __ldcg(dq + i);
+            const uint32_t v = ld_relaxed_sys(dq + i);
             if (v < plo || v >= phi) continue;  // warp-uniform
             const uint32_t sg = (v - plo) / kSeg;
             unsigned prev = 0;

@@ -131,3 +131,40 @@ def test_peer_dead_rank_fails_instead_of_hanging():
     assert out[1][0] == ["dead"]
     msg = out[0][0][0]
     assert msg.startswith("ERR:") and "peer" in msg, msg
+
+
+def _torchrun(args, timeout=900):
+    import socket
+    import subprocess
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(os.path.dirname(HERE), "bench.py")] + args
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout,
+                         cwd=os.path.dirname(HERE))
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]  # rank 0 alone prints
+    return json.loads(lines[0])
+
+
+def test_scale_command_path_two_ranks():
+    """The driver's scaling command (torchrun -> bench.py --gpus 2 -> PeerRunner)
+    end to end, both ranks sharing this GPU: one JSON line, the reference's
+    devices=2 report reproduced byte-for-byte."""
+    line = _torchrun(["--gpus", "2", "--share-gpu", "--steps", "2", "--warmup", "1",
+                      "--no-north-star", "--no-cpu-baseline"])
+    assert line["n_gpus"] == 2 and line["config"]["devices"] == 2
+    assert line["metric"] and line["value"] > 0 and line["e2e"]["value"] > 0
+    assert line["report_parity"] == "identical"
+
+
+def test_scale_command_path_reference_arm():
+    """--impl reference under torchrun: rank 0 alone runs the unmodified
+    reference at devices = world and reports the same config."""
+    line = _torchrun(["--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0"])
+    assert line["impl"] == "reference" and line["config"]["devices"] == 2
+    assert line["report_parity"] == "identical"

@@ -8,7 +8,7 @@ for rep in 1 2; do
     python - $pkg $cfg <<'PY'
 import ast, sys
 d = ast.literal_eval(open("gpurun_out/ph.txt").read())
-print(sys.argv[2], sys.argv[1], {k: round(d[k] * 1e3, 2) for k in ("build", "fill", "simulate", "select", "cascade", "total")}, "krun", round(d["run_kernel"] * 1e3, 2))
+print(sys.argv[2], sys.argv[1], {k: round(d[k] * 1e3, 2) for k in ("build", "fill", "simulate", "select", "cascade", "total")}, "krun", round(d["run_kernel"] * 1e3, 2), "density", round(d.get("item_density", 0), 3), "sweeps", d["sweeps_total"])
 PY
   done
 done

@@ -7,6 +7,8 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
+if os.environ.get("DFS_PKG"):  # another build of the package (A/B)
+    sys.path.insert(0, os.environ["DFS_PKG"])
 import paper_2410_14047_b200 as D  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
