@@ -976,10 +976,10 @@ __device__ __forceinline__ void fill_body(uint32_t n, uint32_t J, uint32_t Jp,
           const uint32_t w = w0 + t * G;
           if (w < q16) {
             uint4 o = v[t];
-            o.x |= expand4(vb[t] & 15u);
-            o.y |= expand4((vb[t] >> 4) & 15u);
-            o.z |= expand4((vb[t] >> 8) & 15u);
-            o.w |= expand4((vb[t] >> 12) & 15u);
+            o.x &= ~expand4(vb[t] & 15u);
+            o.y &= ~expand4((vb[t] >> 4) & 15u);
+            o.z &= ~expand4((vb[t] >> 8) & 15u);
+            o.w &= ~expand4((vb[t] >> 12) & 15u);
             dst[w] = o;
           }
         }
@@ -999,15 +999,17 @@ __device__ __forceinline__ void fill_body(uint32_t n, uint32_t J, uint32_t Jp,
       const ulonglong2 k01 = __ldg(reinterpret_cast<const ulonglong2*>(jkey + j0));
       const ulonglong2 k23 = __ldg(reinterpret_cast<const ulonglong2*>(jkey + j0 + 2));
       const uint32_t vb = (vis[u * W32 + (j0 >> 5)] >> (j0 & 31)) & 15u;
-      uint32_t pw = uint32_t(__clzll(fmix64(k01.x + ug))) |
-                    (uint32_t(__clzll(fmix64(k01.y + ug))) << 8) |
-                    (uint32_t(__clzll(fmix64(k23.x + ug))) << 16) |
-                    (uint32_t(__clzll(fmix64(k23.y + ug))) << 24);
-      if (j0 + 4 > J) {  // pad registers are VISITED
+      // stored byte = register value + 1 (clz <= 64: no carry between bytes)
+      uint32_t pw = (uint32_t(__clzll(fmix64(k01.x + ug))) |
+                     (uint32_t(__clzll(fmix64(k01.y + ug))) << 8) |
+                     (uint32_t(__clzll(fmix64(k23.x + ug))) << 16) |
+                     (uint32_t(__clzll(fmix64(k23.y + ug))) << 24)) +
+                    0x01010101u;
+      if (j0 + 4 > J) {  // pad registers are VISITED (stored 0)
         const uint32_t live = J > j0 ? J - j0 : 0;  // < 4
-        pw |= 0xFFFFFFFFu << (8 * live);
+        pw &= ~(0xFFFFFFFFu << (8 * live));
       }
-      row[w] = pw | expand4(vb);
+      row[w] = pw & ~expand4(vb);
       if (prow) prow[w] = pw;
     }
   }
@@ -1022,12 +1024,34 @@ __global__ void k_fill(uint32_t n, uint32_t J, uint32_t Jp, const uint64_t* __re
 }
 
 // ---------------------------------------------------------------- simulate
-// Byte-wise merge of 4 registers: dst takes max(dst, src) on live simulations;
-// VISITED (-1) in dst is absorbing, VISITED in src never wins
-// (engine.cpp:22-53).  bm = 0xFF per live byte.
+// Register bytes are stored as value + 1 (VISITED -1 -> 0, clz values 0..64
+// -> 1..65), so every stored byte is < 128 and a byte-wise max
+// is four SIMD-within-a-register instructions:
+//   t = (x | 0x80) - y per byte (no borrow crosses a byte: 0x80 + x - y >= 1),
+//   bit 7 of t <=> x >= y, replicated over the byte by a sign-extending PRMT.
+// bit 7 of every byte replicated over the byte (PTX prmt sign mode; the
+// __byte_perm intrinsic ignores the selector's sign bit)
+__device__ __forceinline__ uint32_t sign_bytes(uint32_t t) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, 0, 0xBA98;" : "=r"(r) : "r"(t));
+  return r;
+}
+__device__ __forceinline__ uint32_t ge_mask7(uint32_t x, uint32_t y) {
+  return sign_bytes((x | 0x80808080u) - y);
+}
+__device__ __forceinline__ uint32_t max7(uint32_t x, uint32_t y) {
+  const uint32_t m = ge_mask7(x, y);
+  return (x & m) | (y & ~m);
+}
+// 0xFF per non-zero (non-VISITED) byte: b + 0x7F has bit 7 set iff b >= 1
+// (b < 128: no carry leaves the byte).
+__device__ __forceinline__ uint32_t nz_bits7(uint32_t d) { return (d + 0x7F7F7F7Fu) & 0x80808080u; }
+__device__ __forceinline__ uint32_t nz_mask7(uint32_t d) { return sign_bytes(d + 0x7F7F7F7Fu); }
+// dst takes max(dst, src) on live simulations (engine.cpp:22-53): VISITED
+// (0) in dst is absorbing, VISITED in src never wins, dead simulations (bm
+// byte 0) contribute 0.  bm = 0xFF per live byte.
 __device__ __forceinline__ uint32_t merge4(uint32_t d, uint32_t s, uint32_t bm) {
-  const uint32_t sm = (s & bm) | (0x80808080u & ~bm);  // dead sims -> -128, never win
-  return __vmaxs4(d, sm) | __vcmpeq4(d, 0xFFFFFFFFu);   // keep VISITED
+  return max7(d, s & bm & nz_mask7(d));
 }
 __device__ __forceinline__ unsigned long long merge8(unsigned long long d, unsigned long long s,
                                                      uint32_t m8) {
@@ -1269,7 +1293,7 @@ __device__ __forceinline__ void for_frontier_items(const Items& it, const uint32
   }
 }
 
-constexpr unsigned long long kNeg8 = 0x8080808080808080ull;  // "no contribution"
+constexpr unsigned long long kNeg8 = 0;  // "no contribution" (stored bytes are value + 1)
 #ifndef DFS_SOLO_CHUNKS
 #define DFS_SOLO_CHUNKS 16
 #endif
@@ -1279,14 +1303,13 @@ constexpr uint32_t kPullMaxJp = 4096;  // pull accumulators live in shared memor
 
 // Shared-memory running max of the live bytes of one source word.
 __device__ __forceinline__ void acc_max(unsigned long long* a, unsigned long long sv, uint32_t m8) {
-  const uint32_t blo = expand4(m8 & 15u), bhi = expand4(m8 >> 4);
-  const uint32_t slo = (uint32_t(sv) & blo) | (0x80808080u & ~blo);
-  const uint32_t shi = (uint32_t(sv >> 32) & bhi) | (0x80808080u & ~bhi);
+  const uint32_t slo = uint32_t(sv) & expand4(m8 & 15u);
+  const uint32_t shi = uint32_t(sv >> 32) & expand4(m8 >> 4);
   unsigned long long old = *a;
   for (;;) {
     const unsigned long long nv =
-        (static_cast<unsigned long long>(__vmaxs4(uint32_t(old >> 32), shi)) << 32) |
-        __vmaxs4(uint32_t(old), slo);
+        (static_cast<unsigned long long>(max7(uint32_t(old >> 32), shi)) << 32) |
+        max7(uint32_t(old), slo);
     if (nv == old) return;
     const unsigned long long prev = atomicCAS(a, old, nv);
     if (prev == old) return;
@@ -1294,12 +1317,11 @@ __device__ __forceinline__ void acc_max(unsigned long long* a, unsigned long lon
   }
 }
 
-// dst = max(dst, a) bytewise with VISITED dst absorbing (a already masked).
+// dst = max(dst, a) bytewise with VISITED (0) dst absorbing (a already masked).
 __device__ __forceinline__ unsigned long long merge8_full(unsigned long long d,
                                                           unsigned long long a) {
-  const uint32_t lo = __vmaxs4(uint32_t(d), uint32_t(a)) | __vcmpeq4(uint32_t(d), 0xFFFFFFFFu);
-  const uint32_t hi =
-      __vmaxs4(uint32_t(d >> 32), uint32_t(a >> 32)) | __vcmpeq4(uint32_t(d >> 32), 0xFFFFFFFFu);
+  const uint32_t lo = max7(uint32_t(d), uint32_t(a) & nz_mask7(uint32_t(d)));
+  const uint32_t hi = max7(uint32_t(d >> 32), uint32_t(a >> 32) & nz_mask7(uint32_t(d >> 32)));
   return (static_cast<unsigned long long>(hi) << 32) | lo;
 }
 
@@ -1531,6 +1553,10 @@ __device__ __forceinline__ uint32_t simulate_body(const RankDev& r, const SimOpt
             const int wv = w0[q] + 1 + t;
             sx[t] = (wv < 4 && ((mq[q] >> (8 * wv)) & 0xFFu)) ? __ldcg(sp + wv) : 0;
           }
+#ifdef DFS_EXPERIMENTS
+          if (a.dbg & 32)  // timing experiment only: the first acc max twice (a smaller value: no effect)
+            acc_max(&acc[b * 4 + w0[q]], s0[q] & 0xFEFEFEFEFEFEFEFEull, (mq[q] >> (8 * w0[q])) & 0xFFu);
+#endif
           acc_max(&acc[b * 4 + w0[q]], s0[q], (mq[q] >> (8 * w0[q])) & 0xFFu);
 #pragma unroll
           for (int t = 0; t < 3; ++t) {
@@ -1879,14 +1905,17 @@ __device__ __forceinline__ void pin_after_loads(uint4& v) {
 }
 
 // Score lookup table (shared memory): the high words of 256 doubles (the low
-// words are 0), indexed by a register byte: live r <= K -> 2^-r; live r > K ->
-// 2^60 (flags the exact sequential fallback: without it the sum is <= J <
-// 2^50); negative bytes (VISITED) -> 0.0.  32-bit entries: one bank per
-// value, so a warp's lookups are (nearly) conflict-free.
+// words are 0), indexed by a stored register byte c = r + 1: live r <= K ->
+// 2^-r; live r > K -> 2^60 (flags the exact sequential fallback: without it
+// the sum is <= J < 2^50); c = 0 (VISITED) -> 0.0.  32-bit entries: one bank
+// per value, so a warp's lookups are (nearly) conflict-free.
 __device__ __forceinline__ void score_table(uint32_t* tbl, int K) {
   // high word of 2^-b is (1023 - b) << 20 (b <= 64 keeps it normal); 2^60 flags
-  for (int b = threadIdx.x; b < 256; b += blockDim.x)
-    tbl[b] = b >= 128 ? 0u : (b <= K ? uint32_t(1023 - b) << 20 : uint32_t(1023 + 60) << 20);
+  // stored byte c = register value + 1; c == 0: VISITED
+  for (int c = threadIdx.x; c < 256; c += blockDim.x)
+    tbl[c] = (c == 0 || c >= 128) ? 0u
+                                  : (c - 1 <= K ? uint32_t(1023 - (c - 1)) << 20
+                                                : uint32_t(1023 + 60) << 20);
   __syncthreads();
 }
 
@@ -1902,7 +1931,7 @@ __device__ __forceinline__ void score_acc(uint4 v, const uint32_t* tbl, uint32_t
   double p[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    live += __popc(~w[i] & 0x80808080u);
+    live += __popc(nz_bits7(w[i]));
     p[i] = (score_term(tbl, w[i], 0x4440) + score_term(tbl, w[i], 0x4441)) +
            (score_term(tbl, w[i], 0x4442) + score_term(tbl, w[i], 0x4443));
   }
@@ -1928,7 +1957,7 @@ __device__ __forceinline__ void score_body(const int8_t* __restrict__ regs, uint
   uint32_t G = 32;
   while (G > q16) G >>= 1;
   const uint32_t R = 32 / G, sub = lane / G, sl = lane % G;
-  const uint4 kDead = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+  const uint4 kDead = make_uint4(0u, 0u, 0u, 0u);  // all VISITED
   for (uint64_t k0 = gw * 2 * R; k0 < nrows; k0 += nw * 2 * R) {
     uint32_t u[2], live[2] = {0, 0};
     bool ok[2];
@@ -1981,7 +2010,7 @@ __device__ __forceinline__ void score_body(const int8_t* __restrict__ regs, uint
             denom = 0.0;
             const int8_t* rb = regs + uint64_t(u[h]) * Jp;
             for (uint32_t j = 0; j < J; ++j)
-              if (rb[j] >= 0) denom = __dadd_rn(denom, ldexp(1.0, -int(rb[j])));
+              if (rb[j] != 0) denom = __dadd_rn(denom, ldexp(1.0, -(int(uint8_t(rb[j])) - 1)));
           }
           const double lv = double(live[h]);
           sc = __ddiv_rn(__dmul_rn(lv, lv), __dmul_rn(denom, kPhi));
@@ -2268,7 +2297,7 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
         r.vis[uint64_t(s) * W32 + w] |= bits;
         r.fresh[1][uint64_t(s) * W32 + w] = bits;
         int8_t* rb = r.regs + uint64_t(s) * r.Jp + w * 32;
-        for (uint32_t t = bits; t; t &= t - 1) rb[__ffs(t) - 1] = -1;
+        for (uint32_t t = bits; t; t &= t - 1) rb[__ffs(t) - 1] = 0;
         marked += __popc(bits);
         any = true;
       }
@@ -2324,7 +2353,7 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
       const uint32_t nb = cand & ~atomicOr(vw, cand);
       if (!nb) return;
       int8_t* rb = r.regs + uint64_t(v) * r.Jp + b * 32;
-      for (uint32_t t = nb; t; t &= t - 1) rb[__ffs(t) - 1] = -1;
+      for (uint32_t t = nb; t; t &= t - 1) rb[__ffs(t) - 1] = 0;
       atomicOr(fnxt + uint64_t(v) * W32 + b, nb);
       marked += __popc(nb);
       cascade_mark(v, base, stamp, r.cstamp, r.dirty, &r.ctl->dirty_count, r.fwd.row_chunk, rows_n,
@@ -2418,7 +2447,7 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
             if (!nb) continue;
           }
           int8_t* rb = r.regs + uint64_t(v) * r.Jp + b * 32;
-          for (uint32_t t = nb; t; t &= t - 1) rb[__ffs(t) - 1] = -1;
+          for (uint32_t t = nb; t; t &= t - 1) rb[__ffs(t) - 1] = 0;
           if (owner) fnxt[uint64_t(v) * W32 + b] |= nb;
           else atomicOr(fnxt + uint64_t(v) * W32 + b, nb);
           marked += __popc(nb);

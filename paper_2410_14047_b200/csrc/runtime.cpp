@@ -1026,12 +1026,16 @@ void Context::stage_rebuild(uint32_t tau) {
                               " iterations; register monotonicity must be broken");
 }
 
+// Registers are stored on the device as value + 1 per byte (VISITED -1 -> 0,
+// DESIGN.md §2); the stage API speaks the reference's int8 values.
 void Context::stage_get_registers(uint32_t tau, int8_t* out) {
   check_tau(tau, ranks_.size());
   const RankDev& r = ranks_[tau];
   if (!r.n) return;
   DFS_CUDA(cudaMemcpy2DAsync(out, r.J, r.regs, r.Jp, r.J, r.n, cudaMemcpyDeviceToHost, stream_));
   sync();
+  const size_t total = size_t(r.n) * r.J;
+  for (size_t i = 0; i < total; ++i) out[i] = int8_t(uint8_t(out[i]) - 1u);
 }
 
 // VISITED bitset in the reference layout (sketch.hpp:35-87): per row ceil(J/64)
@@ -1057,13 +1061,13 @@ void Context::stage_set_registers(uint32_t tau, const int8_t* in) {
   RankDev& r = ranks_[tau];
   if (!r.n) return;
   // registers + the VISITED bitset mirror + running count (sketch.hpp:35-87)
-  std::vector<int8_t> full(size_t(r.n) * r.Jp, int8_t(-1));
+  std::vector<int8_t> full(size_t(r.n) * r.Jp, int8_t(0));  // stored value + 1: pads VISITED
   std::vector<uint32_t> vis(size_t(r.n) * r.W32, 0);
   uint64_t visited = 0;
   for (uint32_t u = 0; u < r.n; ++u)
     for (uint32_t j = 0; j < r.J; ++j) {
       const int8_t v = in[size_t(u) * r.J + j];
-      full[size_t(u) * r.Jp + j] = v;
+      full[size_t(u) * r.Jp + j] = int8_t(uint8_t(v) + 1u);
       if (v == -1) {
         vis[size_t(u) * r.W32 + j / 32] |= 1u << (j % 32);
         ++visited;
