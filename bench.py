@@ -49,6 +49,10 @@ CONFIGS = {
     "c4": ("rmat", 26, 1_000_000_000, "const:0.005", 1024, 100,
            "C4: R-MAT scale-26 (1B edges), IC p=0.005, R=1024, K=100"),
 }
+# BASELINE configs[4]: register-count / simulation sweep on the scale-23 graph
+for _r in (64, 128, 256, 512, 1024, 2048, 4096):
+    CONFIGS[f"c5_r{_r}"] = ("rmat", 23, 100_000_000, "const:0.01", _r, 50,
+                            f"C5 sweep: R-MAT scale-23 (100M edges), IC p=0.01, R={_r}, K=50")
 SEED = 7
 
 
