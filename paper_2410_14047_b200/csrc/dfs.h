@@ -152,6 +152,10 @@ struct RunCtl {
   unsigned int snap_dirty;        // dirty rows left by the last cascade (all partitions)
   unsigned int pad;
   double oldscore;
+  // Parked-grid rounds (one partition, no peers): blocks other than block 0
+  // wait on park_seq while block 0 runs rounds alone; block 0 wakes them with
+  // (reason, round, stamp base) when a round needs the grid.
+  unsigned int park_seq, park_reason, park_step, park_base;
 };
 
 struct RunArrays {

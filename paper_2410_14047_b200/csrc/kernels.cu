@@ -2252,7 +2252,25 @@ struct CasOpts {
   int dbg;
   int pull_f;
   int cnt;  // count mode: tally the reference-schedule cascade work units
+  // parked-grid rounds (k_run, one partition): block 0 wakes the parked
+  // blocks when the cascade first needs the grid (unless *awake), and defers
+  // the final release to the caller (episode returned in *defer_e)
+  RunCtl* park = nullptr;
+  uint32_t step = 0;
+  uint32_t* awake = nullptr;
+  uint32_t* defer_e = nullptr;
 };
+
+constexpr unsigned int kWakeSelect = 1, kWakeCascade = 2, kWakeRebuild = 3, kWakeDone = 4;
+// Block 0, thread 0: wake the parked blocks with (reason, round, stamp base).
+__device__ __forceinline__ void park_wake(RunCtl* c, unsigned int reason, uint32_t step,
+                                          uint32_t base) {
+  c->park_reason = reason;
+  c->park_step = step;
+  c->park_base = base;
+  __threadfence();
+  atomicAdd(&c->park_seq, 1u);
+}
 
 // `base` as in simulate_body; returns the next stamp base.  CNT: count mode
 // (a compile-time switch: its bookkeeping stays out of the timed variant's
@@ -2536,9 +2554,17 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
       }
       __syncthreads();
       if (threadIdx.x == 0) {
-        __threadfence();
-        atomicExch(&r.ctl->release, (static_cast<unsigned long long>(base) << 32) |
-                                        (uint64_t(e & 0xFFFu) << 20) | (uint64_t(L) << 2) | code);
+        if (code == 0 && a.park && !*a.awake) {  // parked blocks join for the grid levels
+          park_wake(a.park, kWakeCascade, a.step, base);
+          *a.awake = 1;
+        }
+        if (code == 1 && a.defer_e) {
+          *a.defer_e = e;  // the caller publishes the final release after its round end
+        } else {
+          __threadfence();
+          atomicExch(&r.ctl->release, (static_cast<unsigned long long>(base) << 32) |
+                                          (uint64_t(e & 0xFFFu) << 20) | (uint64_t(L) << 2) | code);
+        }
       }
     } else {
       if (threadIdx.x == 0) {
@@ -2560,6 +2586,11 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
     for (;;) {  // grid-wide levels while the frontier is large
       if (qchunks(qc, L % 4) <= kSoloChunks) break;
       level(L, false);
+      // VISITED counts of the grid levels land before the barrier, so block 0
+      // holds the complete count when the cascade ends in its solo episode
+      for (int o = 16; o; o >>= 1) marked += __shfl_xor_sync(0xffffffffu, marked, o);
+      if (lane == 0 && marked) atomicAdd(&r.ctl->visited, marked);
+      marked = 0;
       grid.sync();
       ++L;
     }
@@ -2721,22 +2752,29 @@ __device__ __forceinline__ double peer_reduced(const PeerView& pv, uint32_t v) {
 }
 
 // Out-of-line phase bodies keep the register allocation of each phase local.
+#ifndef DFS_PHASE_INLINE
+#define DFS_PHASE_INLINE __noinline__
+#endif
 template <int JAC, int CNT>
-__device__ __noinline__ uint32_t run_simulate(const RankDev& r, const SimOpts& o, WarpStage* stage,
+__device__ DFS_PHASE_INLINE uint32_t run_simulate(const RankDev& r, const SimOpts& o, WarpStage* stage,
                                               unsigned long long& s_release,
                                               unsigned long long* dyn, uint32_t base) {
   cg::grid_group grid = cg::this_grid();
   return simulate_body<JAC, CNT>(r, o, grid, stage, s_release, dyn, base);
 }
 template <int CNT>
-__device__ __noinline__ uint32_t run_cascade(const RankDev& r, const CasOpts& o, WarpStage* stage,
+__device__ DFS_PHASE_INLINE uint32_t run_cascade(const RankDev& r, const CasOpts& o, WarpStage* stage,
                                              unsigned long long& s_release, uint32_t* dyn,
                                              uint32_t base) {
   cg::grid_group grid = cg::this_grid();
   return cascade_body<CNT>(r, o, grid, stage, s_release, dyn, base);
 }
 
-template <int JAC, int CNT>
+// PARKED: the parked-grid round loop (one partition, no peers); else the
+// general loop (several partitions on this GPU, or peer mode).  Separate
+// instantiations keep each loop's live state out of the other's register
+// allocation (the phase bodies are out-of-line calls).
+template <int JAC, int CNT, int PARKED>
 __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
   __shared__ WarpStage stage[kWarps];
   __shared__ unsigned long long s_release;
@@ -2751,17 +2789,31 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
   for (uint32_t t = threadIdx.x; t < a.mu; t += blockDim.x) s_tick[t] = ld_volatile(&a.ranks[t].ctl->tick);
   __syncthreads();
   const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
-  unsigned long long t0 = timer ? global_ns() : 0;
+  // Loop-carried per-block state lives in shared memory: the phase bodies
+  // are out-of-line calls, and every register the caller keeps live across
+  // them is one the (interprocedurally allocated) callee cannot use.
+  __shared__ unsigned long long s_t0;
+  __shared__ uint32_t s_cur_rank, s_first_fill;
+  if (threadIdx.x == 0) {
+    s_t0 = timer ? global_ns() : 0;
+    s_cur_rank = 0xFFFFFFFFu;
+    s_first_fill = 1;
+  }
+  __syncthreads();
   auto phase = [&](int which) {
     if (timer) {
       const unsigned long long t1 = global_ns();
-      a.phase_ns[which] += t1 - t0;
-      t0 = t1;
+      a.phase_ns[which] += t1 - s_t0;
+      s_t0 = t1;
     }
   };
-  auto load_rank = [&](uint32_t t) {
+  auto load_rank = [&](uint32_t t) {  // s_r is never modified once loaded
+    if (t == s_cur_rank) return;
     __syncthreads();
-    if (threadIdx.x == 0) s_r = a.ranks[t];
+    if (threadIdx.x == 0) {
+      s_r = a.ranks[t];
+      s_cur_rank = t;
+    }
     __syncthreads();
   };
   const SimOpts so{a.cap, a.dbg, a.sim_pull_f};
@@ -2778,14 +2830,15 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
       for (uint32_t t = 0; t + st < a.mu; t += 2 * st) acc[t] = __dadd_rn(acc[t], acc[t + st]);
     a.reduced[v] = acc[0];
   };
-  bool first_fill = true;  // the first fill ran as a separate full-occupancy launch
+  // (s_first_fill: the first fill ran as a separate full-occupancy launch)
   auto rebuild = [&]() {  // fill -> simulate -> full rescore, every partition
-    if (!first_fill)
+    if (!s_first_fill)
       for (uint32_t t = 0; t < a.mu; ++t) {
         load_rank(t);
         fill_body(s_r.n, s_r.J, s_r.Jp, s_r.jkey, s_r.vis, s_r.regs, s_r.ctl, s_r.pristine, true);
       }
-    first_fill = false;
+    __syncthreads();
+    if (threadIdx.x == 0) s_first_fill = 0;
     grid.sync();
     phase(0);
     for (uint32_t t = 0; t < a.mu; ++t) {
@@ -2823,6 +2876,173 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
   const uint32_t phi = a.peer ? min(a.n, plo + pslice) : 0;
   const uint32_t pnseg = (phi - plo + kSeg - 1) / kSeg;  // slice segments (peer mode)
   const bool tr = (a.dbg & 4) && blockIdx.x == 0 && threadIdx.x == 0;  // DFS_DBG bit 2
+  // select (runtime.cpp:88-121) through the argmax cache.  Small dirty sets:
+  // block 0 rescores them, refreshes their segments and picks the winner with
+  // block barriers only (select_solo, block 0 alone); larger ones run
+  // grid-wide (select_grid, every block).
+  auto select_solo = [&](uint32_t step, bool was_rebuilt) {
+    if (tr) trace(6, step, 0);
+    if (!was_rebuilt) {
+      for (uint32_t t = 0; t < a.mu; ++t) {
+        load_rank(t);
+        score_body(s_r.regs, s_r.n, s_r.J, s_r.Jp, a.K, 0, s_r.dirty, s_r.ctl, s_r.scores,
+                   reinterpret_cast<uint32_t*>(dyn_smem), true);
+      }
+      __syncthreads();
+      if (a.mu > 1) {  // rows dirty in any partition: new binomial sums
+        for (uint32_t t = 0; t < a.mu; ++t) {
+          const RankDev& rt = a.ranks[t];
+          const uint32_t c = ld_volatile(&rt.ctl->dirty_count);
+          for (uint32_t i = threadIdx.x; i < c; i += blockDim.x) reduce_row(__ldcg(rt.dirty + i));
+        }
+        __syncthreads();
+      }
+      if (tr) trace(5, step, 0);
+      // duplicates of one segment compute identical values (benign)
+      for (uint32_t t = 0; t < a.mu; ++t) {
+        const RankDev& rt = a.ranks[t];
+        const uint32_t c = ld_volatile(&rt.ctl->dirty_count);
+        for (uint32_t i = threadIdx.x >> 5; i < c; i += kWarps)
+          seg_recompute(segsrc, a.n, __ldcg(rt.dirty + i) / kSeg, a.ra);
+      }
+      __syncthreads();
+      if (tr) trace(6, step, 1);
+    }
+    const Best t = seg_combine(a.ra, sb, a.ra.nseg);
+    if (threadIdx.x == 0) commit_choice(t, a.ra);
+    __syncthreads();
+    if (tr) trace(7, step, ld_volatile(&a.ra.ctl->choice));
+  };
+  auto select_grid = [&](uint32_t step) {
+    for (uint32_t t = 0; t < a.mu; ++t) {
+      load_rank(t);
+      score_body(s_r.regs, s_r.n, s_r.J, s_r.Jp, a.K, 0, s_r.dirty, s_r.ctl, s_r.scores,
+                 reinterpret_cast<uint32_t*>(dyn_smem));
+    }
+    grid.sync();
+    const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t gthreads = uint64_t(gridDim.x) * blockDim.x;
+    if (a.mu > 1) {
+      for (uint32_t t = 0; t < a.mu; ++t) {
+        const RankDev& rt = a.ranks[t];
+        const uint32_t c = ld_volatile(&rt.ctl->dirty_count);
+        for (uint64_t i = gtid; i < c; i += gthreads) reduce_row(__ldcg(rt.dirty + i));
+      }
+      grid.sync();
+    }
+    const uint64_t gw = gtid >> 5, nw = gthreads >> 5;
+    const uint32_t stampv = step + 1;
+    for (uint32_t t = 0; t < a.mu; ++t) {
+      const RankDev& rt = a.ranks[t];
+      const uint32_t c = ld_volatile(&rt.ctl->dirty_count);
+      for (uint64_t i = gw; i < c; i += nw) {
+        const uint32_t sg = __ldcg(rt.dirty + i) / kSeg;
+        unsigned prev = 0;
+        if (lane_id() == 0) prev = atomicExch(&a.ra.seg_stamp[sg], stampv);
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        if (prev != stampv) seg_recompute(segsrc, a.n, sg, a.ra);
+      }
+    }
+    grid.sync();
+    if (blockIdx.x == 0) {
+      const Best t = seg_combine(a.ra, sb, a.ra.nseg);
+      if (threadIdx.x == 0) commit_choice(t, a.ra);
+      __syncthreads();
+    }
+  };
+  // Parked-grid rounds (one partition, no peers): the other blocks park on
+  // park_seq while block 0 runs whole rounds alone (solo select, solo cascade
+  // levels, round end) without grid barriers; block 0 wakes them with the
+  // round and stamp base when a round needs the grid (a large dirty set, a
+  // large cascade level, a rebuild) and once at the end.  A round of C2's
+  // tail (a few solo cascade levels) costs one block's work instead of two
+  // grid barriers plus the release hand-offs.
+  if (PARKED) {
+    __shared__ uint32_t s_awake, s_defer_e, s_wake[4];
+    if (blockIdx.x != 0) {
+      uint32_t seen = 0;
+      for (;;) {
+        if (threadIdx.x == 0) {
+          uint32_t v;
+          for (;;) {
+            v = ld_volatile(&a.ra.ctl->park_seq);
+            if (v != seen) break;
+            __nanosleep(128);
+          }
+          __threadfence();
+          s_wake[0] = ld_volatile(&a.ra.ctl->park_reason);
+          s_wake[1] = ld_volatile(&a.ra.ctl->park_step);
+          s_wake[3] = v;
+          s_tick[0] = ld_volatile(&a.ra.ctl->park_base);
+        }
+        __syncthreads();
+        const uint32_t reason = s_wake[0], step = s_wake[1];
+        seen = s_wake[3];
+        __syncthreads();
+        if (reason == kWakeDone) break;
+        if (reason == kWakeRebuild) {
+          rebuild();
+          continue;
+        }
+        if (reason == kWakeSelect) select_grid(step);
+        load_rank(0);
+        const CasOpts co{&a.ra.ctl->choice, 0, a.dbg, a.cas_pull_f, CNT};
+        const uint32_t nt =
+            run_cascade<CNT>(s_r, co, stage, s_release, reinterpret_cast<uint32_t*>(dyn_smem), s_tick[0]);
+        if (threadIdx.x == 0) s_tick[0] = nt;  // (the next wake sets it again)
+      }
+      return;
+    }
+    for (uint32_t step = 0; step < a.k; ++step) {
+      const uint32_t nd = rebuilt ? 0u : ld_volatile(&a.ra.ctl->snap_dirty);
+      if (tr) trace(4, step, nd);
+      bool awake = false;
+      if (nd <= kSoloDirty) {
+        select_solo(step, rebuilt);
+      } else {
+        if (threadIdx.x == 0) park_wake(a.ra.ctl, kWakeSelect, step, s_tick[0]);
+        awake = true;
+        select_grid(step);
+      }
+      rebuilt = false;
+      phase(2);
+      load_rank(0);
+      if (threadIdx.x == 0) {
+        s_awake = awake ? 1u : 0u;
+        s_defer_e = 0;
+      }
+      __syncthreads();
+      const uint32_t base = s_tick[0];
+      CasOpts co{&a.ra.ctl->choice, 0, a.dbg, a.cas_pull_f, CNT};
+      co.park = a.ra.ctl;
+      co.step = step;
+      co.awake = &s_awake;
+      co.defer_e = &s_defer_e;
+      const uint32_t nt =
+          run_cascade<CNT>(s_r, co, stage, s_release, reinterpret_cast<uint32_t*>(dyn_smem), base);
+      __syncthreads();  // block 0's VISITED counts are in (each warp adds at the cascade end)
+      if (threadIdx.x == 0) {
+        s_tick[0] = nt;
+        a.ra.ctl->snap_dirty = ld_volatile(&a.ranks[0].ctl->dirty_count);
+        round_end_covered(a.ra, ld_volatile(&a.ranks[0].ctl->visited), a.k, a.R, a.eps);
+        // blocks that joined this round's cascade leave it now (deferred release)
+        __threadfence();
+        atomicExch(&a.ranks[0].ctl->release,
+                   (static_cast<unsigned long long>(base) << 32) |
+                       (uint64_t(s_defer_e & 0xFFFu) << 20) | (uint64_t(nt - base - 2) << 2) | 1ull);
+      }
+      __syncthreads();
+      phase(3);
+      if (step + 1 < a.k && ld_volatile(&a.ra.ctl->rebuild_now)) {
+        if (threadIdx.x == 0) park_wake(a.ra.ctl, kWakeRebuild, step, s_tick[0]);
+        rebuild();
+        phase(2);
+        rebuilt = true;
+      }
+    }
+    if (threadIdx.x == 0) park_wake(a.ra.ctl, kWakeDone, a.k, 0);
+    return;
+  } else {
   for (uint32_t step = 0; step < a.k; ++step) {
     if (tr) trace(4, step, 0);
     if (segs) {
@@ -2833,72 +3053,9 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
       // dirty rows over all partitions (snapshot of the previous round end)
       const uint32_t nd = rebuilt ? 0u : ld_volatile(&a.ra.ctl->snap_dirty);
       if (nd <= kSoloDirty) {
-        if (blockIdx.x == 0) {
-          if (!rebuilt) {
-            for (uint32_t t = 0; t < a.mu; ++t) {
-              load_rank(t);
-              score_body(s_r.regs, s_r.n, s_r.J, s_r.Jp, a.K, 0, s_r.dirty, s_r.ctl, s_r.scores,
-                         reinterpret_cast<uint32_t*>(dyn_smem), true);
-            }
-            __syncthreads();
-            if (a.mu > 1) {  // rows dirty in any partition: new binomial sums
-              for (uint32_t t = 0; t < a.mu; ++t) {
-                const RankDev& rt = a.ranks[t];
-                const uint32_t c = ld_volatile(&rt.ctl->dirty_count);
-                for (uint32_t i = threadIdx.x; i < c; i += blockDim.x) reduce_row(__ldcg(rt.dirty + i));
-              }
-              __syncthreads();
-            }
-            // duplicates of one segment compute identical values (benign)
-            for (uint32_t t = 0; t < a.mu; ++t) {
-              const RankDev& rt = a.ranks[t];
-              const uint32_t c = ld_volatile(&rt.ctl->dirty_count);
-              for (uint32_t i = threadIdx.x >> 5; i < c; i += kWarps)
-                seg_recompute(segsrc, a.n, __ldcg(rt.dirty + i) / kSeg, a.ra);
-            }
-            __syncthreads();
-          }
-          const Best t = seg_combine(a.ra, sb, a.ra.nseg);
-          if (threadIdx.x == 0) commit_choice(t, a.ra);
-          __syncthreads();
-          if (tr) trace(7, step, ld_volatile(&a.ra.ctl->choice));
-        }
+        if (blockIdx.x == 0) select_solo(step, rebuilt);
       } else {
-        for (uint32_t t = 0; t < a.mu; ++t) {
-          load_rank(t);
-          score_body(s_r.regs, s_r.n, s_r.J, s_r.Jp, a.K, 0, s_r.dirty, s_r.ctl, s_r.scores,
-                     reinterpret_cast<uint32_t*>(dyn_smem));
-        }
-        grid.sync();
-        const uint64_t gtid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-        const uint64_t gthreads = uint64_t(gridDim.x) * blockDim.x;
-        if (a.mu > 1) {
-          for (uint32_t t = 0; t < a.mu; ++t) {
-            const RankDev& rt = a.ranks[t];
-            const uint32_t c = ld_volatile(&rt.ctl->dirty_count);
-            for (uint64_t i = gtid; i < c; i += gthreads) reduce_row(__ldcg(rt.dirty + i));
-          }
-          grid.sync();
-        }
-        const uint64_t gw = gtid >> 5, nw = gthreads >> 5;
-        const uint32_t stampv = step + 1;
-        for (uint32_t t = 0; t < a.mu; ++t) {
-          const RankDev& rt = a.ranks[t];
-          const uint32_t c = ld_volatile(&rt.ctl->dirty_count);
-          for (uint64_t i = gw; i < c; i += nw) {
-            const uint32_t sg = __ldcg(rt.dirty + i) / kSeg;
-            unsigned prev = 0;
-            if (lane_id() == 0) prev = atomicExch(&a.ra.seg_stamp[sg], stampv);
-            prev = __shfl_sync(0xffffffffu, prev, 0);
-            if (prev != stampv) seg_recompute(segsrc, a.n, sg, a.ra);
-          }
-        }
-        grid.sync();
-        if (blockIdx.x == 0) {
-          const Best t = seg_combine(a.ra, sb, a.ra.nseg);
-          if (threadIdx.x == 0) commit_choice(t, a.ra);
-          __syncthreads();
-        }
+        select_grid(step);
       }
       rebuilt = false;
       // the cascade's commit (block 0, warp 0) reads the choice; the other
@@ -3014,6 +3171,7 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
       rebuilt = true;
     }
   }
+  }  // !PARKED
 }
 
 // ================================================================= launchers
@@ -3336,16 +3494,20 @@ static const void* sim_kernel(int variant) {
   }
 }
 
+// variants 0-2: general loop (async, Jacobi, Jacobi + count); 3-5: parked
 static const void* run_kernel(int variant) {
   switch (variant) {
-    case 0: return (const void*)k_run<0, 0>;
-    case 1: return (const void*)k_run<1, 0>;
-    default: return (const void*)k_run<1, 1>;
+    case 0: return (const void*)k_run<0, 0, 0>;
+    case 1: return (const void*)k_run<1, 0, 0>;
+    case 2: return (const void*)k_run<1, 1, 0>;
+    case 3: return (const void*)k_run<0, 0, 1>;
+    case 4: return (const void*)k_run<1, 0, 1>;
+    default: return (const void*)k_run<1, 1, 1>;
   }
 }
 
 int coop_grid(int which, int variant) {
-  static int g[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  static int g[16] = {};
   const int slot = which == 0 ? variant : which == 1 ? 3 : 4 + variant;
   if (!g[slot]) {
     int per = 0;
@@ -3433,7 +3595,7 @@ void launch_run(const RankDev* ranks_dev, uint32_t mu, uint32_t k, uint32_t R, u
   RunArgs a{ranks_dev, mu, k, R, n, eps, cap, dbg, spf, cpf, K, ra, parts, ctls, reduced, phase_ns,
             peer ? 1 : 0, peer ? *peer : PeerView{}};
   void* args[] = {&a};
-  const int variant = jacobi ? (count ? 2 : 1) : 0;
+  const int variant = (jacobi ? (count ? 2 : 1) : 0) + (mu == 1 && !peer ? 3 : 0);
   // Ranks sharing one device (single-GPU tests of the peer protocol) split
   // its SMs so that all their persistent grids are co-resident.
   const int share = grid_share > 1 ? grid_share : 1;
