@@ -74,6 +74,7 @@ typedef struct dfs_stats {
   uint32_t max_sweeps;   /* most simulate sweeps of one convergence */
   uint32_t rerun_jacobi; /* 1: a convergence came near sim_cap; the run was decided by the
                             reference's Jacobi schedule (engine.cpp:88-96) */
+  uint64_t rescored_rows; /* rows actually rescored (full passes after fills + dirty rows) */
 } dfs_stats;
 
 const char *dfs_last_error(void);

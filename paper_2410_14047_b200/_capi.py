@@ -48,7 +48,7 @@ class Stats(C.Structure):
                 ("m", C.c_uint64), ("cnt_cas_rows", C.c_uint64), ("cnt_cas_edges", C.c_uint64),
                 ("cnt_cascades", C.c_uint64), ("run_kernel", C.c_double),
                 ("item_density", C.c_double), ("max_sweeps", C.c_uint32),
-                ("rerun_jacobi", C.c_uint32)]
+                ("rerun_jacobi", C.c_uint32), ("rescored_rows", C.c_uint64)]
 
 
 class ReportFields(C.Structure):

@@ -280,6 +280,7 @@ int dfs_last_stats(const dfs_ctx* ctx, dfs_stats* out) {
     out->item_density = r.item_density;
     out->max_sweeps = r.max_sweeps;
     out->rerun_jacobi = r.rerun_jacobi ? 1u : 0u;
+    out->rescored_rows = r.rescored_rows;
   });
 }
 

@@ -106,6 +106,9 @@ struct RankCtl {
   // cascade work units of the reference schedule (count mode): frontier rows
   // summed over levels, device-graph edges out of them, cascades started
   unsigned long long cnt_cas_rows, cnt_cas_edges, cnt_cascades;
+  // rows this run actually rescored (full passes after fills + dirty rows):
+  // the performed score work, next to the reference schedule's K full passes
+  unsigned long long rescored_rows;
 };
 
 // Work queues used by the persistent simulate / cascade kernels.  Rotating

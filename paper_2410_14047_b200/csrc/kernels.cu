@@ -1946,6 +1946,8 @@ __device__ __forceinline__ void score_body(const int8_t* __restrict__ regs, uint
                                            bool block_only = false) {
   score_table(tbl, K);
   const uint32_t nrows = full ? n : ld_volatile(&ctl->dirty_count);
+  if (threadIdx.x == 0 && (block_only || blockIdx.x == 0) && ctl)
+    atomicAdd(&ctl->rescored_rows, (unsigned long long)nrows);
   const unsigned lane = lane_id();
   const uint64_t nw = block_only ? kWarps : (uint64_t(gridDim.x) * blockDim.x) >> 5;
   const uint64_t gw = block_only ? threadIdx.x >> 5

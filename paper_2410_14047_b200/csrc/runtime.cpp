@@ -741,6 +741,7 @@ Report Context::run_impl(const RunConfig& cfg, const HostGraph* host_w_src, bool
     rep.cnt_cas_rows += c.cnt_cas_rows;
     rep.cnt_cas_edges += c.cnt_cas_edges;
     rep.cnt_cascades += c.cnt_cascades;
+    rep.rescored_rows += c.rescored_rows;
   }
   for (uint32_t sd : rep.seeds_dense) rep.seeds.push_back(orig_id_[sd]);
   // comms counters of the reference's collective schedule (collectives.cpp:

@@ -80,6 +80,7 @@ struct Report {  // runtime.hpp:29-41
   // reference-schedule units (count mode), summed over ranks and convergences
   uint64_t cnt_edges = 0, cnt_batches = 0, cnt_touched = 0, cnt_sweeps = 0, cnt_convergences = 0;
   uint64_t cnt_cas_rows = 0, cnt_cas_edges = 0, cnt_cascades = 0;
+  uint64_t rescored_rows = 0;   // rows actually rescored (all partitions)
   double run_kernel = 0;        // seconds of the k_run launch (CUDA events on the stream)
   double item_density = 0;      // live simulations per forward item (partition 0)
   uint64_t launches = 0;        // kernels launched by run()

@@ -58,12 +58,13 @@ def _ref_graph(ref, g, tmp_path, name):
 
 
 # ------------------------------------------------------------ bench workloads
-@pytest.mark.parametrize("cfg", ["c2", "c3ic", "c3"])
+@pytest.mark.parametrize("cfg", ["c2", "c3ic", "c3", "c4s24"])
 def test_bench_workload_reports_match_reference(D, cfg):
     """C2 (16M edges) and the north star (100M edges, IC p=0.01, R=1024, K=50)
     exactly as benched, at every devices value the reference was run with
     (devices=1 is the bench's own setting), plus C3 (weighted cascade, R=1024,
-    36 rebuilds) where recorded."""
+    36 rebuilds) and the C4-shaped scale-24 graph (250M edges, IC p=0.005,
+    R=1024, K=100, 8 partitions) where recorded."""
     gold = _golden(cfg) if cfg in json.load(open(bench.GOLDEN)) else None
     if gold is None or not gold["reports"]:
         pytest.skip(f"no reference report recorded for {cfg}")
@@ -232,3 +233,26 @@ def test_reference_python_smoke_suite_unchanged():
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
     assert "7 passed" in out.stdout, out.stdout[-1000:]
+
+
+def test_c5_sweep_reports_match_reference(D):
+    """BASELINE configs[4] (R = 64..4096 on the scale-23 graph): every (R,
+    devices) the reference was run with, including the degraded plans (J < 32:
+    R = 64, 128 at devices 8; R <= 256 at devices 16)."""
+    with open(bench.GOLDEN) as f:
+        gold = json.load(f)
+    cases = sorted((int(name[4:]), int(d), rep) for name, e in gold.items()
+                   if name.startswith("c5_r") for d, rep in e["reports"].items())
+    if not cases:
+        pytest.skip("no C5 reference reports recorded")
+    gen, a, m, wspec, r0, k, _ = bench.CONFIGS["c5_r1024"]
+    g = D.generate(gen, a, m, bench.SEED)
+    ctx = D.Context(0)
+    ctx.upload(g)
+    degraded = 0
+    for r, devices, want in cases:
+        got = ctx.run_json(None, k=k, r=r, devices=devices, weights=wspec, seed=bench.SEED,
+                           timings=False, resident=True)
+        assert _strip(got) == json.loads(want), (r, devices)
+        degraded += json.loads(want)["degraded_plan"]
+    assert degraded >= 4

@@ -72,6 +72,7 @@ for devices, rs in plan:
                             "launch_ms": round(kr * 1e3, 3),
                             "achieved_gbs": round(alg["run_bytes"] / kr / 1e9, 1),
                             "frac": round(alg["run_bytes"] / kr / 1e9 / peak, 4),
+                            "frac_performed": round(alg["run_bytes_performed"] / kr / 1e9 / peak, 4),
                             "simulate_frac": round(alg["bytes_per_launch"] / per_conv / 1e9 / peak
                                                    if per_conv > 0 else 0.0, 4),
                             "peak_gbs": peak, "peak_source": peak_kind},
