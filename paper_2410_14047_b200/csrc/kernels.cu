@@ -2868,7 +2868,6 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
       grid.sync();
     }
   };
-  rebuild();
   bool rebuilt = true;
   // peer mode: this rank reduces and searches the id slice [plo, phi)
   unsigned long long ep = a.peer ? ld_volatile(&a.pv.box[a.pv.rank]->arrive) : 0;
@@ -2961,9 +2960,20 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
   // grid barriers plus the release hand-offs.
   if (PARKED) {
     __shared__ uint32_t s_awake, s_defer_e, s_wake[4];
-    if (blockIdx.x != 0) {
-      uint32_t seen = 0;
-      for (;;) {
+    // Every block executes rebuild() at ONE call site (the interprocedural
+    // register allocation of the out-of-line simulate phase depends on its
+    // call sites): the loop starts with the initial build for everyone, and
+    // block 0 breaks out of its solo rounds when a rebuild is due.
+    uint32_t seen = 0, step0 = 0;
+    bool rebuilt = true;
+    uint32_t reason = kWakeRebuild;  // the initial fill -> simulate -> score
+    for (;;) {
+      if (reason == kWakeRebuild) {
+        rebuild();
+        if (blockIdx.x == 0 && step0) phase(2);
+        rebuilt = true;
+      }
+      if (blockIdx.x != 0) {
         if (threadIdx.x == 0) {
           uint32_t v;
           for (;;) {
@@ -2978,73 +2988,78 @@ __global__ void __launch_bounds__(kThreads, DFS_SIM_MINB) k_run(RunArgs a) {
           s_tick[0] = ld_volatile(&a.ra.ctl->park_base);
         }
         __syncthreads();
-        const uint32_t reason = s_wake[0], step = s_wake[1];
+        reason = s_wake[0];
+        const uint32_t step = s_wake[1];
         seen = s_wake[3];
         __syncthreads();
         if (reason == kWakeDone) break;
-        if (reason == kWakeRebuild) {
-          rebuild();
-          continue;
-        }
+        if (reason == kWakeRebuild) continue;
         if (reason == kWakeSelect) select_grid(step);
         load_rank(0);
         const CasOpts co{&a.ra.ctl->choice, 0, a.dbg, a.cas_pull_f, CNT};
         const uint32_t nt =
             run_cascade<CNT>(s_r, co, stage, s_release, reinterpret_cast<uint32_t*>(dyn_smem), s_tick[0]);
         if (threadIdx.x == 0) s_tick[0] = nt;  // (the next wake sets it again)
+        continue;
       }
-      return;
-    }
-    for (uint32_t step = 0; step < a.k; ++step) {
-      const uint32_t nd = rebuilt ? 0u : ld_volatile(&a.ra.ctl->snap_dirty);
-      if (tr) trace(4, step, nd);
-      bool awake = false;
-      if (nd <= kSoloDirty) {
-        select_solo(step, rebuilt);
-      } else {
-        if (threadIdx.x == 0) park_wake(a.ra.ctl, kWakeSelect, step, s_tick[0]);
-        awake = true;
-        select_grid(step);
-      }
-      rebuilt = false;
-      phase(2);
-      load_rank(0);
-      if (threadIdx.x == 0) {
-        s_awake = awake ? 1u : 0u;
-        s_defer_e = 0;
-      }
-      __syncthreads();
-      const uint32_t base = s_tick[0];
-      CasOpts co{&a.ra.ctl->choice, 0, a.dbg, a.cas_pull_f, CNT};
-      co.park = a.ra.ctl;
-      co.step = step;
-      co.awake = &s_awake;
-      co.defer_e = &s_defer_e;
-      const uint32_t nt =
-          run_cascade<CNT>(s_r, co, stage, s_release, reinterpret_cast<uint32_t*>(dyn_smem), base);
-      __syncthreads();  // block 0's VISITED counts are in (each warp adds at the cascade end)
-      if (threadIdx.x == 0) {
-        s_tick[0] = nt;
-        a.ra.ctl->snap_dirty = ld_volatile(&a.ranks[0].ctl->dirty_count);
-        round_end_covered(a.ra, ld_volatile(&a.ranks[0].ctl->visited), a.k, a.R, a.eps);
-        // blocks that joined this round's cascade leave it now (deferred release)
-        __threadfence();
-        atomicExch(&a.ranks[0].ctl->release,
-                   (static_cast<unsigned long long>(base) << 32) |
-                       (uint64_t(s_defer_e & 0xFFFu) << 20) | (uint64_t(nt - base - 2) << 2) | 1ull);
-      }
-      __syncthreads();
-      phase(3);
-      if (step + 1 < a.k && ld_volatile(&a.ra.ctl->rebuild_now)) {
-        if (threadIdx.x == 0) park_wake(a.ra.ctl, kWakeRebuild, step, s_tick[0]);
-        rebuild();
+      // block 0: rounds until a rebuild is due or the loop ends
+      reason = kWakeDone;
+      for (; step0 < a.k; ++step0) {
+        const uint32_t step = step0;
+        const uint32_t nd = rebuilt ? 0u : ld_volatile(&a.ra.ctl->snap_dirty);
+        if (tr) trace(4, step, nd);
+        bool awake = false;
+        if (nd <= kSoloDirty) {
+          select_solo(step, rebuilt);
+        } else {
+          if (threadIdx.x == 0) park_wake(a.ra.ctl, kWakeSelect, step, s_tick[0]);
+          awake = true;
+          select_grid(step);
+        }
+        rebuilt = false;
         phase(2);
-        rebuilt = true;
+        load_rank(0);
+        if (threadIdx.x == 0) {
+          s_awake = awake ? 1u : 0u;
+          s_defer_e = 0;
+        }
+        __syncthreads();
+        const uint32_t base = s_tick[0];
+        CasOpts co{&a.ra.ctl->choice, 0, a.dbg, a.cas_pull_f, CNT};
+        co.park = a.ra.ctl;
+        co.step = step;
+        co.awake = &s_awake;
+        co.defer_e = &s_defer_e;
+        const uint32_t nt =
+            run_cascade<CNT>(s_r, co, stage, s_release, reinterpret_cast<uint32_t*>(dyn_smem), base);
+        __syncthreads();  // block 0's VISITED counts are in (each warp adds at the cascade end)
+        if (threadIdx.x == 0) {
+          s_tick[0] = nt;
+          a.ra.ctl->snap_dirty = ld_volatile(&a.ranks[0].ctl->dirty_count);
+          round_end_covered(a.ra, ld_volatile(&a.ranks[0].ctl->visited), a.k, a.R, a.eps);
+          // blocks that joined this round's cascade leave it now (deferred release)
+          __threadfence();
+          atomicExch(&a.ranks[0].ctl->release,
+                     (static_cast<unsigned long long>(base) << 32) |
+                         (uint64_t(s_defer_e & 0xFFFu) << 20) | (uint64_t(nt - base - 2) << 2) | 1ull);
+        }
+        __syncthreads();
+        phase(3);
+        if (step + 1 < a.k && ld_volatile(&a.ra.ctl->rebuild_now)) {
+          if (threadIdx.x == 0) park_wake(a.ra.ctl, kWakeRebuild, step, s_tick[0]);
+          reason = kWakeRebuild;
+          ++step0;
+          break;
+        }
+      }
+      if (reason == kWakeDone) {
+        if (threadIdx.x == 0) park_wake(a.ra.ctl, kWakeDone, a.k, 0);
+        break;
       }
     }
-    if (threadIdx.x == 0) park_wake(a.ra.ctl, kWakeDone, a.k, 0);
     return;
   } else {
+  rebuild();
   for (uint32_t step = 0; step < a.k; ++step) {
     if (tr) trace(4, step, 0);
     if (segs) {
