@@ -257,12 +257,15 @@ void launch_fasst_stats(const DevGraph& g, const uint32_t* w, const uint32_t* x,
 // every edge has that fixed-point weight (w/tw unused).  Items beyond `cap`
 // are dropped (the host re-runs with the exact total, meta[0]); meta[1] +=
 // live (item, simulation) pairs.  tile_state: items_tiles(m) zeroed words,
-// tile_ctr zeroed.
+// tile_ctr zeroed.  row_cnt != nullptr (FASST multi-partition plans): positions
+// whose window misses the partition's value range are skipped and per-row item
+// counts accumulate in row_cnt (n+1 zeroed entries) instead of it.row_off
+// (the caller scans them).
 uint64_t items_tiles(uint64_t npos);
 void launch_items_onepass(const DevGraph& g, const uint32_t* w, const uint32_t* tw,
                           uint32_t wconst, const RankDev& r, int dir, int fasst, Items& it,
                           uint64_t cap, unsigned long long* tile_state, unsigned int* tile_ctr,
-                          unsigned long long* meta, cudaStream_t s);
+                          unsigned long long* meta, uint32_t* row_cnt, cudaStream_t s);
 // meta[0] += items of every stride-th forward position (capacity estimate).
 void launch_items_sample(const DevGraph& g, const uint32_t* w, uint32_t wconst, const RankDev& r,
                          int fasst, uint64_t stride, unsigned long long* meta, cudaStream_t s);

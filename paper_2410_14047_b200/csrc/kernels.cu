@@ -325,11 +325,18 @@ struct ItemsPass {
   uint8_t* it_batch;
   uint32_t* it_row;
   uint64_t* row_off;
+  uint32_t* row_cnt;               // FILTER: per-row item counts (row offsets scanned after)
   unsigned long long* tile_state;  // per tile: flag (2 bits) | value
   unsigned int* tile_ctr;          // dynamic tile ids (look-back forward progress)
   unsigned long long* meta;        // [0] total items, [1] live (item, sim) pairs
 };
 
+// FILTER (FASST partitions of a multi-partition plan): a position whose
+// window block [h & ~(2^(b+1)-1), +2^(b+1)) misses the partition's slot-value
+// range [x_0, x_{J-1}] emits nothing and is dropped after its hash/weight load
+// (≈ 1 - 1/mu of the positions); row offsets then come from per-row counts
+// (warp-aggregated) and a scan over the rows instead of every position's row.
+template <int FILTER>
 __global__ void __launch_bounds__(kTileThreads, 2) k_items_onepass(ItemsPass a) {
   extern __shared__ __align__(16) uint32_t sx[];
   uint32_t* lut = sx + a.Jp;
@@ -339,12 +346,14 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_items_onepass(ItemsPass a) 
     typename BlockScan::TempStorage scan;
     typename BlockExch::TempStorage exch;
   } tmp;
-  __shared__ unsigned long long s_prefix;
-  __shared__ unsigned int s_tile;
+  __shared__ unsigned long long s_prefix, s_lb_sum;
+  __shared__ unsigned int s_tile, s_lb_first;
   for (uint32_t i = threadIdx.x; i < a.Jp; i += blockDim.x) sx[i] = a.x[i];
   if (a.fasst)
     for (uint32_t k = threadIdx.x; k <= (1u << kLutBits); k += blockDim.x) lut[k] = a.glut[k];
   const uint64_t ntiles = (a.npos + kTilePos - 1) / kTilePos;
+  __syncthreads();
+  const uint64_t xmin = sx[0], xmax = sx[a.J - 1];
   // persistent blocks take tiles in order (a tile's look-back waits only on
   // tiles already held by running blocks)
   for (;;) {
@@ -375,6 +384,11 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_items_onepass(ItemsPass a) 
       cnt[i] = 0;
       const uint32_t W = wv[i], h = hv[i];
       if (W == 0) continue;  // fasst.cpp:71 (and past the end)
+      if (FILTER) {  // the window block misses the partition's value range
+        const uint64_t span = uint64_t(2) << (31 - __clz(W));
+        const uint64_t lx = uint64_t(h) & ~(span - 1);
+        if (lx + span <= xmin || lx > xmax) continue;
+      }
       uint32_t lo, hi, alo, ahi;
       edge_window(sx, lut, a.J, h, W, a.fasst, lo, hi, alo, ahi);
       if (hi <= lo) continue;
@@ -397,9 +411,10 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_items_onepass(ItemsPass a) 
     for (int i = 0; i < kPosPerThread; ++i) {
       const uint64_t p = pbase + uint64_t(i) * kTileThreads;
       const bool ok = p < a.npos;
-      rowv[i] = ok ? __ldcs(a.p_row + p) : 0u;
-      prevv[i] = ok && p ? __ldcs(a.p_row + p - 1) : 0xFFFFFFFFu;
-      othv[i] = ok && (info[i] & 0xFFFFu) ? __ldcs(a.p_other + p) : 0u;
+      const bool emits = ok && (info[i] & 0xFFFFu);
+      rowv[i] = (FILTER ? emits : ok) ? __ldcs(a.p_row + p) : 0u;
+      prevv[i] = !FILTER && ok && p ? __ldcs(a.p_row + p - 1) : 0xFFFFFFFFu;
+      othv[i] = emits ? __ldcs(a.p_other + p) : 0u;
     }
     // ---- tile scan in position order (striped -> blocked -> striped)
     BlockExch(tmp.exch).StripedToBlocked(cnt);
@@ -408,29 +423,39 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_items_onepass(ItemsPass a) 
     BlockScan(tmp.scan).ExclusiveSum(cnt, cnt, tile_total);
     __syncthreads();
     BlockExch(tmp.exch).BlockedToStriped(cnt);
-    // ---- decoupled look-back for the tile's global item offset: warp 0
-    // inspects 32 predecessors per step (lane l: tile - 1 - l) and stops at
-    // the nearest one that published its inclusive prefix
-    if (threadIdx.x < 32) {
+    // ---- decoupled look-back for the tile's global item offset, block-wide:
+    // thread t inspects predecessor tile - 1 - t (256 per step) and the block
+    // stops at the nearest one that published its inclusive prefix.  With
+    // every resident block working on its own tile, the nearest inclusive
+    // prefix is about one wave (~300 tiles) back: a warp-wide look-back needed
+    // ~10 dependent steps per tile, this needs 1-2.
+    {
       unsigned long long* st = a.tile_state;
-      const unsigned lane = threadIdx.x;
-      if (lane == 0) __stcg(st + tile, (tile == 0 ? kStInc : kStAgg) | tile_total);
+      if (threadIdx.x == 0) {
+        __stcg(st + tile, (tile == 0 ? kStInc : kStAgg) | tile_total);
+        s_lb_sum = 0;
+      }
       unsigned long long prefix = 0;
-      for (int64_t base = int64_t(tile) - 1; base >= 0; base -= 32) {
-        const int64_t t = base - int64_t(lane);
+      for (int64_t base = int64_t(tile) - 1; base >= 0; base -= kTileThreads) {
+        const int64_t t = base - int64_t(threadIdx.x);
         unsigned long long v = kStInc;  // before tile 0: inclusive prefix 0
         if (t >= 0)
           do {
             v = ld_volatile(st + t);
           } while ((v >> 62) == 0);
-        const unsigned inc = __ballot_sync(0xffffffffu, (v >> 62) == 2);
-        const unsigned stop = inc ? unsigned(__ffs(inc) - 1) : 31u;
-        unsigned long long val = lane <= stop ? (v & kStVal) : 0ull;
+        if (threadIdx.x == 0) s_lb_first = kTileThreads;
+        __syncthreads();
+        if ((v >> 62) == 2) atomicMin(&s_lb_first, unsigned(threadIdx.x));
+        __syncthreads();
+        const unsigned first = s_lb_first;  // nearest inclusive (kTileThreads: none)
+        unsigned long long val = threadIdx.x <= first ? (v & kStVal) : 0ull;
         for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
-        prefix += val;
-        if (inc) break;
+        if (lane_id() == 0 && val) atomicAdd(&s_lb_sum, val);
+        __syncthreads();
+        prefix = s_lb_sum;
+        if (first < kTileThreads) break;
       }
-      if (lane == 0) {
+      if (threadIdx.x == 0) {
         if (tile) __stcg(st + tile, kStInc | (prefix + tile_total));
         s_prefix = prefix;
         if (tile + 1 == ntiles) a.meta[0] = prefix + tile_total;
@@ -444,14 +469,24 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_items_onepass(ItemsPass a) 
 #pragma unroll
     for (int i = 0; i < kPosPerThread; ++i) {
       const uint64_t p = pbase + uint64_t(i) * kTileThreads;
-      if (p >= a.npos) break;
-      uint64_t o = prefix + cnt[i];
       const uint32_t row = rowv[i];
-      // rows (prev_row, row] start at this position (rows without edges share it)
-      for (uint32_t r = prevv[i] + 1; r <= row; ++r) a.row_off[r] = o;
-      const uint32_t c = info[i] & 0xFFFFu;
-      if (p + 1 == a.npos)  // rows after the last edge's row end at the total
-        for (uint32_t r = row + 1; r <= a.n; ++r) a.row_off[r] = o + c;
+      const uint32_t c = p < a.npos ? info[i] & 0xFFFFu : 0u;
+      if (FILTER) {
+        // per-row item counts: lanes of one step hold consecutive positions,
+        // so a row's emitting lanes form one group; one atomic per group
+        const uint32_t key = c ? row : 0xFFFFFFFFu;
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        const unsigned tot = __reduce_add_sync(peers, c);
+        if (c && lane_id() == unsigned(__ffs(peers) - 1)) atomicAdd(a.row_cnt + row, tot);
+      }
+      if (p >= a.npos) continue;
+      uint64_t o = prefix + cnt[i];
+      if (!FILTER) {
+        // rows (prev_row, row] start at this position (rows without edges share it)
+        for (uint32_t r = prevv[i] + 1; r <= row; ++r) a.row_off[r] = o;
+        if (p + 1 == a.npos)  // rows after the last edge's row end at the total
+          for (uint32_t r = row + 1; r <= a.n; ++r) a.row_off[r] = o + c;
+      }
       if (!c) continue;
       const uint32_t other = othv[i];
       const uint32_t b0 = info[i] >> 24, nb = (info[i] >> 16) & 0xFFu;
@@ -476,6 +511,202 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_items_onepass(ItemsPass a) 
       }
     }
     __syncthreads();  // s_tile / s_prefix / scan storage reused by the next tile
+  }
+}
+
+// Partition-sparse variant of the one-pass build (FASST multi-partition
+// plans): a tile's positions whose window block misses the partition's
+// slot-value range (≈ 1 - 1/mu of them) are dropped right after their
+// hash/weight load, the rest are compacted (in position order) into a
+// shared-memory list, and the windows, the scan, the look-back and the item
+// writes run over that dense list with every lane busy (the filtered version
+// of k_items_onepass ran with ~10 of 32 lanes active).  Row offsets come from
+// per-row item counts (segmented warp sums, one atomic per row segment)
+// scanned after the pass.
+constexpr int kSparseCap = kTilePos;  // list capacity = every position of a tile
+
+__device__ __forceinline__ void lookback_block(unsigned long long* st, uint32_t tile,
+                                               uint32_t tile_total, unsigned long long& s_prefix,
+                                               unsigned long long& s_lb_sum,
+                                               unsigned int& s_lb_first) {
+  if (threadIdx.x == 0) {
+    __stcg(st + tile, (tile == 0 ? kStInc : kStAgg) | tile_total);
+    s_lb_sum = 0;
+  }
+  unsigned long long prefix = 0;
+  for (int64_t base = int64_t(tile) - 1; base >= 0; base -= kTileThreads) {
+    const int64_t t = base - int64_t(threadIdx.x);
+    unsigned long long v = kStInc;
+    if (t >= 0)
+      do {
+        v = ld_volatile(st + t);
+      } while ((v >> 62) == 0);
+    if (threadIdx.x == 0) s_lb_first = kTileThreads;
+    __syncthreads();
+    if ((v >> 62) == 2) atomicMin(&s_lb_first, unsigned(threadIdx.x));
+    __syncthreads();
+    const unsigned first = s_lb_first;
+    unsigned long long val = threadIdx.x <= first ? (v & kStVal) : 0ull;
+    for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+    if (lane_id() == 0 && val) atomicAdd(&s_lb_sum, val);
+    __syncthreads();
+    prefix = s_lb_sum;
+    if (first < kTileThreads) break;
+  }
+  if (threadIdx.x == 0) {
+    if (tile) __stcg(st + tile, kStInc | (prefix + tile_total));
+    s_prefix = prefix;
+  }
+}
+
+__global__ void __launch_bounds__(kTileThreads, 3) k_items_sparse(ItemsPass a) {
+  extern __shared__ __align__(16) uint32_t sx[];
+  uint32_t* lut = sx + a.Jp;
+  using BlockScan = cub::BlockScan<uint32_t, kTileThreads>;
+  using BlockExch = cub::BlockExchange<uint32_t, kTileThreads, kPosPerThread>;
+  __shared__ union {
+    typename BlockScan::TempStorage scan;
+    typename BlockExch::TempStorage exch;
+  } tmp;
+  __shared__ uint16_t l_idx[kSparseCap];              // tile-relative position
+  __shared__ uint32_t l_info[kSparseCap], l_a[kSparseCap], l_b[kSparseCap], l_off[kSparseCap];
+  __shared__ unsigned long long s_prefix, s_lb_sum;
+  __shared__ unsigned int s_tile, s_lb_first, s_nrel;
+  for (uint32_t i = threadIdx.x; i < a.Jp; i += blockDim.x) sx[i] = a.x[i];
+  for (uint32_t k = threadIdx.x; k <= (1u << kLutBits); k += blockDim.x) lut[k] = a.glut[k];
+  const uint64_t ntiles = (a.npos + kTilePos - 1) / kTilePos;
+  __syncthreads();
+  const uint64_t xmin = sx[0], xmax = sx[a.J - 1];
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_ctr, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= ntiles) break;
+    const uint64_t t0 = uint64_t(tile) * kTilePos;
+    // ---- A: relevance of the tile's positions (striped, coalesced loads)
+    uint32_t rel[kPosPerThread];
+#pragma unroll
+    for (int i = 0; i < kPosPerThread; ++i) {
+      const uint64_t p = t0 + uint64_t(i) * kTileThreads + threadIdx.x;
+      const bool ok = p < a.npos;
+      const uint32_t W = ok ? (a.p_w ? __ldcs(a.p_w + p) : a.Wc) : 0u;
+      const uint32_t h = ok ? __ldcs(a.p_hash + p) : 0u;
+      rel[i] = 0;
+      if (W != 0) {  // fasst.cpp:71; the window block must meet [x_0, x_{J-1}]
+        const uint64_t span = uint64_t(2) << (31 - __clz(W));
+        const uint64_t lx = uint64_t(h) & ~(span - 1);
+        rel[i] = (lx + span > xmin && lx <= xmax) ? 1u : 0u;
+      }
+    }
+    uint32_t idx[kPosPerThread];
+#pragma unroll
+    for (int i = 0; i < kPosPerThread; ++i) idx[i] = rel[i];
+    BlockExch(tmp.exch).StripedToBlocked(idx);
+    __syncthreads();
+    uint32_t nrel;
+    BlockScan(tmp.scan).ExclusiveSum(idx, idx, nrel);
+    __syncthreads();
+    BlockExch(tmp.exch).BlockedToStriped(idx);
+#pragma unroll
+    for (int i = 0; i < kPosPerThread; ++i)
+      if (rel[i]) l_idx[idx[i]] = uint16_t(i * kTileThreads + threadIdx.x);
+    __syncthreads();
+    // ---- B: windows of the listed positions (dense)
+    uint32_t live = 0;
+    for (uint32_t j = threadIdx.x; j < nrel; j += kTileThreads) {
+      const uint64_t p = t0 + l_idx[j];
+      const uint32_t W = a.p_w ? a.p_w[p] : a.Wc, h = a.p_hash[p];
+      uint32_t lo, hi, alo, ahi, info = 0, mA = 0, mB = 0;
+      edge_window(sx, lut, a.J, h, W, 1, lo, hi, alo, ahi);
+      if (hi > lo) {
+        const uint32_t b0 = lo >> 5, b1 = (hi - 1) >> 5, nb = b1 - b0 + 1;
+        uint32_t c = 0;
+        for (uint32_t b = b0; b <= b1; ++b) {
+          const uint32_t mk = window_batch_mask(sx, h, W, lo, hi, alo, ahi, b);
+          if (b == b0) mA = mk;
+          else if (b == b0 + 1) mB = mk;
+          c += mk != 0;
+          live += __popc(mk);
+        }
+        info = (b0 << 24) | (min(nb, 255u) << 16) | c;
+      }
+      l_info[j] = info;
+      l_a[j] = mA;
+      l_b[j] = mB;
+    }
+    __syncthreads();
+    // ---- C: item offsets in list (= position) order, tile offset by look-back
+    uint32_t c8[kPosPerThread];
+#pragma unroll
+    for (int i = 0; i < kPosPerThread; ++i) {
+      const uint32_t j = threadIdx.x * kPosPerThread + i;  // blocked
+      c8[i] = j < nrel ? (l_info[j] & 0xFFFFu) : 0u;
+    }
+    uint32_t tile_total;
+    BlockScan(tmp.scan).ExclusiveSum(c8, c8, tile_total);
+#pragma unroll
+    for (int i = 0; i < kPosPerThread; ++i) {
+      const uint32_t j = threadIdx.x * kPosPerThread + i;
+      if (j < nrel) l_off[j] = c8[i];
+    }
+    __syncthreads();
+    lookback_block(a.tile_state, tile, tile_total, s_prefix, s_lb_sum, s_lb_first);
+    if (threadIdx.x == 0 && tile + 1 == ntiles) a.meta[0] = s_prefix + tile_total;
+    for (int o = 16; o; o >>= 1) live += __shfl_xor_sync(0xffffffffu, live, o);
+    if (lane_id() == 0 && live) atomicAdd(&a.meta[1], (unsigned long long)live);
+    __syncthreads();
+    const unsigned long long prefix = s_prefix;
+    // ---- D: items (consecutive lanes: consecutive listed positions) and
+    // per-row counts (segmented warp sums over the listed positions' rows)
+    for (uint32_t j0 = (threadIdx.x & ~31u); j0 < nrel; j0 += kTileThreads) {
+      const uint32_t j = j0 + lane_id();
+      const bool in = j < nrel;
+      const uint32_t info = in ? l_info[j] : 0u;
+      const uint32_t c = info & 0xFFFFu;
+      const uint64_t p = t0 + (in ? l_idx[j] : 0u);
+      const uint32_t row = c ? a.p_row[p] : 0xFFFFFFFFu;
+      // segmented inclusive sum of c over runs of equal keys (a run = one
+      // row's consecutive emitting lanes; non-emitting lanes carry a sentinel
+      // key and a zero): head-flag scan, (f, s) <- (f_up | f, f ? s : s_up + s)
+      const uint32_t rprev = __shfl_up_sync(0xffffffffu, row, 1);
+      uint32_t sum = c, head = (lane_id() == 0 || rprev != row) ? 1u : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t up = __shfl_up_sync(0xffffffffu, sum, o);
+        const uint32_t fup = __shfl_up_sync(0xffffffffu, head, o);
+        if (lane_id() >= unsigned(o)) {
+          if (!head) sum += up;
+          head |= fup;
+        }
+      }
+      const uint32_t rnext = __shfl_down_sync(0xffffffffu, row, 1);
+      const bool seg_end = lane_id() == 31 || rnext != row;
+      if (c && seg_end) atomicAdd(a.row_cnt + row, sum);
+      if (!c) continue;
+      const uint32_t other = a.p_other[p];
+      uint64_t o = prefix + l_off[j];
+      const uint32_t b0 = info >> 24, nb = (info >> 16) & 0xFFu;
+      auto emit = [&](uint32_t b, uint32_t mk) {
+        if (!mk) return;
+        if (o < a.cap) {
+          a.it_other[o] = other;
+          a.it_row[o] = row;
+          a.it_mask[o] = mk;
+          a.it_batch[o] = uint8_t(b);
+        }
+        ++o;
+      };
+      emit(b0, l_a[j]);
+      if (nb >= 2) emit(b0 + 1, l_b[j]);
+      if (nb > 2) {
+        const uint32_t W = a.p_w ? a.p_w[p] : a.Wc, h = a.p_hash[p];
+        uint32_t lo, hi, alo, ahi;
+        edge_window(sx, lut, a.J, h, W, 1, lo, hi, alo, ahi);
+        for (uint32_t b = b0 + 2; b <= (hi - 1) >> 5; ++b)
+          emit(b, window_batch_mask(sx, h, W, lo, hi, alo, ahi, b));
+      }
+    }
+    __syncthreads();  // list / scan storage reused by the next tile
   }
 }
 
@@ -3342,7 +3573,9 @@ static ItemsPass items_pass_args(const DevGraph& g, const uint32_t* w, const uin
 static size_t items_smem(const RankDev& r) {
   static bool attr = false;
   if (!attr) {
-    DFS_CUDA(cudaFuncSetAttribute(k_items_onepass, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
+    DFS_CUDA(cudaFuncSetAttribute(k_items_onepass<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
+    DFS_CUDA(cudaFuncSetAttribute(k_items_onepass<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
+    DFS_CUDA(cudaFuncSetAttribute(k_items_sparse, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
     DFS_CUDA(cudaFuncSetAttribute(k_items_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
     attr = true;
   }
@@ -3363,7 +3596,7 @@ void launch_items_sample(const DevGraph& g, const uint32_t* w, uint32_t wconst, 
 void launch_items_onepass(const DevGraph& g, const uint32_t* w, const uint32_t* tw,
                           uint32_t wconst, const RankDev& r, int dir, int fasst, Items& it,
                           uint64_t cap, unsigned long long* tile_state, unsigned int* tile_ctr,
-                          unsigned long long* meta, cudaStream_t s) {
+                          unsigned long long* meta, uint32_t* row_cnt, cudaStream_t s) {
   if (!g.m) return;
   ItemsPass a = items_pass_args(g, w, tw, wconst, r, dir, fasst);
   a.cap = cap;
@@ -3372,15 +3605,25 @@ void launch_items_onepass(const DevGraph& g, const uint32_t* w, const uint32_t* 
   a.it_batch = it.batch;
   a.it_row = it.row;
   a.row_off = it.row_off;
+  a.row_cnt = row_cnt;
   a.tile_state = tile_state;
   a.tile_ctr = tile_ctr;
   a.meta = meta;
   const size_t smem = items_smem(r);
+  const bool filter = row_cnt != nullptr;
   int per = 0;
-  DFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_items_onepass, kTileThreads, smem));
+  DFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per, filter ? k_items_onepass<1> : k_items_onepass<0>, kTileThreads, smem));
   const uint64_t tiles = items_tiles(g.m);
   const int grid = int(std::min<uint64_t>(tiles, uint64_t(std::max(per, 1)) * num_sms()));
-  k_items_onepass<<<grid, kTileThreads, smem, s>>>(a);
+  if (filter) {
+    int ps = 0;
+    DFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k_items_sparse, kTileThreads, smem));
+    const int gs = int(std::min<uint64_t>(tiles, uint64_t(std::max(ps, 1)) * num_sms()));
+    k_items_sparse<<<gs, kTileThreads, smem, s>>>(a);
+  } else {
+    k_items_onepass<0><<<grid, kTileThreads, smem, s>>>(a);
+  }
   DFS_CUDA(cudaGetLastError());
   ++g_launches;
 }

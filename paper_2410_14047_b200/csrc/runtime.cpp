@@ -247,6 +247,7 @@ void Context::build_items(RankDev& r) {
   const int fa = cfg_.fasst ? 1 : 0;
   const uint32_t wconst =
       cfg_.weights.kind == WeightKind::Constant ? to_fixed_point(cfg_.weights.a) : 0u;
+  const bool filter = fa && cfg_.mu > 1 && m > 0;
   // meta: [0..3] fwd chunk meta, [4..7] rev chunk meta, [8] fwd total, [9] fwd
   // live, [10] sample, [12] rev total, [13] rev live, [14] tile counters
   uint64_t* meta = as<uint64_t>(arena_.get("tmp.meta", 16 * 8));
@@ -282,9 +283,23 @@ void Context::build_items(RankDev& r) {
     DFS_CUDA(cudaMemsetAsync(meta + 11, 0, 5 * 8, stream_));
     DFS_CUDA(cudaMemsetAsync(tstate, 0, 2 * tiles * 8, stream_));
     auto* ctr = reinterpret_cast<unsigned int*>(meta + 14);
-    launch_items_onepass(g_, w_, tw_, wconst, r, 0, fa, f, cap, tstate, ctr, um + 8, stream_);
+    // multi-partition FASST plans: positions outside the partition's value
+    // range are skipped; row offsets from per-row counts
+    uint32_t* rc[2] = {nullptr, nullptr};
+    if (filter)
+      for (int d = 0; d < 2; ++d) {
+        rc[d] = as<uint32_t>(arena_.get(d ? "tmp.rowcnt.rev" : "tmp.rowcnt.fwd", (size_t(n) + 2) * 4));
+        DFS_CUDA(cudaMemsetAsync(rc[d], 0, (size_t(n) + 1) * 4, stream_));
+      }
+    launch_items_onepass(g_, w_, tw_, wconst, r, 0, fa, f, cap, tstate, ctr, um + 8, rc[0], stream_);
     launch_items_onepass(g_, w_, tw_, wconst, r, 1, fa, rv, cap, tstate + tiles, ctr + 1, um + 12,
-                         stream_);
+                         rc[1], stream_);
+    if (filter) {
+      const size_t sb = scan_tmp_bytes(uint64_t(n) + 2);
+      void* stmp = arena_.get("tmp.scan", sb);
+      scan_u32_u64(rc[0], f.row_off, n, stmp, sb, stream_);
+      scan_u32_u64(rc[1], rv.row_off, n, stmp, sb, stream_);
+    }
     finish_items(r, 0, cap, meta);
     finish_items(r, 1, cap, meta + 4);
     DFS_CUDA(cudaMemcpyAsync(hm, meta, sizeof hm, cudaMemcpyDeviceToHost, stream_));

@@ -16,7 +16,7 @@ g = D.generate(gen, a, m, bench.SEED)
 ctx = D.Context(0)
 ctx.upload(g)
 for _ in range(runs):
-    rep = ctx.run_json(None, k=k, r=r, devices=1, weights=wspec, seed=bench.SEED, timings=True,
-                       resident=True)
+    rep = ctx.run_json(None, k=k, r=r, devices=int(os.environ.get("DEVICES", "1")), weights=wspec,
+                       seed=bench.SEED, timings=True, resident=True)
 print(rep)
 print(ctx.stats())
