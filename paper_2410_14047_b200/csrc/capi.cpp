@@ -162,6 +162,7 @@ int dfs_graph_arrays(const dfs_graph* g, const uint64_t** offsets, const uint32_
     if (offsets) *offsets = g->g.offsets.data();
     if (adj) *adj = g->g.adj.data();
     if (orig_ids) *orig_ids = g->g.orig_id.data();
+    if (ehash || in_degree) dfs::ensure_graph_fields(g->g);
     if (ehash) *ehash = g->g.ehash.data();
     if (in_degree) *in_degree = g->g.in_degree.data();
   });

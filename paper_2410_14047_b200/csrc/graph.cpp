@@ -84,7 +84,8 @@ static std::vector<RawEdge> parse_edges(std::string_view text, bool directed) {
   return out;
 }
 
-void derive_graph_fields(HostGraph& g) {
+void ensure_graph_fields(const HostGraph& g) {
+  if (g.ehash.size() == g.m && g.in_degree.size() == g.n) return;
   g.ehash.resize(g.m);
   g.in_degree.assign(g.n, 0);
   const int T = hw_threads();
@@ -151,7 +152,6 @@ static HostGraph build_graph(std::vector<RawEdge>& raw) {
     g.adj[k] = merged[k].v;
     g.weights[k] = merged[k].w >= 0.0 ? to_fixed_point(merged[k].w) : 0;
   }
-  derive_graph_fields(g);
   return g;
 }
 
@@ -180,7 +180,6 @@ HostGraph graph_from_csr(uint32_t n, uint64_t m, const uint64_t* offsets, const 
     g.orig_id.resize(n);
     for (uint32_t u = 0; u < n; ++u) g.orig_id[u] = u;
   }
-  derive_graph_fields(g);
   return g;
 }
 
@@ -243,6 +242,7 @@ void assign_weights(const HostGraph& g, const WeightSetting& s, uint64_t seed,
   switch (s.kind) {
     case WeightKind::Constant: std::fill(w.begin(), w.end(), to_fixed_point(s.a)); break;
     case WeightKind::WeightedCascade:
+      ensure_graph_fields(g);
       for (uint64_t e = 0; e < g.m; ++e) w[e] = to_fixed_point(1.0 / g.in_degree[g.adj[e]]);
       break;
     case WeightKind::Normal: {
@@ -313,7 +313,6 @@ static HostGraph load_graph_cache(const std::string& path) {
   in.read(reinterpret_cast<char*>(g.orig_id.data()), std::streamsize(n * 8));
   if (!in) throw Error(kRuntime, "truncated graph cache: " + path);
   if (g.offsets.back() != m) throw Error(kRuntime, "corrupt graph cache: " + path);
-  derive_graph_fields(g);
   return g;
 }
 
@@ -409,7 +408,6 @@ HostGraph generate(uint64_t m, uint64_t id_space, KeyFn key) {
   }
   for (uint32_t u = 0; u < g.n; ++u) g.offsets[size_t(u) + 1] += g.offsets[u];
   g.weights.assign(m, 0);
-  derive_graph_fields(g);
   return g;
 }
 

@@ -17,8 +17,11 @@ struct HostGraph {
   std::vector<uint64_t> offsets;    // n+1
   std::vector<uint32_t> adj;        // m, sorted per row
   std::vector<uint32_t> weights;    // m, fixed point (as loaded)
-  std::vector<uint32_t> ehash;      // m, edge_hash(u, v) on dense ids
-  std::vector<uint32_t> in_degree;  // n
+  // Derived on first host use (ensure_graph_fields): the GPU path never
+  // reads them (k_ehash / k_indeg recompute both at upload), so loaders and
+  // generators do not spend host time on them.
+  mutable std::vector<uint32_t> ehash;      // m, edge_hash(u, v) on dense ids
+  mutable std::vector<uint32_t> in_degree;  // n
   std::vector<uint64_t> orig_id;    // n, ascending
 };
 
@@ -60,6 +63,6 @@ void influence_stats(const HostGraph& g, const std::vector<uint32_t>& w,
 std::vector<uint32_t> greedy_exact(const HostGraph& g, const std::vector<uint32_t>& w, uint32_t k,
                                    uint32_t trials, uint64_t seed);
 
-void derive_graph_fields(HostGraph& g);  // ehash + in_degree (parallel)
+void ensure_graph_fields(const HostGraph& g);  // ehash + in_degree (parallel), once
 
 }  // namespace dfs
