@@ -570,6 +570,8 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_items_sparse(ItemsPass a) {
   } tmp;
   __shared__ uint16_t l_idx[kSparseCap];              // tile-relative position
   __shared__ uint32_t l_info[kSparseCap], l_a[kSparseCap], l_b[kSparseCap], l_off[kSparseCap];
+  // rows of the listed positions: dynamic shared memory after the LUT
+  uint32_t* l_row = lut + (1u << kLutBits) + 1;
   __shared__ unsigned long long s_prefix, s_lb_sum;
   __shared__ unsigned int s_tile, s_lb_first, s_nrel;
   for (uint32_t i = threadIdx.x; i < a.Jp; i += blockDim.x) sx[i] = a.x[i];
@@ -577,20 +579,28 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_items_sparse(ItemsPass a) {
   const uint64_t ntiles = (a.npos + kTilePos - 1) / kTilePos;
   __syncthreads();
   const uint64_t xmin = sx[0], xmax = sx[a.J - 1];
-  for (;;) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_ctr, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    if (tile >= ntiles) break;
-    const uint64_t t0 = uint64_t(tile) * kTilePos;
+  // Static round-robin tiles (tile = block + k * grid): the hashes/weights of
+  // the block's next tile are loaded while the current one is processed (the
+  // DRAM round trip of phase A was the top stall).  Every tile a look-back
+  // waits on is some block's current or finished tile.
+  uint32_t ph[kPosPerThread], pw[kPosPerThread];
+  auto prefetch = [&](uint64_t t) {
+#pragma unroll
+    for (int i = 0; i < kPosPerThread; ++i) {
+      const uint64_t p = t * kTilePos + uint64_t(i) * kTileThreads + threadIdx.x;
+      const bool ok = t < ntiles && p < a.npos;
+      pw[i] = ok ? (a.p_w ? __ldcs(a.p_w + p) : a.Wc) : 0u;
+      ph[i] = ok ? __ldcs(a.p_hash + p) : 0u;
+    }
+  };
+  prefetch(blockIdx.x);
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint64_t t0 = tile * kTilePos;
     // ---- A: relevance of the tile's positions (striped, coalesced loads)
     uint32_t rel[kPosPerThread];
 #pragma unroll
     for (int i = 0; i < kPosPerThread; ++i) {
-      const uint64_t p = t0 + uint64_t(i) * kTileThreads + threadIdx.x;
-      const bool ok = p < a.npos;
-      const uint32_t W = ok ? (a.p_w ? __ldcs(a.p_w + p) : a.Wc) : 0u;
-      const uint32_t h = ok ? __ldcs(a.p_hash + p) : 0u;
+      const uint32_t W = pw[i], h = ph[i];
       rel[i] = 0;
       if (W != 0) {  // fasst.cpp:71; the window block must meet [x_0, x_{J-1}]
         const uint64_t span = uint64_t(2) << (31 - __clz(W));
@@ -598,6 +608,7 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_items_sparse(ItemsPass a) {
         rel[i] = (lx + span > xmin && lx <= xmax) ? 1u : 0u;
       }
     }
+    prefetch(tile + gridDim.x);
     uint32_t idx[kPosPerThread];
 #pragma unroll
     for (int i = 0; i < kPosPerThread; ++i) idx[i] = rel[i];
@@ -616,6 +627,9 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_items_sparse(ItemsPass a) {
     for (uint32_t j = threadIdx.x; j < nrel; j += kTileThreads) {
       const uint64_t p = t0 + l_idx[j];
       const uint32_t W = a.p_w ? a.p_w[p] : a.Wc, h = a.p_hash[p];
+      // row of the listed position: loaded here, in flight while the window
+      // is evaluated (phase D reads it from shared memory)
+      const uint32_t prow = a.p_row[p];
       uint32_t lo, hi, alo, ahi, info = 0, mA = 0, mB = 0;
       edge_window(sx, lut, a.J, h, W, 1, lo, hi, alo, ahi);
       if (hi > lo) {
@@ -633,6 +647,7 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_items_sparse(ItemsPass a) {
       l_info[j] = info;
       l_a[j] = mA;
       l_b[j] = mB;
+      l_row[j] = prow;
     }
     __syncthreads();
     // ---- C: item offsets in list (= position) order, tile offset by look-back
@@ -664,7 +679,8 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_items_sparse(ItemsPass a) {
       const uint32_t info = in ? l_info[j] : 0u;
       const uint32_t c = info & 0xFFFFu;
       const uint64_t p = t0 + (in ? l_idx[j] : 0u);
-      const uint32_t row = c ? a.p_row[p] : 0xFFFFFFFFu;
+      const uint32_t row = c ? l_row[j] : 0xFFFFFFFFu;
+      const uint32_t other = c ? a.p_other[p] : 0u;  // in flight during the segmented sum
       // segmented inclusive sum of c over runs of equal keys (a run = one
       // row's consecutive emitting lanes; non-emitting lanes carry a sentinel
       // key and a zero): head-flag scan, (f, s) <- (f_up | f, f ? s : s_up + s)
@@ -683,7 +699,6 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_items_sparse(ItemsPass a) {
       const bool seg_end = lane_id() == 31 || rnext != row;
       if (c && seg_end) atomicAdd(a.row_cnt + row, sum);
       if (!c) continue;
-      const uint32_t other = a.p_other[p];
       uint64_t o = prefix + l_off[j];
       const uint32_t b0 = info >> 24, nb = (info >> 16) & 0xFFu;
       auto emit = [&](uint32_t b, uint32_t mk) {
@@ -3575,7 +3590,7 @@ static size_t items_smem(const RankDev& r) {
   if (!attr) {
     DFS_CUDA(cudaFuncSetAttribute(k_items_onepass<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
     DFS_CUDA(cudaFuncSetAttribute(k_items_onepass<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
-    DFS_CUDA(cudaFuncSetAttribute(k_items_sparse, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
+    DFS_CUDA(cudaFuncSetAttribute(k_items_sparse, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10));
     DFS_CUDA(cudaFuncSetAttribute(k_items_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
     attr = true;
   }
@@ -3618,9 +3633,10 @@ void launch_items_onepass(const DevGraph& g, const uint32_t* w, const uint32_t* 
   const int grid = int(std::min<uint64_t>(tiles, uint64_t(std::max(per, 1)) * num_sms()));
   if (filter) {
     int ps = 0;
-    DFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k_items_sparse, kTileThreads, smem));
+    const size_t ssm = smem + size_t(kSparseCap) * sizeof(uint32_t);
+    DFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k_items_sparse, kTileThreads, ssm));
     const int gs = int(std::min<uint64_t>(tiles, uint64_t(std::max(ps, 1)) * num_sms()));
-    k_items_sparse<<<gs, kTileThreads, smem, s>>>(a);
+    k_items_sparse<<<gs, kTileThreads, ssm, s>>>(a);
   } else {
     k_items_onepass<0><<<grid, kTileThreads, smem, s>>>(a);
   }
