@@ -514,25 +514,16 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_items_onepass(ItemsPass a) 
   }
 }
 
-// Partition-sparse variant of the one-pass build (FASST multi-partition
-// plans): a tile's positions whose window block misses the partition's
-// slot-value range (≈ 1 - 1/mu of them) are dropped right after their
-// hash/weight load, the rest are compacted (in position order) into a
-// shared-memory list, and the windows, the scan, the look-back and the item
-// writes run over that dense list with every lane busy (the filtered version
-// of k_items_onepass ran with ~10 of 32 lanes active).  Row offsets come from
-// per-row item counts (segmented warp sums, one atomic per row segment)
-// scanned after the pass.
-constexpr int kSparseCap = kTilePos;  // list capacity = every position of a tile
-
-__device__ __forceinline__ void lookback_block(unsigned long long* st, uint32_t tile,
-                                               uint32_t tile_total, unsigned long long& s_prefix,
-                                               unsigned long long& s_lb_sum,
-                                               unsigned int& s_lb_first) {
-  if (threadIdx.x == 0) {
-    __stcg(st + tile, (tile == 0 ? kStInc : kStAgg) | tile_total);
-    s_lb_sum = 0;
-  }
+// Look-back of a tile whose aggregate is already published: sums the
+// predecessors back to the nearest published inclusive prefix (block-wide,
+// 256 predecessors per step), publishes this tile's inclusive prefix and
+// leaves the exclusive prefix in s_prefix (valid after the final barrier).
+__device__ __forceinline__ void lookback_resolve(unsigned long long* st, uint64_t tile,
+                                                 uint32_t tile_total,
+                                                 unsigned long long& s_prefix,
+                                                 unsigned long long& s_lb_sum,
+                                                 unsigned int& s_lb_first) {
+  if (threadIdx.x == 0) s_lb_sum = 0;
   unsigned long long prefix = 0;
   for (int64_t base = int64_t(tile) - 1; base >= 0; base -= kTileThreads) {
     const int64_t t = base - int64_t(threadIdx.x);
@@ -557,32 +548,112 @@ __device__ __forceinline__ void lookback_block(unsigned long long* st, uint32_t 
     if (tile) __stcg(st + tile, kStInc | (prefix + tile_total));
     s_prefix = prefix;
   }
+  __syncthreads();
+}
+
+// Partition-sparse variant of the one-pass build (FASST multi-partition
+// plans): a tile's positions whose window block misses the partition's
+// slot-value range (≈ 1 - 1/mu of them) are dropped right after their
+// hash/weight load, the rest are compacted (in position order, warp ballots)
+// into a shared-memory list, and the windows and the scan run over that dense
+// list with every lane busy.  Row offsets come from per-row item counts
+// (segmented warp sums, one atomic per row segment) scanned after the pass.
+//
+// Tiles are taken round-robin (tile = block + k * grid) and each tile's
+// item writes are DEFERRED by one tile: after tile t's windows and scan the
+// block publishes t's aggregate, then resolves the look-back of its previous
+// tile (whose predecessors have long published theirs) and writes that
+// tile's items, and keeps t's lists for the next round (a tile listing more
+// than kPendCap positions is resolved and written at once).  Without the
+// deferral, a tile's look-back waited for the slowest tile of its wave (39%
+// of the stall samples).  The next tile's hashes/weights are loaded while the
+// current one is processed.
+constexpr int kSparseCap = kTilePos;  // list capacity = every position of a tile
+constexpr int kPendCap = 512;         // deferred list capacity
+constexpr int kTileWarps = kTileThreads / 32;
+
+// Items and per-row counts of one tile's list (positions t0 + idx[j]).
+__device__ __forceinline__ void sparse_write(const ItemsPass& a, const uint32_t* sx,
+                                             const uint32_t* lut, uint64_t t0, uint32_t nrel,
+                                             const uint16_t* idx, const uint32_t* info_l,
+                                             const uint32_t* la, const uint32_t* lb,
+                                             const uint32_t* loff, const uint32_t* lrow,
+                                             unsigned long long prefix) {
+  for (uint32_t j0 = (threadIdx.x & ~31u); j0 < nrel; j0 += kTileThreads) {
+    const uint32_t j = j0 + lane_id();
+    const bool in = j < nrel;
+    const uint32_t info = in ? info_l[j] : 0u;
+    const uint32_t c = info & 0xFFFFu;
+    const uint64_t p = t0 + (in ? idx[j] : 0u);
+    const uint32_t row = c ? lrow[j] : 0xFFFFFFFFu;
+    const uint32_t other = c ? a.p_other[p] : 0u;  // in flight during the segmented sum
+    // segmented inclusive sum of c over runs of equal rows (head-flag scan)
+    const uint32_t rprev = __shfl_up_sync(0xffffffffu, row, 1);
+    uint32_t sum = c, head = (lane_id() == 0 || rprev != row) ? 1u : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t up = __shfl_up_sync(0xffffffffu, sum, o);
+      const uint32_t fup = __shfl_up_sync(0xffffffffu, head, o);
+      if (lane_id() >= unsigned(o)) {
+        if (!head) sum += up;
+        head |= fup;
+      }
+    }
+    const uint32_t rnext = __shfl_down_sync(0xffffffffu, row, 1);
+    const bool seg_end = lane_id() == 31 || rnext != row;
+    if (c && seg_end) atomicAdd(a.row_cnt + row, sum);
+    if (!c) continue;
+    uint64_t o = prefix + loff[j];
+    const uint32_t b0 = info >> 24, nb = (info >> 16) & 0xFFu;
+    auto emit = [&](uint32_t b, uint32_t mk) {
+      if (!mk) return;
+      if (o < a.cap) {
+        a.it_other[o] = other;
+        a.it_row[o] = row;
+        a.it_mask[o] = mk;
+        a.it_batch[o] = uint8_t(b);
+      }
+      ++o;
+    };
+    emit(b0, la[j]);
+    if (nb >= 2) emit(b0 + 1, lb[j]);
+    if (nb > 2) {
+      const uint32_t W = a.p_w ? a.p_w[p] : a.Wc, h = a.p_hash[p];
+      uint32_t lo, hi, alo, ahi;
+      edge_window(sx, lut, a.J, h, W, 1, lo, hi, alo, ahi);
+      for (uint32_t b = b0 + 2; b <= (hi - 1) >> 5; ++b)
+        emit(b, window_batch_mask(sx, h, W, lo, hi, alo, ahi, b));
+    }
+  }
+}
+
+size_t sparse_extra_smem() {
+  return size_t(kSparseCap + 5 * kPendCap) * sizeof(uint32_t) + size_t(kPendCap) * sizeof(uint16_t);
 }
 
 __global__ void __launch_bounds__(kTileThreads, 3) k_items_sparse(ItemsPass a) {
   extern __shared__ __align__(16) uint32_t sx[];
   uint32_t* lut = sx + a.Jp;
+  uint32_t* l_row = lut + (1u << kLutBits) + 1;  // kSparseCap
+  uint32_t* q_info = l_row + kSparseCap;          // deferred tile: kPendCap each
+  uint32_t* q_a = q_info + kPendCap;
+  uint32_t* q_b = q_a + kPendCap;
+  uint32_t* q_off = q_b + kPendCap;
+  uint32_t* q_row = q_off + kPendCap;
+  uint16_t* q_idx = reinterpret_cast<uint16_t*>(q_row + kPendCap);
   using BlockScan = cub::BlockScan<uint32_t, kTileThreads>;
-  using BlockExch = cub::BlockExchange<uint32_t, kTileThreads, kPosPerThread>;
-  __shared__ union {
-    typename BlockScan::TempStorage scan;
-    typename BlockExch::TempStorage exch;
-  } tmp;
-  __shared__ uint16_t l_idx[kSparseCap];              // tile-relative position
+  __shared__ typename BlockScan::TempStorage scan_tmp;
+  __shared__ uint16_t l_idx[kSparseCap];  // tile-relative position
   __shared__ uint32_t l_info[kSparseCap], l_a[kSparseCap], l_b[kSparseCap], l_off[kSparseCap];
-  // rows of the listed positions: dynamic shared memory after the LUT
-  uint32_t* l_row = lut + (1u << kLutBits) + 1;
+  __shared__ uint32_t s_wcnt[kPosPerThread * kTileWarps];
   __shared__ unsigned long long s_prefix, s_lb_sum;
-  __shared__ unsigned int s_tile, s_lb_first, s_nrel;
+  __shared__ unsigned int s_lb_first, s_nrel;
   for (uint32_t i = threadIdx.x; i < a.Jp; i += blockDim.x) sx[i] = a.x[i];
   for (uint32_t k = threadIdx.x; k <= (1u << kLutBits); k += blockDim.x) lut[k] = a.glut[k];
   const uint64_t ntiles = (a.npos + kTilePos - 1) / kTilePos;
   __syncthreads();
   const uint64_t xmin = sx[0], xmax = sx[a.J - 1];
-  // Static round-robin tiles (tile = block + k * grid): the hashes/weights of
-  // the block's next tile are loaded while the current one is processed (the
-  // DRAM round trip of phase A was the top stall).  Every tile a look-back
-  // waits on is some block's current or finished tile.
+  const unsigned lane = lane_id(), wi = threadIdx.x >> 5;
   uint32_t ph[kPosPerThread], pw[kPosPerThread];
   auto prefetch = [&](uint64_t t) {
 #pragma unroll
@@ -593,6 +664,19 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_items_sparse(ItemsPass a) {
       ph[i] = ok ? __ldcs(a.p_hash + p) : 0u;
     }
   };
+  // resolve the look-back of tile t and write its items from the given lists
+  auto finish_tile = [&](uint64_t t, uint32_t total, uint32_t n, const uint16_t* idx,
+                         const uint32_t* info_l, const uint32_t* la, const uint32_t* lb,
+                         const uint32_t* loff, const uint32_t* lrow) {
+    lookback_resolve(a.tile_state, t, total, s_prefix, s_lb_sum, s_lb_first);
+    const unsigned long long prefix = s_prefix;
+    if (threadIdx.x == 0 && t + 1 == ntiles) a.meta[0] = prefix + total;
+    sparse_write(a, sx, lut, t * kTilePos, n, idx, info_l, la, lb, loff, lrow, prefix);
+    __syncthreads();  // lists / s_prefix reusable
+  };
+  constexpr uint64_t kNone = ~0ull;
+  uint64_t pend = kNone;
+  uint32_t pend_total = 0, pend_n = 0;
   prefetch(blockIdx.x);
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint64_t t0 = tile * kTilePos;
@@ -609,18 +693,35 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_items_sparse(ItemsPass a) {
       }
     }
     prefetch(tile + gridDim.x);
-    uint32_t idx[kPosPerThread];
+    // compaction in position order: (step i, warp, lane) is position order
+    unsigned bal[kPosPerThread];
 #pragma unroll
-    for (int i = 0; i < kPosPerThread; ++i) idx[i] = rel[i];
-    BlockExch(tmp.exch).StripedToBlocked(idx);
+    for (int i = 0; i < kPosPerThread; ++i) bal[i] = __ballot_sync(0xffffffffu, rel[i] != 0);
+    if (lane == 0)
+#pragma unroll
+      for (int i = 0; i < kPosPerThread; ++i) s_wcnt[i * kTileWarps + wi] = __popc(bal[i]);
     __syncthreads();
-    uint32_t nrel;
-    BlockScan(tmp.scan).ExclusiveSum(idx, idx, nrel);
+    if (wi == 0) {  // exclusive scan of the 64 (step, warp) counts, two per lane
+      const uint32_t c0 = s_wcnt[2 * lane], c1 = s_wcnt[2 * lane + 1];
+      uint32_t incl = c0 + c1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= unsigned(o)) incl += t;
+      }
+      const uint32_t ex = incl - c0 - c1;
+      s_wcnt[2 * lane] = ex;
+      s_wcnt[2 * lane + 1] = ex + c0;
+      if (lane == 31) s_nrel = incl;
+    }
     __syncthreads();
-    BlockExch(tmp.exch).BlockedToStriped(idx);
+    const unsigned below = (1u << lane) - 1u;
 #pragma unroll
     for (int i = 0; i < kPosPerThread; ++i)
-      if (rel[i]) l_idx[idx[i]] = uint16_t(i * kTileThreads + threadIdx.x);
+      if (rel[i])
+        l_idx[s_wcnt[i * kTileWarps + wi] + __popc(bal[i] & below)] =
+            uint16_t(i * kTileThreads + threadIdx.x);
+    const uint32_t nrel = s_nrel;
     __syncthreads();
     // ---- B: windows of the listed positions (dense)
     uint32_t live = 0;
@@ -628,7 +729,7 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_items_sparse(ItemsPass a) {
       const uint64_t p = t0 + l_idx[j];
       const uint32_t W = a.p_w ? a.p_w[p] : a.Wc, h = a.p_hash[p];
       // row of the listed position: loaded here, in flight while the window
-      // is evaluated (phase D reads it from shared memory)
+      // is evaluated (the write phase reads it from shared memory)
       const uint32_t prow = a.p_row[p];
       uint32_t lo, hi, alo, ahi, info = 0, mA = 0, mB = 0;
       edge_window(sx, lut, a.J, h, W, 1, lo, hi, alo, ahi);
@@ -650,7 +751,7 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_items_sparse(ItemsPass a) {
       l_row[j] = prow;
     }
     __syncthreads();
-    // ---- C: item offsets in list (= position) order, tile offset by look-back
+    // ---- C: item offsets in list (= position) order; publish the aggregate
     uint32_t c8[kPosPerThread];
 #pragma unroll
     for (int i = 0; i < kPosPerThread; ++i) {
@@ -658,71 +759,38 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_items_sparse(ItemsPass a) {
       c8[i] = j < nrel ? (l_info[j] & 0xFFFFu) : 0u;
     }
     uint32_t tile_total;
-    BlockScan(tmp.scan).ExclusiveSum(c8, c8, tile_total);
+    BlockScan(scan_tmp).ExclusiveSum(c8, c8, tile_total);
 #pragma unroll
     for (int i = 0; i < kPosPerThread; ++i) {
       const uint32_t j = threadIdx.x * kPosPerThread + i;
       if (j < nrel) l_off[j] = c8[i];
     }
-    __syncthreads();
-    lookback_block(a.tile_state, tile, tile_total, s_prefix, s_lb_sum, s_lb_first);
-    if (threadIdx.x == 0 && tile + 1 == ntiles) a.meta[0] = s_prefix + tile_total;
+    if (threadIdx.x == 0) __stcg(a.tile_state + tile, (tile == 0 ? kStInc : kStAgg) | tile_total);
     for (int o = 16; o; o >>= 1) live += __shfl_xor_sync(0xffffffffu, live, o);
-    if (lane_id() == 0 && live) atomicAdd(&a.meta[1], (unsigned long long)live);
+    if (lane == 0 && live) atomicAdd(&a.meta[1], (unsigned long long)live);
     __syncthreads();
-    const unsigned long long prefix = s_prefix;
-    // ---- D: items (consecutive lanes: consecutive listed positions) and
-    // per-row counts (segmented warp sums over the listed positions' rows)
-    for (uint32_t j0 = (threadIdx.x & ~31u); j0 < nrel; j0 += kTileThreads) {
-      const uint32_t j = j0 + lane_id();
-      const bool in = j < nrel;
-      const uint32_t info = in ? l_info[j] : 0u;
-      const uint32_t c = info & 0xFFFFu;
-      const uint64_t p = t0 + (in ? l_idx[j] : 0u);
-      const uint32_t row = c ? l_row[j] : 0xFFFFFFFFu;
-      const uint32_t other = c ? a.p_other[p] : 0u;  // in flight during the segmented sum
-      // segmented inclusive sum of c over runs of equal keys (a run = one
-      // row's consecutive emitting lanes; non-emitting lanes carry a sentinel
-      // key and a zero): head-flag scan, (f, s) <- (f_up | f, f ? s : s_up + s)
-      const uint32_t rprev = __shfl_up_sync(0xffffffffu, row, 1);
-      uint32_t sum = c, head = (lane_id() == 0 || rprev != row) ? 1u : 0u;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t up = __shfl_up_sync(0xffffffffu, sum, o);
-        const uint32_t fup = __shfl_up_sync(0xffffffffu, head, o);
-        if (lane_id() >= unsigned(o)) {
-          if (!head) sum += up;
-          head |= fup;
-        }
+    // ---- D: the previous tile's items, then defer this one
+    if (pend != kNone)
+      finish_tile(pend, pend_total, pend_n, q_idx, q_info, q_a, q_b, q_off, q_row);
+    if (nrel <= uint32_t(kPendCap)) {
+      for (uint32_t j = threadIdx.x; j < nrel; j += kTileThreads) {
+        q_idx[j] = l_idx[j];
+        q_info[j] = l_info[j];
+        q_a[j] = l_a[j];
+        q_b[j] = l_b[j];
+        q_off[j] = l_off[j];
+        q_row[j] = l_row[j];
       }
-      const uint32_t rnext = __shfl_down_sync(0xffffffffu, row, 1);
-      const bool seg_end = lane_id() == 31 || rnext != row;
-      if (c && seg_end) atomicAdd(a.row_cnt + row, sum);
-      if (!c) continue;
-      uint64_t o = prefix + l_off[j];
-      const uint32_t b0 = info >> 24, nb = (info >> 16) & 0xFFu;
-      auto emit = [&](uint32_t b, uint32_t mk) {
-        if (!mk) return;
-        if (o < a.cap) {
-          a.it_other[o] = other;
-          a.it_row[o] = row;
-          a.it_mask[o] = mk;
-          a.it_batch[o] = uint8_t(b);
-        }
-        ++o;
-      };
-      emit(b0, l_a[j]);
-      if (nb >= 2) emit(b0 + 1, l_b[j]);
-      if (nb > 2) {
-        const uint32_t W = a.p_w ? a.p_w[p] : a.Wc, h = a.p_hash[p];
-        uint32_t lo, hi, alo, ahi;
-        edge_window(sx, lut, a.J, h, W, 1, lo, hi, alo, ahi);
-        for (uint32_t b = b0 + 2; b <= (hi - 1) >> 5; ++b)
-          emit(b, window_batch_mask(sx, h, W, lo, hi, alo, ahi, b));
-      }
+      pend = tile;
+      pend_total = tile_total;
+      pend_n = nrel;
+      __syncthreads();
+    } else {
+      finish_tile(tile, tile_total, nrel, l_idx, l_info, l_a, l_b, l_off, l_row);
+      pend = kNone;
     }
-    __syncthreads();  // list / scan storage reused by the next tile
   }
+  if (pend != kNone) finish_tile(pend, pend_total, pend_n, q_idx, q_info, q_a, q_b, q_off, q_row);
 }
 
 // Item count of every stride-th position (capacity estimate of a one-pass
@@ -3633,7 +3701,7 @@ void launch_items_onepass(const DevGraph& g, const uint32_t* w, const uint32_t* 
   const int grid = int(std::min<uint64_t>(tiles, uint64_t(std::max(per, 1)) * num_sms()));
   if (filter) {
     int ps = 0;
-    const size_t ssm = smem + size_t(kSparseCap) * sizeof(uint32_t);
+    const size_t ssm = smem + sparse_extra_smem();
     DFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k_items_sparse, kTileThreads, ssm));
     const int gs = int(std::min<uint64_t>(tiles, uint64_t(std::max(ps, 1)) * num_sms()));
     k_items_sparse<<<gs, kTileThreads, ssm, s>>>(a);
