@@ -331,189 +331,6 @@ struct ItemsPass {
   unsigned long long* meta;        // [0] total items, [1] live (item, sim) pairs
 };
 
-// FILTER (FASST partitions of a multi-partition plan): a position whose
-// window block [h & ~(2^(b+1)-1), +2^(b+1)) misses the partition's slot-value
-// range [x_0, x_{J-1}] emits nothing and is dropped after its hash/weight load
-// (≈ 1 - 1/mu of the positions); row offsets then come from per-row counts
-// (warp-aggregated) and a scan over the rows instead of every position's row.
-template <int FILTER>
-__global__ void __launch_bounds__(kTileThreads, 2) k_items_onepass(ItemsPass a) {
-  extern __shared__ __align__(16) uint32_t sx[];
-  uint32_t* lut = sx + a.Jp;
-  using BlockScan = cub::BlockScan<uint32_t, kTileThreads>;
-  using BlockExch = cub::BlockExchange<uint32_t, kTileThreads, kPosPerThread>;
-  __shared__ union {
-    typename BlockScan::TempStorage scan;
-    typename BlockExch::TempStorage exch;
-  } tmp;
-  __shared__ unsigned long long s_prefix, s_lb_sum;
-  __shared__ unsigned int s_tile, s_lb_first;
-  for (uint32_t i = threadIdx.x; i < a.Jp; i += blockDim.x) sx[i] = a.x[i];
-  if (a.fasst)
-    for (uint32_t k = threadIdx.x; k <= (1u << kLutBits); k += blockDim.x) lut[k] = a.glut[k];
-  const uint64_t ntiles = (a.npos + kTilePos - 1) / kTilePos;
-  __syncthreads();
-  const uint64_t xmin = sx[0], xmax = sx[a.J - 1];
-  // persistent blocks take tiles in order (a tile's look-back waits only on
-  // tiles already held by running blocks)
-  for (;;) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(a.tile_ctr, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    if (tile >= ntiles) break;
-    // striped positions: step i covers kTileThreads consecutive positions
-    // (coalesced loads, and consecutive lanes write consecutive items)
-    const uint64_t pbase = uint64_t(tile) * kTilePos + threadIdx.x;
-    // ---- phase 1: windows, counts, masks of the first two batches
-    uint32_t mA[kPosPerThread], mB[kPosPerThread], info[kPosPerThread];  // b0 << 24 | nb << 16 | count
-    uint32_t cnt[kPosPerThread];
-    uint32_t live = 0;
-    // every position's hash and weight in flight together
-    uint32_t hv[kPosPerThread], wv[kPosPerThread];
-#pragma unroll
-    for (int i = 0; i < kPosPerThread; ++i) {
-      const uint64_t p = pbase + uint64_t(i) * kTileThreads;
-      const bool ok = p < a.npos;
-      wv[i] = ok ? (a.p_w ? __ldcs(a.p_w + p) : a.Wc) : 0u;
-      hv[i] = ok ? __ldcs(a.p_hash + p) : 0u;
-    }
-#pragma unroll
-    for (int i = 0; i < kPosPerThread; ++i) {
-      mA[i] = mB[i] = 0;
-      info[i] = 0;
-      cnt[i] = 0;
-      const uint32_t W = wv[i], h = hv[i];
-      if (W == 0) continue;  // fasst.cpp:71 (and past the end)
-      if (FILTER) {  // the window block misses the partition's value range
-        const uint64_t span = uint64_t(2) << (31 - __clz(W));
-        const uint64_t lx = uint64_t(h) & ~(span - 1);
-        if (lx + span <= xmin || lx > xmax) continue;
-      }
-      uint32_t lo, hi, alo, ahi;
-      edge_window(sx, lut, a.J, h, W, a.fasst, lo, hi, alo, ahi);
-      if (hi <= lo) continue;
-      const uint32_t b0 = lo >> 5, b1 = (hi - 1) >> 5, nb = b1 - b0 + 1;
-      uint32_t c = 0;
-      for (uint32_t b = b0; b <= b1; ++b) {
-        const uint32_t mk = window_batch_mask(sx, h, W, lo, hi, alo, ahi, b);
-        if (b == b0) mA[i] = mk;
-        else if (b == b0 + 1) mB[i] = mk;
-        c += mk != 0;
-        live += __popc(mk);
-      }
-      info[i] = (b0 << 24) | (min(nb, 255u) << 16) | c;
-      cnt[i] = c;
-    }
-    // phase-2 inputs of all 8 positions (rows, previous rows, other endpoints)
-    // in flight while the tile offset is resolved
-    uint32_t rowv[kPosPerThread], prevv[kPosPerThread], othv[kPosPerThread];
-#pragma unroll
-    for (int i = 0; i < kPosPerThread; ++i) {
-      const uint64_t p = pbase + uint64_t(i) * kTileThreads;
-      const bool ok = p < a.npos;
-      const bool emits = ok && (info[i] & 0xFFFFu);
-      rowv[i] = (FILTER ? emits : ok) ? __ldcs(a.p_row + p) : 0u;
-      prevv[i] = !FILTER && ok && p ? __ldcs(a.p_row + p - 1) : 0xFFFFFFFFu;
-      othv[i] = emits ? __ldcs(a.p_other + p) : 0u;
-    }
-    // ---- tile scan in position order (striped -> blocked -> striped)
-    BlockExch(tmp.exch).StripedToBlocked(cnt);
-    __syncthreads();
-    uint32_t tile_total;
-    BlockScan(tmp.scan).ExclusiveSum(cnt, cnt, tile_total);
-    __syncthreads();
-    BlockExch(tmp.exch).BlockedToStriped(cnt);
-    // ---- decoupled look-back for the tile's global item offset, block-wide:
-    // thread t inspects predecessor tile - 1 - t (256 per step) and the block
-    // stops at the nearest one that published its inclusive prefix.  With
-    // every resident block working on its own tile, the nearest inclusive
-    // prefix is about one wave (~300 tiles) back: a warp-wide look-back needed
-    // ~10 dependent steps per tile, this needs 1-2.
-    {
-      unsigned long long* st = a.tile_state;
-      if (threadIdx.x == 0) {
-        __stcg(st + tile, (tile == 0 ? kStInc : kStAgg) | tile_total);
-        s_lb_sum = 0;
-      }
-      unsigned long long prefix = 0;
-      for (int64_t base = int64_t(tile) - 1; base >= 0; base -= kTileThreads) {
-        const int64_t t = base - int64_t(threadIdx.x);
-        unsigned long long v = kStInc;  // before tile 0: inclusive prefix 0
-        if (t >= 0)
-          do {
-            v = ld_volatile(st + t);
-          } while ((v >> 62) == 0);
-        if (threadIdx.x == 0) s_lb_first = kTileThreads;
-        __syncthreads();
-        if ((v >> 62) == 2) atomicMin(&s_lb_first, unsigned(threadIdx.x));
-        __syncthreads();
-        const unsigned first = s_lb_first;  // nearest inclusive (kTileThreads: none)
-        unsigned long long val = threadIdx.x <= first ? (v & kStVal) : 0ull;
-        for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
-        if (lane_id() == 0 && val) atomicAdd(&s_lb_sum, val);
-        __syncthreads();
-        prefix = s_lb_sum;
-        if (first < kTileThreads) break;
-      }
-      if (threadIdx.x == 0) {
-        if (tile) __stcg(st + tile, kStInc | (prefix + tile_total));
-        s_prefix = prefix;
-        if (tile + 1 == ntiles) a.meta[0] = prefix + tile_total;
-      }
-    }
-    for (int o = 16; o; o >>= 1) live += __shfl_xor_sync(0xffffffffu, live, o);
-    if (lane_id() == 0 && live) atomicAdd(&a.meta[1], (unsigned long long)live);
-    __syncthreads();
-    const unsigned long long prefix = s_prefix;
-    // ---- phase 2: items and row offsets
-#pragma unroll
-    for (int i = 0; i < kPosPerThread; ++i) {
-      const uint64_t p = pbase + uint64_t(i) * kTileThreads;
-      const uint32_t row = rowv[i];
-      const uint32_t c = p < a.npos ? info[i] & 0xFFFFu : 0u;
-      if (FILTER) {
-        // per-row item counts: lanes of one step hold consecutive positions,
-        // so a row's emitting lanes form one group; one atomic per group
-        const uint32_t key = c ? row : 0xFFFFFFFFu;
-        const unsigned peers = __match_any_sync(0xffffffffu, key);
-        const unsigned tot = __reduce_add_sync(peers, c);
-        if (c && lane_id() == unsigned(__ffs(peers) - 1)) atomicAdd(a.row_cnt + row, tot);
-      }
-      if (p >= a.npos) continue;
-      uint64_t o = prefix + cnt[i];
-      if (!FILTER) {
-        // rows (prev_row, row] start at this position (rows without edges share it)
-        for (uint32_t r = prevv[i] + 1; r <= row; ++r) a.row_off[r] = o;
-        if (p + 1 == a.npos)  // rows after the last edge's row end at the total
-          for (uint32_t r = row + 1; r <= a.n; ++r) a.row_off[r] = o + c;
-      }
-      if (!c) continue;
-      const uint32_t other = othv[i];
-      const uint32_t b0 = info[i] >> 24, nb = (info[i] >> 16) & 0xFFu;
-      auto emit = [&](uint32_t b, uint32_t mk) {
-        if (!mk) return;
-        if (o < a.cap) {
-          a.it_other[o] = other;
-          a.it_row[o] = row;
-          a.it_mask[o] = mk;
-          a.it_batch[o] = uint8_t(b);
-        }
-        ++o;
-      };
-      emit(b0, mA[i]);
-      if (nb >= 2) emit(b0 + 1, mB[i]);
-      if (nb > 2) {  // wide window: re-evaluate the remaining batches
-        const uint32_t h = hv[i], W = wv[i];
-        uint32_t lo, hi, alo, ahi;
-        edge_window(sx, lut, a.J, h, W, a.fasst, lo, hi, alo, ahi);
-        for (uint32_t b = b0 + 2; b <= (hi - 1) >> 5; ++b)
-          emit(b, window_batch_mask(sx, h, W, lo, hi, alo, ahi, b));
-      }
-    }
-    __syncthreads();  // s_tile / s_prefix / scan storage reused by the next tile
-  }
-}
-
 // Look-back of a tile whose aggregate is already published: sums the
 // predecessors back to the nearest published inclusive prefix (block-wide,
 // 256 predecessors per step), publishes this tile's inclusive prefix and
@@ -791,6 +608,166 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_items_sparse(ItemsPass a) {
     }
   }
   if (pend != kNone) finish_tile(pend, pend_total, pend_n, q_idx, q_info, q_a, q_b, q_off, q_row);
+}
+
+// One-pass build of one direction (one partition per context, or a naive
+// plan): persistent blocks take 2048-position tiles round-robin (tile =
+// block + k * grid); a thread evaluates the windows of its 8 striped
+// positions once, the tile's counts are scanned in position order, and the
+// tile's aggregate is published at once.  The item and row-offset writes are
+// DEFERRED by one tile (per-position masks, counts, offsets and rows parked
+// in shared memory): the block resolves the look-back of its previous tile
+// -- whose predecessors published long ago -- and writes it while the next
+// tile is in flight, instead of waiting for the slowest tile of the wave.
+constexpr uint32_t kDeferWords = 5 * kTilePos;  // deferred tile: mA, mB, info, offset, row
+
+__global__ void __launch_bounds__(kTileThreads, 2) k_items_onepass(ItemsPass a) {
+  extern __shared__ __align__(16) uint32_t sx[];
+  uint32_t* lut = sx + a.Jp;
+  uint32_t* d_a = lut + (1u << kLutBits) + 1;  // striped position index i * 256 + tid
+  uint32_t* d_b = d_a + kTilePos;
+  uint32_t* d_info = d_b + kTilePos;  // b0 << 24 | nb << 16 | count
+  uint32_t* d_off = d_info + kTilePos;
+  uint32_t* d_row = d_off + kTilePos;
+  using BlockScan = cub::BlockScan<uint32_t, kTileThreads>;
+  using BlockExch = cub::BlockExchange<uint32_t, kTileThreads, kPosPerThread>;
+  __shared__ union {
+    typename BlockScan::TempStorage scan;
+    typename BlockExch::TempStorage exch;
+  } tmp;
+  __shared__ unsigned long long s_prefix, s_lb_sum;
+  __shared__ unsigned int s_lb_first;
+  for (uint32_t i = threadIdx.x; i < a.Jp; i += blockDim.x) sx[i] = a.x[i];
+  if (a.fasst)
+    for (uint32_t k = threadIdx.x; k <= (1u << kLutBits); k += blockDim.x) lut[k] = a.glut[k];
+  const uint64_t ntiles = (a.npos + kTilePos - 1) / kTilePos;
+  __syncthreads();
+  // look-back of tile t (aggregate already published), then its writes
+  auto finish_tile = [&](uint64_t t, uint32_t total) {
+    lookback_resolve(a.tile_state, t, total, s_prefix, s_lb_sum, s_lb_first);
+    const unsigned long long prefix = s_prefix;
+    if (threadIdx.x == 0 && t + 1 == ntiles) a.meta[0] = prefix + total;
+    const uint64_t pbase = t * kTilePos + threadIdx.x;
+    uint32_t othv[kPosPerThread];
+#pragma unroll
+    for (int i = 0; i < kPosPerThread; ++i) {  // every position's other endpoint in flight
+      const uint32_t k = i * kTileThreads + threadIdx.x;
+      const uint64_t p = pbase + uint64_t(i) * kTileThreads;
+      othv[i] = (p < a.npos && (d_info[k] & 0xFFFFu)) ? __ldcs(a.p_other + p) : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < kPosPerThread; ++i) {
+      const uint32_t k = i * kTileThreads + threadIdx.x;
+      const uint64_t p = pbase + uint64_t(i) * kTileThreads;
+      if (p >= a.npos) continue;
+      const uint32_t row = d_row[k], info = d_info[k], c = info & 0xFFFFu;
+      uint64_t o = prefix + d_off[k];
+      // rows (prev_row, row] start at this position (rows without edges share it)
+      const uint32_t prev = k ? d_row[k - 1] : (p ? __ldcs(a.p_row + p - 1) : 0xFFFFFFFFu);
+      for (uint32_t r = prev + 1; r <= row; ++r) a.row_off[r] = o;
+      if (p + 1 == a.npos)  // rows after the last edge's row end at the total
+        for (uint32_t r = row + 1; r <= a.n; ++r) a.row_off[r] = o + c;
+      if (!c) continue;
+      const uint32_t other = othv[i];
+      const uint32_t b0 = info >> 24, nb = (info >> 16) & 0xFFu;
+      auto emit = [&](uint32_t b, uint32_t mk) {
+        if (!mk) return;
+        if (o < a.cap) {
+          a.it_other[o] = other;
+          a.it_row[o] = row;
+          a.it_mask[o] = mk;
+          a.it_batch[o] = uint8_t(b);
+        }
+        ++o;
+      };
+      emit(b0, d_a[k]);
+      if (nb >= 2) emit(b0 + 1, d_b[k]);
+      if (nb > 2) {  // wide window: re-evaluate the remaining batches
+        const uint32_t h = a.p_hash[p], W = a.p_w ? a.p_w[p] : a.Wc;
+        uint32_t lo, hi, alo, ahi;
+        edge_window(sx, lut, a.J, h, W, a.fasst, lo, hi, alo, ahi);
+        for (uint32_t b = b0 + 2; b <= (hi - 1) >> 5; ++b)
+          emit(b, window_batch_mask(sx, h, W, lo, hi, alo, ahi, b));
+      }
+    }
+    __syncthreads();  // deferred buffers reusable
+  };
+  constexpr uint64_t kNone = ~0ull;
+  uint64_t pend = kNone;
+  uint32_t pend_total = 0;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    // striped positions: step i covers kTileThreads consecutive positions
+    // (coalesced loads, and consecutive lanes write consecutive items)
+    const uint64_t pbase = tile * kTilePos + threadIdx.x;
+    // ---- phase 1: windows, counts, masks of the first two batches
+    uint32_t mA[kPosPerThread], mB[kPosPerThread], info[kPosPerThread];
+    uint32_t cnt[kPosPerThread];
+    uint32_t live = 0;
+    // every position's hash and weight in flight together
+    uint32_t hv[kPosPerThread], wv[kPosPerThread];
+#pragma unroll
+    for (int i = 0; i < kPosPerThread; ++i) {
+      const uint64_t p = pbase + uint64_t(i) * kTileThreads;
+      const bool ok = p < a.npos;
+      wv[i] = ok ? (a.p_w ? __ldcs(a.p_w + p) : a.Wc) : 0u;
+      hv[i] = ok ? __ldcs(a.p_hash + p) : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < kPosPerThread; ++i) {
+      mA[i] = mB[i] = 0;
+      info[i] = 0;
+      cnt[i] = 0;
+      const uint32_t W = wv[i], h = hv[i];
+      if (W == 0) continue;  // fasst.cpp:71 (and past the end)
+      uint32_t lo, hi, alo, ahi;
+      edge_window(sx, lut, a.J, h, W, a.fasst, lo, hi, alo, ahi);
+      if (hi <= lo) continue;
+      const uint32_t b0 = lo >> 5, b1 = (hi - 1) >> 5, nb = b1 - b0 + 1;
+      uint32_t c = 0;
+      for (uint32_t b = b0; b <= b1; ++b) {
+        const uint32_t mk = window_batch_mask(sx, h, W, lo, hi, alo, ahi, b);
+        if (b == b0) mA[i] = mk;
+        else if (b == b0 + 1) mB[i] = mk;
+        c += mk != 0;
+        live += __popc(mk);
+      }
+      info[i] = (b0 << 24) | (min(nb, 255u) << 16) | c;
+      cnt[i] = c;
+    }
+    // rows of all 8 positions in flight while the tile is scanned
+    uint32_t rowv[kPosPerThread];
+#pragma unroll
+    for (int i = 0; i < kPosPerThread; ++i) {
+      const uint64_t p = pbase + uint64_t(i) * kTileThreads;
+      rowv[i] = p < a.npos ? __ldcs(a.p_row + p) : 0u;
+    }
+    // ---- tile scan in position order (striped -> blocked -> striped)
+    BlockExch(tmp.exch).StripedToBlocked(cnt);
+    __syncthreads();
+    uint32_t tile_total;
+    BlockScan(tmp.scan).ExclusiveSum(cnt, cnt, tile_total);
+    __syncthreads();
+    BlockExch(tmp.exch).BlockedToStriped(cnt);
+    if (threadIdx.x == 0) __stcg(a.tile_state + tile, (tile == 0 ? kStInc : kStAgg) | tile_total);
+    for (int o = 16; o; o >>= 1) live += __shfl_xor_sync(0xffffffffu, live, o);
+    if (lane_id() == 0 && live) atomicAdd(&a.meta[1], (unsigned long long)live);
+    __syncthreads();
+    // ---- the previous tile's writes, then park this one
+    if (pend != kNone) finish_tile(pend, pend_total);
+#pragma unroll
+    for (int i = 0; i < kPosPerThread; ++i) {
+      const uint32_t k = i * kTileThreads + threadIdx.x;
+      d_a[k] = mA[i];
+      d_b[k] = mB[i];
+      d_info[k] = info[i];
+      d_off[k] = cnt[i];
+      d_row[k] = rowv[i];
+    }
+    pend = tile;
+    pend_total = tile_total;
+    __syncthreads();
+  }
+  if (pend != kNone) finish_tile(pend, pend_total);
 }
 
 // Item count of every stride-th position (capacity estimate of a one-pass
@@ -3656,8 +3633,7 @@ static ItemsPass items_pass_args(const DevGraph& g, const uint32_t* w, const uin
 static size_t items_smem(const RankDev& r) {
   static bool attr = false;
   if (!attr) {
-    DFS_CUDA(cudaFuncSetAttribute(k_items_onepass<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
-    DFS_CUDA(cudaFuncSetAttribute(k_items_onepass<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
+    DFS_CUDA(cudaFuncSetAttribute(k_items_onepass, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 << 10));
     DFS_CUDA(cudaFuncSetAttribute(k_items_sparse, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10));
     DFS_CUDA(cudaFuncSetAttribute(k_items_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
     attr = true;
@@ -3694,11 +3670,7 @@ void launch_items_onepass(const DevGraph& g, const uint32_t* w, const uint32_t* 
   a.meta = meta;
   const size_t smem = items_smem(r);
   const bool filter = row_cnt != nullptr;
-  int per = 0;
-  DFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &per, filter ? k_items_onepass<1> : k_items_onepass<0>, kTileThreads, smem));
   const uint64_t tiles = items_tiles(g.m);
-  const int grid = int(std::min<uint64_t>(tiles, uint64_t(std::max(per, 1)) * num_sms()));
   if (filter) {
     int ps = 0;
     const size_t ssm = smem + sparse_extra_smem();
@@ -3706,7 +3678,11 @@ void launch_items_onepass(const DevGraph& g, const uint32_t* w, const uint32_t* 
     const int gs = int(std::min<uint64_t>(tiles, uint64_t(std::max(ps, 1)) * num_sms()));
     k_items_sparse<<<gs, kTileThreads, ssm, s>>>(a);
   } else {
-    k_items_onepass<0><<<grid, kTileThreads, smem, s>>>(a);
+    int per = 0;
+    const size_t dsm = smem + size_t(kDeferWords) * sizeof(uint32_t);
+    DFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_items_onepass, kTileThreads, dsm));
+    const int grid = int(std::min<uint64_t>(tiles, uint64_t(std::max(per, 1)) * num_sms()));
+    k_items_onepass<<<grid, kTileThreads, dsm, s>>>(a);
   }
   DFS_CUDA(cudaGetLastError());
   ++g_launches;
