@@ -2243,12 +2243,14 @@ __device__ __forceinline__ void score_body(const int8_t* __restrict__ regs, uint
   const uint64_t nw = block_only ? kWarps : (uint64_t(gridDim.x) * blockDim.x) >> 5;
   const uint64_t gw = block_only ? threadIdx.x >> 5
                                  : (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  // G lanes per row (power of two <= the row's 16-byte words), R rows per
-  // warp, two row groups per step: every lane keeps up to 8 independent
-  // 16-byte loads in flight before reducing (the score is a streaming pass).
+  // G lanes per row (power of two, at most a quarter of the row's 16-byte
+  // words), R rows per warp, two row groups per step: every lane keeps 8
+  // independent 16-byte loads in flight before reducing (the score is a
+  // streaming pass; with G up to the row's word count, J = 1024 rows left half
+  // and J = 256 rows three quarters of the slots empty).
   const uint32_t q16 = Jp >> 4;
   uint32_t G = 32;
-  while (G > q16) G >>= 1;
+  while (G > 1 && 4 * G > q16) G >>= 1;
   const uint32_t R = 32 / G, sub = lane / G, sl = lane % G;
   const uint4 kDead = make_uint4(0u, 0u, 0u, 0u);  // all VISITED
   for (uint64_t k0 = gw * 2 * R; k0 < nrows; k0 += nw * 2 * R) {
@@ -2267,10 +2269,11 @@ __device__ __forceinline__ void score_body(const int8_t* __restrict__ regs, uint
       for (int h = 0; h < 2; ++h) {
         const uint4* rp = reinterpret_cast<const uint4*>(regs + uint64_t(u[h]) * Jp);
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {  // unconditional (clamped) loads: all 8 in flight
+        for (int t = 0; t < 4; ++t) {  // all live loads in flight together
+          // (idx < q16 is warp-uniform: q16 is a multiple of G)
           const uint32_t idx = w0 + t * G;
-          va[h][t] = ld_stream_early(rp + (idx < q16 ? idx : q16 - 1));
-          if (!ok[h] || idx >= q16) va[h][t] = kDead;
+          va[h][t] = idx < q16 ? ld_stream_early(rp + idx) : kDead;
+          if (!ok[h]) va[h][t] = kDead;
         }
       }
 #pragma unroll
@@ -2280,7 +2283,8 @@ __device__ __forceinline__ void score_body(const int8_t* __restrict__ regs, uint
 #pragma unroll
       for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int t = 0; t < 4; ++t) score_acc(va[h][t], tbl, live[h], den[h]);
+        for (int t = 0; t < 4; ++t)
+          if (w0 - sl + t * G < q16) score_acc(va[h][t], tbl, live[h], den[h]);
     }
     for (uint32_t o = G >> 1; o; o >>= 1) {
 #pragma unroll
