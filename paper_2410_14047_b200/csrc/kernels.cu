@@ -1238,11 +1238,12 @@ __device__ __forceinline__ void fill_body(uint32_t n, uint32_t J, uint32_t Jp,
   const uint32_t W32 = Jp >> 5;
   const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   if (use_pristine && pristine) {
-    // Streaming copy (16-byte vectors, G lanes per row, 4 loads in flight
-    // per lane) with the VISITED bits re-applied.
+    // Streaming copy (16-byte vectors, G lanes per row — at most a quarter of
+    // the row's words, so every lane has 4 loads in flight) with the VISITED
+    // bits re-applied.
     const uint32_t q16 = Jp >> 4;
     uint32_t G = 32;
-    while (G > q16) G >>= 1;
+    while (G > 1 && 4 * G > q16) G >>= 1;
     const uint32_t R = 32 / G, lane = lane_id(), sub = lane / G, sl = lane % G;
     const uint64_t gw = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     for (uint64_t u0 = gw * R; u0 < n; u0 += nw * R) {
