@@ -2529,13 +2529,21 @@ struct CasArgs {
   int pull_f;  // bottom-up when frontier chunks * pull_f > total (DFS_CAS_PULL, default 8)
 };
 
-// Clear the fresh bits of the rows listed in one generation.
+// Clear the fresh bits of the rows listed in one generation.  A warp takes 32
+// listed rows at a time (one coalesced load of their ids, then 32 rows of
+// independent stores): one row per warp iteration made every row a dependent
+// id load -> store round trip, ~0.4 ms per million-row level.
 __device__ __forceinline__ void clear_rows(uint32_t* f, const uint32_t* rows, unsigned nr,
                                            uint32_t W32, uint64_t gwarp, uint64_t nw,
                                            unsigned lane) {
-  for (uint64_t k = gwarp; k < nr; k += nw) {
-    const uint64_t row = uint64_t(__ldcg(rows + k)) * W32;
-    for (uint32_t w = lane; w < W32; w += 32) f[row + w] = 0;
+  for (uint64_t k0 = gwarp * 32; k0 < nr; k0 += nw * 32) {
+    const uint64_t k = k0 + lane;
+    const uint32_t mine = k < nr ? __ldcg(rows + k) : 0u;
+    const uint32_t cnt = nr - k0 < 32 ? uint32_t(nr - k0) : 32u;
+    for (uint32_t j = 0; j < cnt; ++j) {
+      const uint64_t row = uint64_t(__shfl_sync(0xffffffffu, mine, j)) * W32;
+      for (uint32_t w = lane; w < W32; w += 32) f[row + w] = 0;
+    }
   }
 }
 
