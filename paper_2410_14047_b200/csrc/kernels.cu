@@ -2709,6 +2709,12 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
       // a shared accumulator, then claims the unvisited ones with one update
       // per batch word (direction-optimising BFS, Beamer et al.).
       const uint64_t nbig = r.rev.nbig;
+      // Parents' bits: the live VISITED bitset, read in place, instead of the
+      // level's fresh bits (count mode keeps the reference's level structure).
+      // VISITED is closed under live edges after every cascade, so a parent's
+      // older bits add no candidate, and bits a parent gained earlier in THIS
+      // level propagate at once (fewer bottom-up levels; same closure).
+      const uint32_t* fpar = CNT ? fcur : r.vis;
       uint32_t c_nx = my_warp < nbig ? r.rev.big[my_warp] : 0;  // one iteration ahead (| owner flag)
       for (uint64_t k = my_warp; k < nbig; k += n_warps) {
         __syncwarp();
@@ -2744,7 +2750,7 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          fq[q] = mq[q] ? __ldcg(fcur + uint64_t(uq[q]) * W32 + bq[q]) & mq[q] : 0;
+          fq[q] = mq[q] ? __ldcg(fpar + uint64_t(uq[q]) * W32 + bq[q]) & mq[q] : 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           if (fq[q]) {
@@ -2807,7 +2813,7 @@ __device__ __forceinline__ uint32_t cascade_body(const RankDev& r, const CasOpts
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           xq[q] = mq[q] ? __ldcg(r.vis + uint64_t(vq[q]) * W32 + bq[q]) : 0xFFFFFFFFu;
-          fq[q] = mq[q] ? __ldcg(fcur + uint64_t(uq[q]) * W32 + bq[q]) : 0;
+          fq[q] = mq[q] ? __ldcg(fpar + uint64_t(uq[q]) * W32 + bq[q]) : 0;
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
