@@ -642,11 +642,15 @@ Report Context::run_impl(const RunConfig& cfg, const HostGraph* host_w_src, bool
   // When sweeps / cascade levels switch to pull (frontier chunks * f > all
   // chunks): dense items (many live simulations each, e.g. weighted cascade)
   // make full pull passes pay off earlier (A/B: C3 simulate -19%, cascade
-  // -21%; sparse IC items keep the later switch).  DFS_SIM_PULL /
-  // DFS_CAS_PULL override.
+  // -21%; sparse IC items keep the later switch).  Since the bottom-up
+  // cascade levels propagate in place (bits gained in a level spread within
+  // it), mid-density items (IC at R = 1024: the north star, density 7.5) gain
+  // from an EARLIER bottom-up switch (cascade 11.7 -> 10.4 ms at f = 16),
+  // while C3 (density 19) keeps f = 4 and C2 (2.7) f = 8 (A/B over
+  // f = 4, 8, 16, 32).  DFS_SIM_PULL / DFS_CAS_PULL override.
   const double density = ranks_[0].fwd.count ? double(ranks_[0].fwd.live) / ranks_[0].fwd.count : 0;
   const int pull_sim = density >= 10.0 ? 1 : density >= 6.0 ? 2 : 4;
-  const int pull_cas = density >= 6.0 ? 4 : 8;
+  const int pull_cas = density >= 10.0 ? 4 : density >= 6.0 ? 16 : 8;
   static const bool multi_env =
       getenv("DFS_RUN_MODE") && std::string(getenv("DFS_RUN_MODE")) == "launches";
   const bool multi = multi_env && !peer;  // peer mode exchanges inside k_run only
