@@ -1223,6 +1223,23 @@ __global__ void __launch_bounds__(1024, 1) k_mc_bfs(McBfs a) {
 __device__ __forceinline__ uint32_t expand4(uint32_t m4) {
   return ((m4 * 0x00204081u) & 0x01010101u) * 0xFFu;
 }
+// clz64(fmix64(k)) (hash.hpp:9-16) on 32-bit halves with only the words the
+// count needs: the final k ^= k >> 33 never moves the leading one (bits
+// 31..63 are unchanged by it, and below 2^31 it is the identity), so the count
+// is that of the second product, whose high word is hi*Clo + lo*Chi +
+// umulhi(lo, Clo); its low word matters only when the high word is zero.
+__device__ __forceinline__ uint32_t clz_fmix64(uint64_t k) {
+  constexpr uint32_t c1lo = 0xed558ccdu, c1hi = 0xff51afd7u;
+  constexpr uint32_t c2lo = 0x1a85ec53u, c2hi = 0xc4ceb9feu;
+  uint32_t lo = uint32_t(k), hi = uint32_t(k >> 32);
+  lo ^= hi >> 1;                                             // k ^= k >> 33
+  const uint32_t lo2 = lo * c1lo;                            // k *= C1
+  const uint32_t hi2 = hi * c1lo + lo * c1hi + __umulhi(lo, c1lo);
+  const uint32_t lo3 = lo2 ^ (hi2 >> 1);                     // k ^= k >> 33
+  const uint32_t hi4 = hi2 * c2lo + lo3 * c2hi + __umulhi(lo3, c2lo);  // (k *= C2) >> 32
+  return hi4 ? uint32_t(__clz(hi4)) : 32u + uint32_t(__clz(lo3 * c2lo));
+}
+
 // sketch.cpp:55-66: M[u][j] = clz64(fmix64(jkey[j] + u*golden)) unless VISITED.
 // One thread per 4 registers (one u32 store, coalesced across the warp).
 // use_pristine: registers are the cached first fill with VISITED re-applied
@@ -1292,10 +1309,8 @@ __device__ __forceinline__ void fill_body(uint32_t n, uint32_t J, uint32_t Jp,
       const ulonglong2 k23 = __ldg(reinterpret_cast<const ulonglong2*>(jkey + j0 + 2));
       const uint32_t vb = (vis[u * W32 + (j0 >> 5)] >> (j0 & 31)) & 15u;
       // stored byte = register value + 1 (clz <= 64: no carry between bytes)
-      uint32_t pw = (uint32_t(__clzll(fmix64(k01.x + ug))) |
-                     (uint32_t(__clzll(fmix64(k01.y + ug))) << 8) |
-                     (uint32_t(__clzll(fmix64(k23.x + ug))) << 16) |
-                     (uint32_t(__clzll(fmix64(k23.y + ug))) << 24)) +
+      uint32_t pw = (clz_fmix64(k01.x + ug) | (clz_fmix64(k01.y + ug) << 8) |
+                     (clz_fmix64(k23.x + ug) << 16) | (clz_fmix64(k23.y + ug) << 24)) +
                     0x01010101u;
       if (j0 + 4 > J) {  // pad registers are VISITED (stored 0)
         const uint32_t live = J > j0 ? J - j0 : 0;  // < 4
