@@ -1237,7 +1237,19 @@ __device__ __forceinline__ uint32_t clz_fmix64(uint64_t k) {
   const uint32_t hi2 = hi * c1lo + lo * c1hi + __umulhi(lo, c1lo);
   const uint32_t lo3 = lo2 ^ (hi2 >> 1);                     // k ^= k >> 33
   const uint32_t hi4 = hi2 * c2lo + lo3 * c2hi + __umulhi(lo3, c2lo);  // (k *= C2) >> 32
-  return hi4 ? uint32_t(__clz(hi4)) : 32u + uint32_t(__clz(lo3 * c2lo));
+  if (__builtin_expect(hi4 != 0, 1)) return uint32_t(__clz(hi4));
+  return 32u + uint32_t(__clz(lo3 * c2lo));  // (probability 2^-32)
+}
+
+// 64-bit add on the integer ALU (add.cc / addc): written as a + b the
+// compiler folds it into the multiply-add pipe (IMAD.WIDE), which the hash's
+// multiplies already saturate.
+__device__ __forceinline__ uint64_t add64_alu(uint64_t a, uint64_t b) {
+  uint32_t lo, hi;
+  asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, %5;"
+      : "=r"(lo), "=r"(hi)
+      : "r"(uint32_t(a)), "r"(uint32_t(a >> 32)), "r"(uint32_t(b)), "r"(uint32_t(b >> 32)));
+  return (static_cast<uint64_t>(hi) << 32) | lo;
 }
 
 // sketch.cpp:55-66: M[u][j] = clz64(fmix64(jkey[j] + u*golden)) unless VISITED.
@@ -1309,9 +1321,13 @@ __device__ __forceinline__ void fill_body(uint32_t n, uint32_t J, uint32_t Jp,
       const ulonglong2 k23 = __ldg(reinterpret_cast<const ulonglong2*>(jkey + j0 + 2));
       const uint32_t vb = (vis[u * W32 + (j0 >> 5)] >> (j0 & 31)) & 15u;
       // stored byte = register value + 1 (clz <= 64: no carry between bytes)
-      uint32_t pw = (clz_fmix64(k01.x + ug) | (clz_fmix64(k01.y + ug) << 8) |
-                     (clz_fmix64(k23.x + ug) << 16) | (clz_fmix64(k23.y + ug) << 24)) +
-                    0x01010101u;
+      // four counts packed by byte permutes (ALU) rather than shifts the
+      // compiler would issue as IMAD.SHL on the busy multiply pipe
+      const uint32_t c01 = __byte_perm(clz_fmix64(add64_alu(k01.x, ug)),
+                                       clz_fmix64(add64_alu(k01.y, ug)), 0x1140);
+      const uint32_t c23 = __byte_perm(clz_fmix64(add64_alu(k23.x, ug)),
+                                       clz_fmix64(add64_alu(k23.y, ug)), 0x1140);
+      uint32_t pw = __byte_perm(c01, c23, 0x5410) + 0x01010101u;
       if (j0 + 4 > J) {  // pad registers are VISITED (stored 0)
         const uint32_t live = J > j0 ? J - j0 : 0;  // < 4
         pw &= ~(0xFFFFFFFFu << (8 * live));
