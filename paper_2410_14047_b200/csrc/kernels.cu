@@ -621,7 +621,11 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_items_sparse(ItemsPass a) {
 // tile is in flight, instead of waiting for the slowest tile of the wave.
 constexpr uint32_t kDeferWords = 5 * kTilePos;  // deferred tile: mA, mB, info, offset, row
 
-__global__ void __launch_bounds__(kTileThreads, 2) k_items_onepass(ItemsPass a) {
+// MINB blocks per SM: 3 for constant weights (one narrow window per edge:
+// C2 build 1.24 -> 1.10 ms, north star 7.9 -> 7.15 ms), 2 for per-edge weights
+// (wide weighted-cascade windows need the registers: C3 58 -> 62 ms at 3).
+template <int MINB>
+__global__ void __launch_bounds__(kTileThreads, MINB) k_items_onepass(ItemsPass a) {
   extern __shared__ __align__(16) uint32_t sx[];
   uint32_t* lut = sx + a.Jp;
   uint32_t* d_a = lut + (1u << kLutBits) + 1;  // striped position index i * 256 + tid
@@ -3683,7 +3687,8 @@ static ItemsPass items_pass_args(const DevGraph& g, const uint32_t* w, const uin
 static size_t items_smem(const RankDev& r) {
   static bool attr = false;
   if (!attr) {
-    DFS_CUDA(cudaFuncSetAttribute(k_items_onepass, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 << 10));
+    DFS_CUDA(cudaFuncSetAttribute(k_items_onepass<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 << 10));
+    DFS_CUDA(cudaFuncSetAttribute(k_items_onepass<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 << 10));
     DFS_CUDA(cudaFuncSetAttribute(k_items_sparse, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10));
     DFS_CUDA(cudaFuncSetAttribute(k_items_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 << 10));
     attr = true;
@@ -3730,9 +3735,11 @@ void launch_items_onepass(const DevGraph& g, const uint32_t* w, const uint32_t* 
   } else {
     int per = 0;
     const size_t dsm = smem + size_t(kDeferWords) * sizeof(uint32_t);
-    DFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_items_onepass, kTileThreads, dsm));
+    const void* fn = wconst ? (const void*)k_items_onepass<3> : (const void*)k_items_onepass<2>;
+    DFS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kTileThreads, dsm));
     const int grid = int(std::min<uint64_t>(tiles, uint64_t(std::max(per, 1)) * num_sms()));
-    k_items_onepass<<<grid, kTileThreads, dsm, s>>>(a);
+    if (wconst) k_items_onepass<3><<<grid, kTileThreads, dsm, s>>>(a);
+    else k_items_onepass<2><<<grid, kTileThreads, dsm, s>>>(a);
   }
   DFS_CUDA(cudaGetLastError());
   ++g_launches;
